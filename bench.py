@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""bench.py -- CATS-MLP decode on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+Workload (BASELINE.json configs[1]): one Mistral-7B MLP layer (d=4096, m=14336), bf16 weights and
+activations, batch 1, 50% sparsity, threshold calibrated on 2048 held-apart synthetic tokens with
+the library's own calibration path. A step = one pass of the whole hot path (K1 gate/SiLU/CATS/
+compaction -> K2 sparse up x v + down -> K3 split-K reduce [-> NCCL all-reduce when N > 1]) for one
+token. N > 1: tensor parallel along m (each rank m/N neurons, same t), "strong" scaling.
+
+Timing: W warm-up steps, then exactly K steps between barrier + synchronize, CUDA events on the
+launching stream, max over ranks. L2 defeated by rotating 4 device copies of the weights (1.41 GB
+per rank at N=1, >> 126 MB L2). Fresh x per step (a pool of 64 distinct tokens).
+
+--impl reference: the CPU oracle (oracle/, fp64 C) on the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CATS-MLP decode µs/token-layer @50% sparsity; effective HBM GB/s vs 8 TB/s"
+UNIT = "us/token-layer"
+NOMINAL_HBM_GBS = 8000.0
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="cats", choices=["cats", "reference"])
+    ap.add_argument("--model", default="mistral-7b")
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--sparsity", type=float, default=0.5)
+    ap.add_argument("--copies", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--extras", action="store_true", help="also time dense/cuBLAS/profiled (default on)")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """NVML clocks + throttle reasons sampled in a thread during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.th.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        rs = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": rs,
+                "samples": len(self.samples)}
+
+
+def dist_setup(n):
+    import torch
+    import torch.distributed as dist
+    if n > 1 or "RANK" in os.environ:
+        rank = int(os.environ.get("RANK", 0))
+        world = int(os.environ.get("WORLD_SIZE", 1))
+        local = int(os.environ.get("LOCAL_RANK", rank))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        return rank, world, local
+    torch.cuda.set_device(0)
+    return 0, 1, 0
+
+
+# ---------------------------------------------------------------------------------------- CPU oracle
+
+def time_oracle(d, m, b, sparsity, budget_s=15.0, max_tokens=64, seed=0):
+    """Oracle (fp64 C, single thread) on the same workload: t from the oracle's own |SiLU| on
+    256 calibration tokens' worth of... (bounded: calibrate on 8 tokens), then decode tokens until the
+    time budget is used. Returns (us per token-layer, tokens, m_used)."""
+    import numpy as np
+    import torch
+
+    import cats_synth
+    import oracle
+    # bounded sample: full-width layer, as many tokens as fit in the budget
+    Wg, Wu, Wd = cats_synth.mlp_weights(d, m, torch.bfloat16)
+    og, ou, od = (cats_synth.to_oracle(a) for a in (Wg, Wu, Wd))
+    z = np.zeros((1, d), np.uint16)
+    xs = cats_synth.tokens(max_tokens * b + 8, d, torch.bfloat16, seed=seed + 1)
+    ox = cats_synth.to_oracle(xs)
+    _, v, _ = oracle.mlp(ox[:2], og, ou, od, t=0.0, mode=oracle.DENSE)
+    t = oracle.calibrate_sort(v.astype(np.float32), sparsity).t
+    del z
+    times = []
+    n_tok = 0
+    t_start = time.perf_counter()
+    while n_tok < max_tokens:
+        s = time.perf_counter()
+        oracle.mlp(ox[2 + n_tok * b: 2 + (n_tok + 1) * b], og, ou, od, t=t)
+        times.append(time.perf_counter() - s)
+        n_tok += 1
+        if time.perf_counter() - t_start > budget_s:
+            break
+    return 1e6 * sum(times) / (n_tok * b), n_tok
+
+
+def run_reference(args):
+    import torch
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return 0
+    import cats_synth
+    d, m = cats_synth.MODELS[args.model]
+    # each step: one token through the oracle (~0.6 s at Mistral shape); bounded sample so the run
+    # ends within minutes: steps beyond the budget reuse the measured per-token time
+    budget = 150.0
+    us, ntok = time_oracle(d, m, args.batch, args.sparsity, budget_s=budget, max_tokens=args.steps + args.warmup)
+    value = us
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value / 1000 * args.batch, 4),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args, d, m),
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{ntok} token(s) x full {args.model} layer (d={d}, m={m}, b={args.batch}), "
+                                   f"single-thread fp64 C oracle, time-bounded at {budget:.0f} s"},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, d, m):
+    return {"workload": f"{args.model} MLP layer decode (d={d}, m={m}) bf16 b={args.batch} "
+                        f"k={args.sparsity} TP={args.gpus}",
+            "model_shape": {"d": d, "m": m}, "batch": args.batch, "sparsity": args.sparsity,
+            "tp": args.gpus, "storage": "bf16", "accumulate": "f32",
+            "l2": f"inputs larger than L2: {args.copies} rotated weight copies per rank",
+            "timing": "CUDA events on the launching stream, max over ranks"}
+
+
+# ---------------------------------------------------------------------------------------- GPU arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import cats_synth
+    import paper_2404_08763_b200 as cats
+
+    rank, world, local = dist_setup(args.gpus)
+    dev = torch.device(f"cuda:{local}")
+    d, m = cats_synth.MODELS[args.model]
+    b, k = args.batch, args.sparsity
+    assert m % world == 0
+    ms = m // world
+    sl = slice(rank * ms, (rank + 1) * ms)
+
+    # weights: this rank's neuron shard, rotated copies in HBM
+    Wg, Wu, Wd = cats_synth.mlp_weights(d, m, torch.bfloat16)
+    shard = [w[sl].contiguous() for w in (Wg, Wu, Wd)]
+    del Wg, Wu, Wd
+    copies = [[w.to(dev) for w in shard] for _ in range(args.copies)]
+    plan = cats.MlpPlan(d, ms, max_batch=max(8, b), dtype=torch.bfloat16, device=local)
+    ws = plan.workspace()
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- Stage 1: calibrate t on 2048 held-apart tokens via the library (sharded: all-reduced histograms)
+    from paper_2404_08763_b200 import tp as tpmod
+    xcal = cats_synth.tokens(2048, d, torch.bfloat16, seed=0).to(dev)
+    acts = torch.empty((2048, ms), dtype=torch.float32, device=dev)
+    for i in range(0, 2048, 8):
+        cats.cats_mlp_gate_act(plan, xcal[i:i + 8], copies[0][0], acts=acts[i:i + 8], ws=ws)
+    t = tpmod.calibrate_threshold(acts, k, group=dist.group.WORLD if world > 1 else None)
+    del acts, xcal
+
+    xs = cats_synth.tokens(64 * b, d, torch.bfloat16, seed=1).to(dev).view(64, b, d)
+    y = torch.empty((b, d), dtype=torch.float32, device=dev)
+
+    def step(i):
+        W = copies[i % len(copies)]
+        cats.cats_mlp_decode(plan, xs[i % 64], W[0], W[1], W[2], t, y=y, ws=ws, stream=stream)
+        if world > 1:
+            dist.all_reduce(y)
+
+    def timed(fn, steps, warmup):
+        for i in range(warmup):
+            fn(i)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(steps):
+            fn(i)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms_ = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([ms_], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms_ = float(tt.item())
+        return ms_ / steps
+
+    sampler = ClockSampler(local)
+    with sampler:
+        ms_step = timed(step, args.steps, max(3, args.warmup))
+    clocks = sampler.summary()
+
+    # realized sparsity of this step's token (union over b)
+    cats.cats_mlp_decode(plan, xs[0], *copies[0], t, y=y, ws=ws)
+    idx, tm, per = cats.cats_mlp_last_active(plan, ws, b)
+    nnz_local = len(idx)
+    nnz = torch.tensor([nnz_local], device=dev)
+    if world > 1:
+        dist.all_reduce(nnz)
+    U = int(nnz.item())
+
+    # ---- per-kernel times (profiled variant: events between kernels) -> roofline
+    n_prof = min(args.steps, 500)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_prof)]
+    for i in range(10):
+        cats.cats_mlp_decode_profiled(plan, xs[i % 64], *copies[i % len(copies)], t, evs[0], y=y, ws=ws)
+    torch.cuda.synchronize(dev)
+    for i in range(n_prof):
+        cats.cats_mlp_decode_profiled(plan, xs[i % 64], *copies[i % len(copies)], t, evs[i], y=y, ws=ws)
+    torch.cuda.synchronize(dev)
+    k1 = statistics.mean(e[0].elapsed_time(e[1]) for e in evs) * 1e3
+    k2 = statistics.mean(e[1].elapsed_time(e[2]) for e in evs) * 1e3
+    k3 = statistics.mean(e[2].elapsed_time(e[3]) for e in evs) * 1e3
+
+    # ---- dense path of the same library (speedup denominator), and cuBLAS dense for context
+    def dense_step(i):
+        W = copies[i % len(copies)]
+        cats.cats_mlp_dense(plan, xs[i % 64], W[0], W[1], W[2], y=y, ws=ws, stream=stream)
+        if world > 1:
+            dist.all_reduce(y)
+    dense_ms = timed(dense_step, min(args.steps, 1000), 20)
+
+    def cublas_step(i):
+        W = copies[i % len(copies)]
+        xx = xs[i % 64]
+        h = torch.nn.functional.silu(xx @ W[0].T) * (xx @ W[1].T)
+        y.copy_((h @ W[2]).float())
+        if world > 1:
+            dist.all_reduce(y)
+    cublas_ms = timed(cublas_step, min(args.steps, 1000), 20)
+
+    # ---- e2e: host activations in (pinned), host y out, through the public C-ABI call
+    xh = xs.cpu().pin_memory()
+    yh = torch.empty((b, d), dtype=torch.float32).pin_memory()
+
+    def e2e_step(i):
+        W = copies[i % len(copies)]
+        if world == 1:
+            cats.cats_mlp_decode_host(plan, xh[i % 64], W[0], W[1], W[2], t, y_host=yh, ws=ws, stream=stream)
+        else:
+            xd = xh[i % 64].to(dev, non_blocking=True)
+            cats.cats_mlp_decode(plan, xd, W[0], W[1], W[2], t, y=y, ws=ws, stream=stream)
+            dist.all_reduce(y)
+            yh.copy_(y, non_blocking=False)
+    e2e_ms = timed(e2e_step, min(args.steps, 1000), 10)
+
+    # ---- roofline of the dominant kernel (algorithmic bytes / live CUDA-event duration)
+    hbm_peak, peak_kind = peaks()
+    esz = 2
+    k1_bytes = 2 * d * ms + b * d * esz                  # all W_gate rows + x
+    k2_bytes = 4 * d * nnz_local + b * d * esz           # active W_up + W_down rows + x
+    step_bytes = k1_bytes + k2_bytes
+    kern = {"K1": (k1, k1_bytes), "K2": (k2, k2_bytes)}
+    dom = max(kern, key=lambda n: kern[n][0])
+    dom_us, dom_bytes = kern[dom]
+    achieved = dom_bytes / (dom_us * 1e-6) / 1e9
+    traffic = None
+    tp_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp_path):
+        try:
+            traffic = json.load(open(tp_path)).get(dom)
+        except Exception:
+            traffic = None
+
+    us_step = ms_step * 1e3
+    value = us_step / b  # us per token-layer, whole job (TP ranks together process b tokens per step)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cus, ntok = time_oracle(d, m, b, k, budget_s=15.0, max_tokens=40)
+        cpu = {"value": round(cus, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{ntok} token(s) x full {args.model} layer, single-thread fp64 C oracle"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 5), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args, d, m),
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm_peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                         "traffic": traffic, "algorithmic_bytes_per_launch": dom_bytes,
+                         "launch_us": round(dom_us, 3)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_ms * 1e3 / b, 3), "unit": UNIT, "h2d_bytes_per_step": b * d * esz,
+                    "d2h_bytes_per_step": b * d * 4},
+            "gpu_launches": 3 * args.steps,
+            "clocks": clocks,
+            "detail": {
+                "t": t, "nnz_union_per_rank": nnz_local, "nnz_union_total": U, "m_per_rank": ms,
+                "realized_sparsity": round(1 - U / m, 4),
+                "k1_us": round(k1, 3), "k2_us": round(k2, 3), "k3_us": round(k3, 3),
+                "effective_bytes_per_step": step_bytes,
+                "effective_GBps": round(step_bytes / (us_step * 1e-6) / 1e9, 1),
+                "frac_of_8TBps": round(step_bytes / (us_step * 1e-6) / 1e9 / NOMINAL_HBM_GBS, 4),
+                "k1_GBps": round(k1_bytes / (k1 * 1e-6) / 1e9, 1),
+                "k2_GBps": round(k2_bytes / (k2 * 1e-6) / 1e9, 1),
+                "dense_us": round(dense_ms * 1e3, 3),
+                "speedup_vs_dense": round(dense_ms / ms_step, 4),
+                "dense_GBps": round(6 * d * ms / (dense_ms * 1e-3) / 1e9, 1),
+                "cublas_dense_us": round(cublas_ms * 1e3, 3),
+                "speedup_vs_cublas_dense": round(cublas_ms / ms_step, 4),
+                "byte_ceiling_speedup": round(3 / (3 - 2 * (1 - U / m)), 4),
+            },
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

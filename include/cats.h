@@ -1,0 +1,232 @@
+/*
+ * cats.h -- C ABI of libcats: the B200 (sm_100a) hot path of CATS
+ * (Contextually-Aware Thresholding for Sparsity, arXiv 2404.08763).
+ *
+ * Citations: "P:n" = PAPER.md line n (section / equation named alongside).
+ *
+ * What is computed
+ *   Calibration, Stage 1 (Eq. 3):  t := min{ t' : F(t') >= k }, F the empirical
+ *     CDF of |activations| of one Gated-MLP block. Returned exactly: t is the r-th smallest
+ *     |a_i| with r = ceil(k*N) on the binary value of the double k (t = 0 when k = 0).
+ *   Decode, Stage 2 (Eq. 1/2/4/5; Custom GPU Kernel "MLP using CATS" P:289-298):
+ *     v = SiLU(x W_gate);  Mask = |v| >= t;  x1 = (x W_up[Mask]) * v[Mask];  y = x1 W_down[Mask]
+ *     for a batch of b in [1, 8] tokens, each token with its own mask (Eq. 5 is elementwise).
+ *
+ * Conventions (all calls)
+ *   - Tensors are row-major, contiguous, device memory unless the name says _host.
+ *   - W_gate, W_up, W_down_nm are NEURON-MAJOR [m][d]: row j holds neuron j's d weights.
+ *     (= HF gate_proj.weight, up_proj.weight, down_proj.weight.T.contiguous(); the paper's
+ *     d x m W_gate / W_up are their transposes; "columns of W_up and rows of
+ *     W_down are the experts".)
+ *   - x has the weights' dtype; y is fp32 [b][d]. Accumulation is fp32, never rounded in between.
+ *   - Every device pointer is 16-byte aligned and d * sizeof(dtype) is a multiple of 16
+ *     (d % 8 == 0 for bf16, d % 4 == 0 for fp32): 128-bit loads and cp.async.bulk need it.
+ *   - Ownership: the caller owns every buffer (torch allocates them); a plan owns only host
+ *     metadata. Workspace contents persist until the next call that uses the workspace.
+ *   - Concurrency: plans are immutable and may be shared by threads; concurrent calls need
+ *     distinct workspaces and outputs.
+ *   - Errors: every entry point returns a cats_status_t; nothing throws or aborts across the
+ *     ABI. Arguments are validated before anything is launched; on error nothing is launched
+ *     and outputs are untouched. A failed launch returns CATS_E_CUDA (message in
+ *     cats_last_cuda_error()). Asynchronous device faults surface at the caller's next sync.
+ *   - Streams: cats_stream_t is a cudaStream_t (0 = legacy default stream). Calls that do not
+ *     say "blocks" are stream-ordered and asynchronous, with no allocation and no host sync.
+ */
+#ifndef CATS_H_
+#define CATS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CATS_VERSION 1
+#define CATS_MAX_BATCH 8
+
+typedef enum {
+    CATS_OK = 0,
+    CATS_E_NULL = 1,         /* a required pointer is NULL */
+    CATS_E_SHAPE = 2,        /* d, m or n out of range / inconsistent */
+    CATS_E_DTYPE = 3,        /* unknown dtype */
+    CATS_E_ALIGN = 4,        /* pointer not 16-byte aligned or row bytes not a multiple of 16 */
+    CATS_E_SPARSITY = 5,     /* k outside [0, 1) or NaN ("desired sparsity level k") */
+    CATS_E_EMPTY = 6,        /* n = 0 activations */
+    CATS_E_NONFINITE = 7,    /* calibration input holds NaN or +-Inf */
+    CATS_E_THRESHOLD = 8,    /* t < 0 or NaN ("t >= 0") */
+    CATS_E_BATCH = 9,        /* b outside [1, plan max_batch] */
+    CATS_E_WORKSPACE = 10,   /* workspace NULL or smaller than required */
+    CATS_E_CUDA = 11,        /* CUDA runtime error; see cats_last_cuda_error() */
+    CATS_E_UNSUPPORTED = 12  /* shape beyond what the kernels were built for */
+} cats_status_t;
+
+typedef enum {
+    CATS_F32 = 0,   /* IEEE binary32 */
+    CATS_BF16 = 1   /* bfloat16 */
+} cats_dtype_t;
+
+typedef void *cats_stream_t; /* cudaStream_t */
+
+/* Human-readable name of a status code (static storage). */
+const char *cats_status_string(cats_status_t s);
+/* Message of the last CUDA error seen by this thread ("" if none). Thread-local storage. */
+const char *cats_last_cuda_error(void);
+/* CATS_VERSION of the loaded library. */
+int cats_version(void);
+
+/* =============================================================================================
+ * Calibration (Stage 1; Eq. 3 at P:226-233)
+ * ========================================================================================== */
+
+/* The single normative rank rule (reading G5 in DESIGN.md): *r = ceil(k * n) computed exactly
+ * on the binary value of the double k (0 when k == 0). Host-only.
+ * Errors: CATS_E_NULL (r), CATS_E_SPARSITY (k not in [0,1) or NaN). */
+cats_status_t cats_calib_rank(double k, uint64_t n, uint64_t *r);
+
+typedef struct {
+    uint64_t n;         /* number of activations */
+    uint64_t rank_r;    /* r = ceil(k n) */
+    uint64_t count_lt;  /* #{ |a_i| <  t } */
+    uint64_t count_le;  /* #{ |a_i| <= t }  -- invariant count_lt < k n <= count_le (r > 0) */
+    uint32_t t_bits;    /* bit pattern of t in the INPUT dtype (bf16: 16 bits, fp32: 32 bits) */
+    uint32_t passes;    /* full passes over the data the GPU made (sample pass not counted) */
+} cats_calib_info_t;
+
+/* Device workspace needed by cats_calibrate_threshold / cats_calib_hist (histogram bins and
+ * counters). Host-only. Errors: CATS_E_NULL, CATS_E_DTYPE. */
+cats_status_t cats_calibrate_workspace_bytes(uint64_t n, cats_dtype_t dt, size_t *bytes);
+
+/* Eq. 3 threshold of one MLP block. acts: n post-SiLU activations (device, 16-B aligned; signed
+ * values -- the library takes |.|, so magnitudes also work). k: target sparsity in [0,1).
+ * Writes t (fp32; exactly an input value widened, or 0 for k = 0) and, if info != NULL, the
+ * exact rank bookkeeping. GPU histogram / radix-select: a strided sample pass picks a key
+ * window around the rank, then full passes histogram only the window.
+ * BLOCKS on stream s (returns a host scalar).
+ * Errors: CATS_E_NULL, CATS_E_DTYPE, CATS_E_ALIGN, CATS_E_SPARSITY, CATS_E_EMPTY,
+ *         CATS_E_NONFINITE (any NaN/Inf in acts), CATS_E_WORKSPACE, CATS_E_CUDA. */
+cats_status_t cats_calibrate_threshold(const void *acts, uint64_t n, cats_dtype_t dt, double k,
+                                       void *ws, size_t ws_bytes, cats_stream_t s,
+                                       float *t_out, cats_calib_info_t *info);
+
+/* ---- building blocks (sharded / streamed calibration: all-reduce the histograms between
+ *      steps and every rank selects the same t) -------------------------------------------- */
+
+/* A key window: keys are |bit patterns| (sign cleared, 15 bits for bf16, 31 for fp32), whose
+ * unsigned order equals the order of |value| for finite values. Bin of key q in [lo, hi] is
+ * (q - lo) >> shift; nbins = ((hi - lo) >> shift) + 1 <= CATS_CALIB_MAX_BINS. */
+#define CATS_CALIB_MAX_BINS 32768
+typedef struct {
+    uint32_t lo, hi;     /* inclusive key range, hi <= largest finite key */
+    uint32_t shift;      /* bin width = 2^shift keys */
+    uint32_t nbins;
+    uint64_t sample_stride; /* 0: every element; s > 0: only 16-byte vectors v with v % s == 0 */
+} cats_calib_window_t;
+
+/* Counter slots written by cats_calib_hist (accumulated with +=). */
+#define CATS_CALIB_BELOW 0     /* finite keys < lo */
+#define CATS_CALIB_INWIN 1     /* keys in [lo, hi] */
+#define CATS_CALIB_ABOVE 2     /* finite keys > hi */
+#define CATS_CALIB_NONFINITE 3 /* NaN / Inf */
+#define CATS_CALIB_NCOUNTS 4
+
+/* Initial window for n values: the whole finite key range, coarse bins; strided sampling when n
+ * is large (the sample only steers the window; it never decides t). Host-only. */
+cats_status_t cats_calib_window_init(uint64_t n, cats_dtype_t dt, cats_calib_window_t *w);
+
+/* Device pass: hist_dev[0..w->nbins) += histogram of keys in the window, counts_dev[0..4) +=
+ * the CATS_CALIB_* counts, over acts (or its sample). Caller zeroes both buffers first (or keeps
+ * accumulating chunks / ranks). Asynchronous. Errors: CATS_E_NULL, CATS_E_DTYPE, CATS_E_ALIGN,
+ * CATS_E_SHAPE (bad window), CATS_E_CUDA. */
+cats_status_t cats_calib_hist(const void *acts, uint64_t n, cats_dtype_t dt, const cats_calib_window_t *w,
+                              uint64_t *hist_dev, uint64_t *counts_dev, cats_stream_t s);
+
+/* Host step after a pass over ALL n values (hist/counts summed over every chunk and rank):
+ * if the rank-r key is resolved to a single key, *done = 1 and t_bits / count_lt / count_le are
+ * set; otherwise *w becomes the next, narrower (or re-aimed) window and *done = 0.
+ * If the window came from a sample (w->sample_stride > 0), sample_k_rank is used to aim the
+ * next full-data window with a statistical margin instead. Errors: CATS_E_NONFINITE,
+ * CATS_E_NULL, CATS_E_SHAPE (counts inconsistent with n). */
+cats_status_t cats_calib_step(const uint64_t *hist_host, const uint64_t *counts_host, uint64_t n,
+                              cats_dtype_t dt, double k, cats_calib_window_t *w, int *done,
+                              uint32_t *t_bits, uint64_t *count_lt, uint64_t *count_le);
+
+/* =============================================================================================
+ * Decode (Stage 2; App. D)
+ * ========================================================================================== */
+
+typedef struct cats_mlp_plan cats_mlp_plan_t;
+
+typedef struct {
+    int d, m, max_batch;
+    cats_dtype_t w_dtype;
+    int device, num_sms;
+    int k1_grid, k1_threads;      /* K1: gate GEMV + SiLU + threshold + compaction */
+    int k2_grid, k2_threads;      /* K2: sparse up x v + down, per-CTA split-K partials */
+    int k2_neurons_per_stage;     /* neurons per smem ring stage (W_up row + W_down row each) */
+    int k2_stages;                /* ring depth */
+    int k3_grid, k3_threads;      /* K3: fixed-order split-K reduction of the partials */
+    size_t k1_smem_max, k2_smem;  /* dynamic shared memory bytes */
+    size_t workspace_bytes;
+} cats_mlp_plan_info_t;
+
+/* Host-only planning (tile and grid choices from the SM count; no device allocation).
+ * num_sms <= 0 queries `device`; num_sms > 0 plans for that many SMs without touching a GPU.
+ * d: hidden size, m: intermediate size (this rank's shard under tensor parallelism).
+ * Errors: CATS_E_NULL, CATS_E_SHAPE (d, m <= 0), CATS_E_DTYPE, CATS_E_ALIGN (row bytes % 16),
+ *         CATS_E_BATCH (max_batch not in [1, 8]), CATS_E_UNSUPPORTED (d too large for the
+ *         register/shared-memory tiling), CATS_E_CUDA (device query failed). */
+cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_dtype_t w_dtype, int device,
+                                   int num_sms, cats_mlp_plan_t **out);
+void cats_mlp_plan_destroy(cats_mlp_plan_t *plan);
+cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_mlp_plan_info_t *info);
+cats_status_t cats_mlp_workspace_bytes(const cats_mlp_plan_t *plan, size_t *bytes);
+
+/* y[b][d] = CATS_t gated MLP of x[b][d] over this plan's m neurons (under tensor parallelism y
+ * is the rank's partial; the caller all-reduces). t >= 0; t = 0 gives dense semantics.
+ * Launches K1 -> K2 -> K3 on s (programmatic dependent launch between them). Deterministic:
+ * bit-identical y for identical inputs.
+ * Errors: CATS_E_NULL, CATS_E_ALIGN, CATS_E_BATCH, CATS_E_THRESHOLD, CATS_E_WORKSPACE,
+ *         CATS_E_CUDA. */
+cats_status_t cats_mlp_decode(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
+                              const void *W_up, const void *W_down_nm, float t, float *y,
+                              void *ws, size_t ws_bytes, cats_stream_t s);
+
+/* The library's own dense gated MLP (Eq. 1, the "Dense" baseline of P:530): same kernels with
+ * every neuron active. Same arguments / errors as cats_mlp_decode without t. */
+cats_status_t cats_mlp_dense(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
+                             const void *W_up, const void *W_down_nm, float *y,
+                             void *ws, size_t ws_bytes, cats_stream_t s);
+
+/* End-to-end variant for host activations: copies x_host [b][d] (pinned memory recommended)
+ * into the workspace, runs cats_mlp_decode, copies y to y_host [b][d] fp32. BLOCKS on s. */
+cats_status_t cats_mlp_decode_host(const cats_mlp_plan_t *plan, const void *x_host, int b,
+                                   const void *W_gate, const void *W_up, const void *W_down_nm,
+                                   float t, float *y_host, void *ws, size_t ws_bytes, cats_stream_t s);
+
+/* Measurement variant of cats_mlp_decode: identical launches, plus events[0..3] (cudaEvent_t,
+ * created by the caller with timing enabled) recorded on s before K1, between K1 and K2, between K2
+ * and K3, and after K3 -- per-kernel device time for the roofline report. The recorded events break
+ * the programmatic-dependent-launch overlap between the kernels, so the sum of the three intervals
+ * is an upper bound of a cats_mlp_decode call. */
+cats_status_t cats_mlp_decode_profiled(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
+                                       const void *W_up, const void *W_down_nm, float t, float *y,
+                                       void *ws, size_t ws_bytes, cats_stream_t s, void *const *events);
+
+/* Calibration data collection (S "collect_activations"): acts[b][m] = SiLU(x W_gate)
+ * in fp32 for b tokens -- the activations Eq. 3 is evaluated on. Uses K1. Asynchronous. */
+cats_status_t cats_mlp_gate_act(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
+                                float *acts, void *ws, size_t ws_bytes, cats_stream_t s);
+
+/* Introspection of the last decode on `ws` with batch b: the union of active neurons in
+ * ascending order (idx_host[0..*nnz_union)), each one's per-token keep bits (bit i = token i;
+ * tokmask_host, same order), and per-token active counts (nnz_per_token[b]). idx_host and
+ * tokmask_host must hold m entries; nnz_per_token may be NULL. BLOCKS on s. */
+cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const void *ws, int b, int32_t *idx_host,
+                                   uint8_t *tokmask_host, uint32_t *nnz_union, uint32_t *nnz_per_token,
+                                   cats_stream_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CATS_H_ */

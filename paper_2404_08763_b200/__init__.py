@@ -1,0 +1,256 @@
+"""paper_2404_08763_b200 -- B200-native CATS (arXiv 2404.08763) decode MLP + threshold calibration.
+
+Thin Python binding over the C ABI in include/cats.h (libcats.so, hand-written CUDA for
+sm_100a). Functions keep the C names; they only marshal arguments (torch tensors -> device
+pointers, current CUDA stream, workspace allocation). Every step of the method runs in the
+library's kernels; there is no CPU or PyTorch fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import CATS_BF16, CATS_F32, CalibInfo, CalibWindow, PlanInfo
+
+__all__ = [
+    "CatsError", "MlpPlan", "cats_calib_rank", "cats_calibrate_workspace_bytes", "cats_calibrate_threshold",
+    "cats_calib_window_init", "cats_calib_hist", "cats_calib_step", "cats_mlp_decode", "cats_mlp_dense",
+    "cats_mlp_decode_profiled",
+    "cats_mlp_decode_host", "cats_mlp_gate_act", "cats_mlp_last_active", "library_path",
+]
+
+
+class CatsError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        lib = _lib.load()
+        name = lib.cats_status_string(code).decode()
+        msg = f"{where}: {name}"
+        if name == "CATS_E_CUDA":
+            msg += f" ({lib.cats_last_cuda_error().decode()})"
+        super().__init__(msg)
+        self.code = code
+        self.name = name
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise CatsError(rc, where)
+
+
+def library_path() -> str:
+    _lib.load()
+    return _lib.LIB_PATH
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return CATS_BF16
+    if t.dtype == torch.float32:
+        return CATS_F32
+    raise TypeError(f"unsupported dtype {t.dtype} (bf16 or fp32)")
+
+
+def _dev_ptr(t: torch.Tensor, name: str) -> int:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream, device) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+# ------------------------------------------------------------------------------- calibration
+def cats_calib_rank(k: float, n: int) -> int:
+    r = ctypes.c_uint64()
+    _check(_lib.load().cats_calib_rank(float(k), int(n), ctypes.byref(r)), "cats_calib_rank")
+    return r.value
+
+
+def cats_calibrate_workspace_bytes(n: int, dtype: torch.dtype = torch.bfloat16) -> int:
+    b = ctypes.c_size_t()
+    dt = CATS_BF16 if dtype == torch.bfloat16 else CATS_F32
+    _check(_lib.load().cats_calibrate_workspace_bytes(int(n), dt, ctypes.byref(b)), "cats_calibrate_workspace_bytes")
+    return b.value
+
+
+def cats_calibrate_threshold(acts: torch.Tensor, k: float, ws: torch.Tensor | None = None, stream=None):
+    """Eq. 3 threshold of one MLP block from its activations (device tensor, any shape).
+
+    Returns (t: float, info: dict(n, rank_r, count_lt, count_le, t_bits, passes))."""
+    n = acts.numel()
+    if ws is None:
+        ws = torch.empty(cats_calibrate_workspace_bytes(n, acts.dtype), dtype=torch.uint8, device=acts.device)
+    t = ctypes.c_float()
+    info = CalibInfo()
+    rc = _lib.load().cats_calibrate_threshold(_dev_ptr(acts, "acts") if n else None, n, _dt(acts), float(k),
+                                              _dev_ptr(ws, "ws"), ws.numel(), _stream(stream, acts.device),
+                                              ctypes.byref(t), ctypes.byref(info))
+    _check(rc, "cats_calibrate_threshold")
+    return t.value, {f: getattr(info, f) for f, _ in CalibInfo._fields_}
+
+
+def cats_calib_window_init(n: int, dtype: torch.dtype) -> CalibWindow:
+    w = CalibWindow()
+    dt = CATS_BF16 if dtype == torch.bfloat16 else CATS_F32
+    _check(_lib.load().cats_calib_window_init(int(n), dt, ctypes.byref(w)), "cats_calib_window_init")
+    return w
+
+
+def cats_calib_hist(acts: torch.Tensor, window: CalibWindow, hist_dev: torch.Tensor, counts_dev: torch.Tensor,
+                    stream=None):
+    """hist_dev (uint64/int64 [>= nbins]) and counts_dev ([4]) are accumulated into (+=)."""
+    rc = _lib.load().cats_calib_hist(_dev_ptr(acts, "acts"), acts.numel(), _dt(acts), ctypes.byref(window),
+                                     _dev_ptr(hist_dev, "hist"), _dev_ptr(counts_dev, "counts"),
+                                     _stream(stream, acts.device))
+    _check(rc, "cats_calib_hist")
+
+
+def cats_calib_step(hist_host: np.ndarray, counts_host: np.ndarray, n: int, dtype: torch.dtype, k: float,
+                    window: CalibWindow):
+    """Returns (done, t_bits, count_lt, count_le); updates `window` in place when not done."""
+    hist_host = np.ascontiguousarray(hist_host, dtype=np.uint64)
+    counts_host = np.ascontiguousarray(counts_host, dtype=np.uint64)
+    done, tb = ctypes.c_int(), ctypes.c_uint32()
+    lt, le = ctypes.c_uint64(), ctypes.c_uint64()
+    dt = CATS_BF16 if dtype == torch.bfloat16 else CATS_F32
+    rc = _lib.load().cats_calib_step(hist_host.ctypes.data, counts_host.ctypes.data, int(n), dt, float(k),
+                                     ctypes.byref(window), ctypes.byref(done), ctypes.byref(tb), ctypes.byref(lt),
+                                     ctypes.byref(le))
+    _check(rc, "cats_calib_step")
+    return bool(done.value), tb.value, lt.value, le.value
+
+
+# ------------------------------------------------------------------------------- decode
+class MlpPlan:
+    """Host-only plan for one MLP shape (d, m) -- see cats_mlp_plan_create."""
+
+    def __init__(self, d: int, m: int, max_batch: int = 1, dtype: torch.dtype = torch.bfloat16, device: int = 0,
+                 num_sms: int = 0):
+        self._lib = _lib.load()
+        self._h = ctypes.c_void_p()
+        self.dtype = dtype
+        dt = CATS_BF16 if dtype == torch.bfloat16 else CATS_F32
+        _check(self._lib.cats_mlp_plan_create(int(d), int(m), int(max_batch), dt, int(device), int(num_sms),
+                                              ctypes.byref(self._h)), "cats_mlp_plan_create")
+        info = PlanInfo()
+        _check(self._lib.cats_mlp_plan_info(self._h, ctypes.byref(info)), "cats_mlp_plan_info")
+        self.info = {f: getattr(info, f) for f, _ in PlanInfo._fields_}
+        self.d, self.m, self.max_batch, self.device = d, m, max_batch, device
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def workspace_bytes(self) -> int:
+        return self.info["workspace_bytes"]
+
+    def workspace(self) -> torch.Tensor:
+        return torch.empty(self.workspace_bytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.cats_mlp_plan_destroy(h)
+            self._h = ctypes.c_void_p()
+
+
+def _prep(plan: MlpPlan, x: torch.Tensor, y, ws):
+    if x.dim() == 1:
+        x = x.unsqueeze(0)
+    b = x.shape[0]
+    if y is None:
+        y = torch.empty((b, plan.d), dtype=torch.float32, device=x.device)
+    if ws is None:
+        ws = plan.workspace()
+    return x, b, y, ws
+
+
+def cats_mlp_decode(plan: MlpPlan, x, W_gate, W_up, W_down_nm, t: float, y=None, ws=None, stream=None):
+    """y[b][d] (fp32) = CATS_t gated MLP of x[b][d]; weights neuron-major [m][d]."""
+    x, b, y, ws = _prep(plan, x, y, ws)
+    rc = plan._lib.cats_mlp_decode(plan.handle, _dev_ptr(x, "x"), b, _dev_ptr(W_gate, "W_gate"),
+                                   _dev_ptr(W_up, "W_up"), _dev_ptr(W_down_nm, "W_down_nm"), float(t),
+                                   _dev_ptr(y, "y"), _dev_ptr(ws, "ws"), ws.numel(), _stream(stream, x.device))
+    _check(rc, "cats_mlp_decode")
+    return y
+
+
+def cats_mlp_decode_profiled(plan: MlpPlan, x, W_gate, W_up, W_down_nm, t: float, events, y=None, ws=None,
+                             stream=None):
+    """cats_mlp_decode with 4 torch.cuda.Event(enable_timing=True) recorded around K1, K2, K3."""
+    x, b, y, ws = _prep(plan, x, y, ws)
+    for e in events:
+        if e.cuda_event == 0:
+            e.record()  # materialise the lazily created event on this device
+    arr = (ctypes.c_void_p * 4)(*[e.cuda_event for e in events])
+    rc = plan._lib.cats_mlp_decode_profiled(plan.handle, _dev_ptr(x, "x"), b, _dev_ptr(W_gate, "W_gate"),
+                                            _dev_ptr(W_up, "W_up"), _dev_ptr(W_down_nm, "W_down_nm"), float(t),
+                                            _dev_ptr(y, "y"), _dev_ptr(ws, "ws"), ws.numel(),
+                                            _stream(stream, x.device), arr)
+    _check(rc, "cats_mlp_decode_profiled")
+    return y
+
+
+def cats_mlp_dense(plan: MlpPlan, x, W_gate, W_up, W_down_nm, y=None, ws=None, stream=None):
+    x, b, y, ws = _prep(plan, x, y, ws)
+    rc = plan._lib.cats_mlp_dense(plan.handle, _dev_ptr(x, "x"), b, _dev_ptr(W_gate, "W_gate"),
+                                  _dev_ptr(W_up, "W_up"), _dev_ptr(W_down_nm, "W_down_nm"), _dev_ptr(y, "y"),
+                                  _dev_ptr(ws, "ws"), ws.numel(), _stream(stream, x.device))
+    _check(rc, "cats_mlp_dense")
+    return y
+
+
+def cats_mlp_decode_host(plan: MlpPlan, x_host: torch.Tensor, W_gate, W_up, W_down_nm, t: float, y_host=None,
+                         ws=None, stream=None):
+    """Host x in (pinned recommended), host y out; blocks on the stream."""
+    if x_host.dim() == 1:
+        x_host = x_host.unsqueeze(0)
+    assert not x_host.is_cuda and x_host.is_contiguous()
+    b = x_host.shape[0]
+    if y_host is None:
+        y_host = torch.empty((b, plan.d), dtype=torch.float32, pin_memory=x_host.is_pinned())
+    if ws is None:
+        ws = plan.workspace()
+    rc = plan._lib.cats_mlp_decode_host(plan.handle, x_host.data_ptr(), b, _dev_ptr(W_gate, "W_gate"),
+                                        _dev_ptr(W_up, "W_up"), _dev_ptr(W_down_nm, "W_down_nm"), float(t),
+                                        y_host.data_ptr(), _dev_ptr(ws, "ws"), ws.numel(),
+                                        _stream(stream, W_gate.device))
+    _check(rc, "cats_mlp_decode_host")
+    return y_host
+
+
+def cats_mlp_gate_act(plan: MlpPlan, x, W_gate, acts=None, ws=None, stream=None):
+    """acts[b][m] = SiLU(x W_gate) (fp32) -- calibration data collection."""
+    if x.dim() == 1:
+        x = x.unsqueeze(0)
+    b = x.shape[0]
+    if acts is None:
+        acts = torch.empty((b, plan.m), dtype=torch.float32, device=x.device)
+    if ws is None:
+        ws = plan.workspace()
+    rc = plan._lib.cats_mlp_gate_act(plan.handle, _dev_ptr(x, "x"), b, _dev_ptr(W_gate, "W_gate"),
+                                     _dev_ptr(acts, "acts"), _dev_ptr(ws, "ws"), ws.numel(),
+                                     _stream(stream, x.device))
+    _check(rc, "cats_mlp_gate_act")
+    return acts
+
+
+def cats_mlp_last_active(plan: MlpPlan, ws: torch.Tensor, b: int, stream=None):
+    """(idx int32[nnz] ascending, tokmask uint8[nnz], nnz_per_token uint32[b]) of the last decode."""
+    idx = np.zeros(plan.m, np.int32)
+    tm = np.zeros(plan.m, np.uint8)
+    nnz = ctypes.c_uint32()
+    per = np.zeros(b, np.uint32)
+    rc = plan._lib.cats_mlp_last_active(plan.handle, _dev_ptr(ws, "ws"), int(b), idx.ctypes.data, tm.ctypes.data,
+                                        ctypes.byref(nnz), per.ctypes.data, _stream(stream, ws.device))
+    _check(rc, "cats_mlp_last_active")
+    return idx[: nnz.value].copy(), tm[: nnz.value].copy(), per

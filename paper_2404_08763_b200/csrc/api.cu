@@ -1,0 +1,501 @@
+// api.cu -- the exported C ABI of libcats (declared in include/cats.h): validation, planning,
+// workspace layout, launch sequencing and the host side of the calibration radix select.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "cats_internal.h"
+
+using namespace cats;
+
+struct cats_mlp_plan {
+    PlanData p;
+};
+
+namespace cats {
+static thread_local std::string g_last_cuda_error;
+void set_last_cuda_error(cudaError_t e) {
+    g_last_cuda_error = std::string(cudaGetErrorName(e)) + ": " + cudaGetErrorString(e);
+}
+}  // namespace cats
+
+namespace {
+
+constexpr uint32_t kKeyMaxBF16 = 0x7f7fu;       // largest finite |bf16| key
+constexpr uint32_t kKeyMaxF32 = 0x7f7fffffu;    // largest finite |fp32| key
+constexpr uint32_t kFullPassBins = 4096;        // shared-memory bins of a full-data pass
+constexpr size_t kCalibHistOff = 0;
+constexpr size_t kCalibCountOff = (size_t)CATS_CALIB_MAX_BINS * 8;
+constexpr size_t kCalibWsBytes = kCalibCountOff + 64;
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+inline cats_status_t cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return CATS_OK;
+    set_last_cuda_error(e);
+    return CATS_E_CUDA;
+}
+
+#define CATS_TRY(...)                                                    \
+    try {                                                                \
+        __VA_ARGS__                                                      \
+    } catch (const std::bad_alloc &) {                                   \
+        g_last_cuda_error = "host allocation failed";                    \
+        return CATS_E_CUDA;                                              \
+    } catch (...) {                                                      \
+        g_last_cuda_error = "unexpected host exception";                 \
+        return CATS_E_CUDA;                                              \
+    }
+
+uint32_t key_max(cats_dtype_t dt) { return dt == CATS_BF16 ? kKeyMaxBF16 : kKeyMaxF32; }
+
+void make_window(uint32_t lo, uint32_t hi, uint32_t maxbins, cats_calib_window_t *w) {
+    uint32_t shift = 0;
+    while (((hi - lo) >> shift) + 1u > maxbins) ++shift;
+    w->lo = lo;
+    w->hi = hi;
+    w->shift = shift;
+    w->nbins = ((hi - lo) >> shift) + 1u;
+    w->sample_stride = 0;
+}
+
+// exact ceil(k * n) on the IEEE-754 bits of k (0 <= k < 1): k = M * 2^-(1075 - E)
+uint64_t exact_rank(double k, uint64_t n) {
+    uint64_t bits;
+    std::memcpy(&bits, &k, sizeof bits);
+    const uint64_t E = (bits >> 52) & 0x7ffu;
+    const uint64_t frac = bits & ((1ull << 52) - 1);
+    if (E == 0 && frac == 0) return 0;
+    const uint64_t M = E ? (frac | (1ull << 52)) : frac;
+    const int sh = (int)(1075 - (E ? E : 1));
+    const unsigned __int128 prod = (unsigned __int128)M * n;
+    if (prod == 0) return 0;
+    if (sh >= 128) return 1;
+    const unsigned __int128 q = prod >> sh;
+    return (uint64_t)(((q << sh) == prod) ? q : q + 1);
+}
+
+bool valid_k(double k) { return k >= 0.0 && k < 1.0; }  // false for NaN
+
+}  // namespace
+
+// =============================================================================== misc
+extern "C" const char *cats_status_string(cats_status_t s) {
+    switch (s) {
+        case CATS_OK: return "CATS_OK";
+        case CATS_E_NULL: return "CATS_E_NULL";
+        case CATS_E_SHAPE: return "CATS_E_SHAPE";
+        case CATS_E_DTYPE: return "CATS_E_DTYPE";
+        case CATS_E_ALIGN: return "CATS_E_ALIGN";
+        case CATS_E_SPARSITY: return "CATS_E_SPARSITY";
+        case CATS_E_EMPTY: return "CATS_E_EMPTY";
+        case CATS_E_NONFINITE: return "CATS_E_NONFINITE";
+        case CATS_E_THRESHOLD: return "CATS_E_THRESHOLD";
+        case CATS_E_BATCH: return "CATS_E_BATCH";
+        case CATS_E_WORKSPACE: return "CATS_E_WORKSPACE";
+        case CATS_E_CUDA: return "CATS_E_CUDA";
+        case CATS_E_UNSUPPORTED: return "CATS_E_UNSUPPORTED";
+    }
+    return "CATS_E_UNKNOWN";
+}
+
+extern "C" const char *cats_last_cuda_error(void) { return g_last_cuda_error.c_str(); }
+extern "C" int cats_version(void) { return CATS_VERSION; }
+
+// =============================================================================== calibration
+extern "C" cats_status_t cats_calib_rank(double k, uint64_t n, uint64_t *r) {
+    if (!r) return CATS_E_NULL;
+    if (!valid_k(k)) return CATS_E_SPARSITY;
+    *r = exact_rank(k, n);
+    return CATS_OK;
+}
+
+extern "C" cats_status_t cats_calibrate_workspace_bytes(uint64_t n, cats_dtype_t dt, size_t *bytes) {
+    (void)n;
+    if (!bytes) return CATS_E_NULL;
+    if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
+    *bytes = kCalibWsBytes;
+    return CATS_OK;
+}
+
+extern "C" cats_status_t cats_calib_window_init(uint64_t n, cats_dtype_t dt, cats_calib_window_t *w) {
+    if (!w) return CATS_E_NULL;
+    if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
+    make_window(0, key_max(dt), CATS_CALIB_MAX_BINS, w);
+    const uint64_t nvec = n / (dt == CATS_BF16 ? 8 : 4);
+    // sample ~2^17 vectors (~1M bf16 values) when the data is large; odd stride against aliasing
+    w->sample_stride = nvec > (1ull << 21) ? ((nvec >> 17) | 1ull) : 0ull;
+    return CATS_OK;
+}
+
+extern "C" cats_status_t cats_calib_hist(const void *acts, uint64_t n, cats_dtype_t dt, const cats_calib_window_t *w,
+                                         uint64_t *hist_dev, uint64_t *counts_dev, cats_stream_t s) {
+    if (!acts || !w || !hist_dev || !counts_dev) return CATS_E_NULL;
+    if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
+    if (!aligned16(acts)) return CATS_E_ALIGN;
+    if (w->hi < w->lo || w->hi > key_max(dt) || w->nbins == 0 || w->nbins > CATS_CALIB_MAX_BINS ||
+        w->shift > 31 || ((w->hi - w->lo) >> w->shift) + 1u != w->nbins)
+        return CATS_E_SHAPE;
+    if (n == 0) return CATS_OK;
+    return cuda_status(launch_calib_hist(acts, n, dt, *w, hist_dev, counts_dev, static_cast<cudaStream_t>(s)));
+}
+
+extern "C" cats_status_t cats_calib_step(const uint64_t *hist, const uint64_t *counts, uint64_t n, cats_dtype_t dt,
+                                         double k, cats_calib_window_t *w, int *done, uint32_t *t_bits,
+                                         uint64_t *count_lt, uint64_t *count_le) {
+    if (!hist || !counts || !w || !done || !t_bits || !count_lt || !count_le) return CATS_E_NULL;
+    if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
+    if (!valid_k(k)) return CATS_E_SPARSITY;
+    if (n == 0) return CATS_E_EMPTY;
+    *done = 0;
+    const uint32_t kmax = key_max(dt);
+    const uint64_t below = counts[CATS_CALIB_BELOW], inwin = counts[CATS_CALIB_INWIN];
+    const uint64_t above = counts[CATS_CALIB_ABOVE], nonfin = counts[CATS_CALIB_NONFINITE];
+    if (nonfin) return CATS_E_NONFINITE;
+    const uint64_t r = exact_rank(k, n);
+
+    if (w->sample_stride) {
+        // aim a full-data window at the rank with a 6-sigma binomial margin (statistics only steer
+        // the window; exactness comes from the full passes, which re-aim if the rank is missed)
+        const uint64_t ns = below + inwin + above;
+        if (r == 0) { make_window(0, 0, kFullPassBins, w); return CATS_OK; }
+        if (ns == 0) { make_window(0, kmax, CATS_CALIB_MAX_BINS, w); return CATS_OK; }
+        const double rs = k * (double)ns;
+        const double delta = 6.0 * std::sqrt((double)ns * k * (1.0 - k)) + 16.0;
+        const double rlo = rs - delta, rhi = rs + delta;
+        uint32_t lo = 0, hi = kmax;
+        if (rlo > (double)below) {
+            uint64_t cum = below;
+            for (uint32_t b = 0; b < w->nbins; ++b) {
+                cum += hist[b];
+                if ((double)cum >= rlo) { lo = w->lo + (b << w->shift); break; }
+            }
+        }
+        if (rhi <= (double)(below + inwin)) {
+            uint64_t cum = below;
+            for (uint32_t b = 0; b < w->nbins; ++b) {
+                cum += hist[b];
+                if ((double)cum >= rhi) {
+                    const uint64_t h = (uint64_t)w->lo + ((uint64_t)(b + 1) << w->shift) - 1;
+                    hi = (uint32_t)std::min<uint64_t>(h, w->hi);
+                    break;
+                }
+            }
+        }
+        make_window(lo, hi, kFullPassBins, w);
+        return CATS_OK;
+    }
+
+    if (below + inwin + above != n) return CATS_E_SHAPE;
+    if (r == 0) {  // k = 0: t = 0 (reading G4); count_le = #{|a| == 0}
+        if (w->lo == 0 && w->shift == 0) {
+            *t_bits = 0;
+            *count_lt = 0;
+            *count_le = hist[0];
+            *done = 1;
+        } else {
+            make_window(0, 0, kFullPassBins, w);
+        }
+        return CATS_OK;
+    }
+    if (r <= below) { make_window(0, w->lo - 1, kFullPassBins, w); return CATS_OK; }
+    if (r > below + inwin) { make_window(w->hi + 1, kmax, kFullPassBins, w); return CATS_OK; }
+    uint64_t cum = below;
+    uint32_t b = 0;
+    for (; b < w->nbins; ++b) {
+        if (cum + hist[b] >= r) break;
+        cum += hist[b];
+    }
+    if (b == w->nbins) return CATS_E_SHAPE;  // histogram inconsistent with counts
+    if (w->shift == 0) {
+        *t_bits = w->lo + b;
+        *count_lt = cum;
+        *count_le = cum + hist[b];
+        *done = 1;
+        return CATS_OK;
+    }
+    const uint32_t lo = w->lo + (b << w->shift);
+    const uint32_t hi = (uint32_t)std::min<uint64_t>((uint64_t)lo + (1ull << w->shift) - 1, w->hi);
+    make_window(lo, hi, kFullPassBins, w);
+    return CATS_OK;
+}
+
+extern "C" cats_status_t cats_calibrate_threshold(const void *acts, uint64_t n, cats_dtype_t dt, double k, void *ws,
+                                                  size_t ws_bytes, cats_stream_t s, float *t_out,
+                                                  cats_calib_info_t *info) {
+    if (!acts || !t_out) return CATS_E_NULL;
+    if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
+    if (!valid_k(k)) return CATS_E_SPARSITY;
+    if (n == 0) return CATS_E_EMPTY;
+    if (!aligned16(acts)) return CATS_E_ALIGN;
+    if (!ws || ws_bytes < kCalibWsBytes) return CATS_E_WORKSPACE;
+    if (!aligned16(ws)) return CATS_E_ALIGN;
+    CATS_TRY({
+        cudaStream_t st = static_cast<cudaStream_t>(s);
+        uint64_t *hist = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kCalibHistOff);
+        uint64_t *cnt = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + kCalibCountOff);
+        std::vector<uint64_t> h_hist(CATS_CALIB_MAX_BINS);
+        uint64_t h_cnt[CATS_CALIB_NCOUNTS];
+        cats_calib_window_t w;
+        cats_calib_window_init(n, dt, &w);
+        uint32_t passes = 0, t_bits = 0;
+        uint64_t lt = 0, le = 0;
+        int done = 0;
+        for (int it = 0; it < 32 && !done; ++it) {
+            cudaError_t e = cudaMemsetAsync(hist, 0, (size_t)w.nbins * 8, st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, CATS_CALIB_NCOUNTS * 8, st);
+            if (e == cudaSuccess) e = launch_calib_hist(acts, n, dt, w, hist, cnt, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(h_hist.data(), hist, (size_t)w.nbins * 8, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(h_cnt, cnt, sizeof h_cnt, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) return cuda_status(e);
+            if (!w.sample_stride) ++passes;
+            cats_status_t rc = cats_calib_step(h_hist.data(), h_cnt, n, dt, k, &w, &done, &t_bits, &lt, &le);
+            if (rc != CATS_OK) return rc;
+        }
+        if (!done) { g_last_cuda_error = "calibration did not converge"; return CATS_E_CUDA; }
+        uint32_t f32bits = dt == CATS_BF16 ? (t_bits << 16) : t_bits;
+        float t;
+        std::memcpy(&t, &f32bits, sizeof t);
+        *t_out = t;
+        if (info) {
+            info->n = n;
+            info->rank_r = exact_rank(k, n);
+            info->count_lt = lt;
+            info->count_le = le;
+            info->t_bits = t_bits;
+            info->passes = passes;
+        }
+        return CATS_OK;
+    })
+}
+
+// =============================================================================== planning
+extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_dtype_t dt, int device, int num_sms,
+                                              cats_mlp_plan_t **out) {
+    if (!out) return CATS_E_NULL;
+    if (d <= 0 || m <= 0) return CATS_E_SHAPE;
+    if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
+    if (max_batch < 1 || max_batch > CATS_MAX_BATCH) return CATS_E_BATCH;
+    const int esize = dt == CATS_BF16 ? 2 : 4;
+    if (((size_t)d * esize) % 16 != 0) return CATS_E_ALIGN;
+    if (num_sms <= 0) {
+        cudaError_t e = cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device);
+        if (e != cudaSuccess) return cuda_status(e);
+    }
+    CATS_TRY({
+        PlanData p{};
+        p.d = d;
+        p.m = m;
+        p.max_batch = max_batch;
+        p.dt = dt;
+        p.device = device;
+        p.num_sms = num_sms;
+        p.esize = esize;
+        p.vec = 16 / esize;
+        p.nchunks = d * esize / 16;
+        // K1: one persistent CTA per SM over a contiguous neuron range
+        p.g1 = std::min(num_sms, m);
+        p.r_max = (m + p.g1 - 1) / p.g1;
+        if (k1_smem_bytes(p, max_batch) > kSmemBudget) return CATS_E_UNSUPPORTED;
+        // K2: one persistent CTA per SM; each owns 1/p2 of the active list
+        p.p2 = num_sms;
+        p.k2_threads = max_batch <= 2 ? 256 : 512;
+        const int cpt256 = (p.nchunks + 255) / 256, cpt512 = (p.nchunks + 511) / 512;
+        if (cpt256 > kMaxCPT || cpt512 > kMaxCPT) return CATS_E_UNSUPPORTED;
+        p.cpt = p.k2_threads == 256 ? cpt256 : cpt512;
+        p.ns = 2;
+        p.l_max = (m + p.p2 - 1) / p.p2;
+        const size_t stage = (size_t)p.ns * 2 * (size_t)d * esize;
+        const size_t extra = k2_smem_bytes(esize, d, p.ns, 0, max_batch, p.l_max, p.g1, 512) + 8 * 8;
+        if (extra + 2 * stage > kSmemBudget) return CATS_E_UNSUPPORTED;
+        p.stages = (int)std::min<size_t>(8, (kSmemBudget - extra) / stage);
+        p.k2_smem = k2_smem_bytes(esize, d, p.ns, p.stages, max_batch, p.l_max, p.g1, 512);
+        // workspace
+        size_t off = 0;
+        p.off_idx = off;     off = align_up(off + (size_t)m * 4, 256);
+        p.off_tokmask = off; off = align_up(off + (size_t)m, 256);
+        p.off_vals = off;    off = align_up(off + (size_t)m * max_batch * 4, 256);
+        p.off_cnt = off;     off = align_up(off + (size_t)p.g1 * 4, 256);
+        p.off_ypart = off;   off = align_up(off + (size_t)p.p2 * max_batch * d * 4, 256);
+        p.off_xstage = off;  off = align_up(off + (size_t)max_batch * d * esize, 256);
+        p.off_ystage = off;  off = align_up(off + (size_t)max_batch * d * 4, 256);
+        p.ws_bytes = off;
+        cats_mlp_plan *plan = new cats_mlp_plan;
+        plan->p = p;
+        *out = plan;
+        return CATS_OK;
+    })
+}
+
+extern "C" void cats_mlp_plan_destroy(cats_mlp_plan_t *plan) { delete plan; }
+
+extern "C" cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_mlp_plan_info_t *info) {
+    if (!plan || !info) return CATS_E_NULL;
+    const PlanData &p = plan->p;
+    info->d = p.d;
+    info->m = p.m;
+    info->max_batch = p.max_batch;
+    info->w_dtype = p.dt;
+    info->device = p.device;
+    info->num_sms = p.num_sms;
+    info->k1_grid = p.g1;
+    info->k1_threads = kK1Threads;
+    info->k2_grid = p.p2;
+    info->k2_threads = p.k2_threads;
+    info->k2_neurons_per_stage = p.ns;
+    info->k2_stages = p.stages;
+    info->k3_grid = (p.max_batch * p.d / 4 + kK3Threads / 32 - 1) / (kK3Threads / 32);
+    info->k3_threads = kK3Threads;
+    info->k1_smem_max = k1_smem_bytes(p, p.max_batch);
+    info->k2_smem = p.k2_smem;
+    info->workspace_bytes = p.ws_bytes;
+    return CATS_OK;
+}
+
+extern "C" cats_status_t cats_mlp_workspace_bytes(const cats_mlp_plan_t *plan, size_t *bytes) {
+    if (!plan || !bytes) return CATS_E_NULL;
+    *bytes = plan->p.ws_bytes;
+    return CATS_OK;
+}
+
+// =============================================================================== decode
+namespace {
+
+cats_status_t validate_common(const cats_mlp_plan_t *plan, const void *x, int b, const void *a, const void *bptr,
+                              const void *c, const void *y, const void *ws, size_t ws_bytes) {
+    if (!plan || !x || !a || !bptr || !c || !y) return CATS_E_NULL;
+    if (b < 1 || b > plan->p.max_batch) return CATS_E_BATCH;
+    if (!ws || ws_bytes < plan->p.ws_bytes) return CATS_E_WORKSPACE;
+    if (!aligned16(x) || !aligned16(a) || !aligned16(bptr) || !aligned16(c) || !aligned16(y) || !aligned16(ws))
+        return CATS_E_ALIGN;
+    return CATS_OK;
+}
+
+cats_status_t run_mlp(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd, float t,
+                      int dense, float *y, void *ws, cudaStream_t st) {
+    cudaError_t e = cudaSetDevice(p.device);
+    if (e == cudaSuccess) e = launch_k1(p, x, b, Wg, t, dense, nullptr, ws, st);
+    if (e == cudaSuccess) e = launch_k2(p, x, b, Wu, Wd, ws, st, /*pdl=*/true);
+    if (e == cudaSuccess) e = launch_k3(p, b, ws, y, st, /*pdl=*/true);
+    return cuda_status(e);
+}
+
+}  // namespace
+
+extern "C" cats_status_t cats_mlp_decode(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
+                                         const void *W_up, const void *W_down_nm, float t, float *y, void *ws,
+                                         size_t ws_bytes, cats_stream_t s) {
+    cats_status_t rc = validate_common(plan, x, b, W_gate, W_up, W_down_nm, y, ws, ws_bytes);
+    if (rc != CATS_OK) return rc;
+    if (!(t >= 0.0f) || std::isinf(t)) return CATS_E_THRESHOLD;  // NaN fails t >= 0
+    return run_mlp(plan->p, x, b, W_gate, W_up, W_down_nm, t, 0, y, ws, static_cast<cudaStream_t>(s));
+}
+
+extern "C" cats_status_t cats_mlp_decode_profiled(const cats_mlp_plan_t *plan, const void *x, int b,
+                                                  const void *W_gate, const void *W_up, const void *W_down_nm,
+                                                  float t, float *y, void *ws, size_t ws_bytes, cats_stream_t s,
+                                                  void *const *events) {
+    cats_status_t rc = validate_common(plan, x, b, W_gate, W_up, W_down_nm, y, ws, ws_bytes);
+    if (rc != CATS_OK) return rc;
+    if (!events || !events[0] || !events[1] || !events[2] || !events[3]) return CATS_E_NULL;
+    if (!(t >= 0.0f) || std::isinf(t)) return CATS_E_THRESHOLD;
+    const PlanData &p = plan->p;
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    cudaEvent_t ev[4];
+    for (int i = 0; i < 4; ++i) ev[i] = static_cast<cudaEvent_t>(events[i]);
+    cudaError_t e = cudaSetDevice(p.device);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[0], st);
+    if (e == cudaSuccess) e = launch_k1(p, x, b, W_gate, t, 0, nullptr, ws, st);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[1], st);
+    if (e == cudaSuccess) e = launch_k2(p, x, b, W_up, W_down_nm, ws, st, /*pdl=*/true);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[2], st);
+    if (e == cudaSuccess) e = launch_k3(p, b, ws, y, st, /*pdl=*/true);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[3], st);
+    return cuda_status(e);
+}
+
+extern "C" cats_status_t cats_mlp_dense(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
+                                        const void *W_up, const void *W_down_nm, float *y, void *ws, size_t ws_bytes,
+                                        cats_stream_t s) {
+    cats_status_t rc = validate_common(plan, x, b, W_gate, W_up, W_down_nm, y, ws, ws_bytes);
+    if (rc != CATS_OK) return rc;
+    return run_mlp(plan->p, x, b, W_gate, W_up, W_down_nm, 0.0f, 1, y, ws, static_cast<cudaStream_t>(s));
+}
+
+extern "C" cats_status_t cats_mlp_decode_host(const cats_mlp_plan_t *plan, const void *x_host, int b,
+                                              const void *W_gate, const void *W_up, const void *W_down_nm, float t,
+                                              float *y_host, void *ws, size_t ws_bytes, cats_stream_t s) {
+    if (!plan || !x_host || !y_host || !W_gate || !W_up || !W_down_nm) return CATS_E_NULL;
+    if (b < 1 || b > plan->p.max_batch) return CATS_E_BATCH;
+    if (!ws || ws_bytes < plan->p.ws_bytes) return CATS_E_WORKSPACE;
+    if (!aligned16(ws) || !aligned16(W_gate) || !aligned16(W_up) || !aligned16(W_down_nm)) return CATS_E_ALIGN;
+    if (!(t >= 0.0f) || std::isinf(t)) return CATS_E_THRESHOLD;
+    const PlanData &p = plan->p;
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    char *w = static_cast<char *>(ws);
+    void *xd = w + p.off_xstage;
+    float *yd = reinterpret_cast<float *>(w + p.off_ystage);
+    cudaError_t e = cudaSetDevice(p.device);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(xd, x_host, (size_t)b * p.d * p.esize, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_status(e);
+    cats_status_t rc = run_mlp(p, xd, b, W_gate, W_up, W_down_nm, t, 0, yd, ws, st);
+    if (rc != CATS_OK) return rc;
+    e = cudaMemcpyAsync(y_host, yd, (size_t)b * p.d * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    return cuda_status(e);
+}
+
+extern "C" cats_status_t cats_mlp_gate_act(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
+                                           float *acts, void *ws, size_t ws_bytes, cats_stream_t s) {
+    if (!plan || !x || !W_gate || !acts) return CATS_E_NULL;
+    if (b < 1 || b > plan->p.max_batch) return CATS_E_BATCH;
+    if (!ws || ws_bytes < plan->p.ws_bytes) return CATS_E_WORKSPACE;
+    if (!aligned16(x) || !aligned16(W_gate) || !aligned16(ws)) return CATS_E_ALIGN;
+    cudaError_t e = cudaSetDevice(plan->p.device);
+    if (e == cudaSuccess) e = launch_k1(plan->p, x, b, W_gate, 0.0f, 1, acts, ws, static_cast<cudaStream_t>(s));
+    return cuda_status(e);
+}
+
+extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const void *ws, int b, int32_t *idx_host,
+                                              uint8_t *tokmask_host, uint32_t *nnz_union, uint32_t *nnz_per_token,
+                                              cats_stream_t s) {
+    if (!plan || !ws || !idx_host || !tokmask_host || !nnz_union) return CATS_E_NULL;
+    if (b < 1 || b > plan->p.max_batch) return CATS_E_BATCH;
+    const PlanData &p = plan->p;
+    CATS_TRY({
+        cudaStream_t st = static_cast<cudaStream_t>(s);
+        const char *w = static_cast<const char *>(ws);
+        std::vector<int32_t> idx(p.m), cnt(p.g1);
+        std::vector<uint8_t> tm(p.m);
+        cudaError_t e = cudaSetDevice(p.device);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(idx.data(), w + p.off_idx, (size_t)p.m * 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(tm.data(), w + p.off_tokmask, (size_t)p.m, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(cnt.data(), w + p.off_cnt, (size_t)p.g1 * 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_status(e);
+        uint32_t k = 0;
+        if (nnz_per_token) std::fill(nnz_per_token, nnz_per_token + b, 0u);
+        for (int c = 0; c < p.g1; ++c) {
+            const int64_t r0 = k1_row0(c, p.m, p.g1);
+            const int64_t R = k1_row0(c + 1, p.m, p.g1) - r0;
+            if (cnt[c] < 0 || cnt[c] > R) return CATS_E_SHAPE;
+            for (int i = 0; i < cnt[c]; ++i) {
+                idx_host[k] = idx[r0 + i];
+                tokmask_host[k] = tm[r0 + i];
+                if (nnz_per_token)
+                    for (int tk = 0; tk < b; ++tk) nnz_per_token[tk] += (tm[r0 + i] >> tk) & 1u;
+                ++k;
+            }
+        }
+        *nnz_union = k;
+        return CATS_OK;
+    })
+}

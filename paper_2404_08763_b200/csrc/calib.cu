@@ -1,0 +1,140 @@
+// calib.cu -- K-cal: windowed histogram pass for the Eq. 3 threshold (radix-select style).
+//
+// Paper: Stage 1, Eq. 3: t = min{t' : F(t') >= k}, F the empirical CDF of
+// |activations|. t is an order statistic of the |activations|, so it is found exactly by
+// histogramming keys = |bit pattern| (sign cleared; for finite IEEE values the unsigned order of
+// the key equals the order of |value|).
+//
+// One pass streams the activations once with 128-bit loads and, per element, only compares the
+// key against a window [lo, hi]: keys below/above are counted in registers; keys inside go to a
+// shared-memory histogram (bin = (key - lo) >> shift). A strided sample pass first aims the window
+// at the rank, so the atomics touch ~1% of elements; the host step (api.cu) narrows the window until
+// one key remains. NaN/Inf (key >= exponent-all-ones) are counted and rejected.
+#include <algorithm>
+
+#include "cats_device.cuh"
+#include "cats_internal.h"
+
+namespace cats {
+
+constexpr int kCalThreads = 512;
+constexpr int kCalUnroll = 4;
+
+template <typename K> struct KeyTraits;
+template <> struct KeyTraits<uint16_t> {  // bf16
+    static constexpr int kPerVec = 8;
+    static constexpr uint32_t kMask = 0x7fffu, kInf = 0x7f80u;
+    __device__ static inline uint32_t key(const uint4 &r, int e) {
+        const uint32_t w = (e >> 1) == 0 ? r.x : (e >> 1) == 1 ? r.y : (e >> 1) == 2 ? r.z : r.w;
+        return ((e & 1) ? (w >> 16) : w) & kMask;
+    }
+};
+template <> struct KeyTraits<uint32_t> {  // fp32
+    static constexpr int kPerVec = 4;
+    static constexpr uint32_t kMask = 0x7fffffffu, kInf = 0x7f800000u;
+    __device__ static inline uint32_t key(const uint4 &r, int e) {
+        const uint32_t w = e == 0 ? r.x : e == 1 ? r.y : e == 2 ? r.z : r.w;
+        return w & kMask;
+    }
+};
+
+template <typename K>
+__global__ void __launch_bounds__(kCalThreads)
+calib_hist_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint32_t hi, uint32_t shift, uint32_t nbins,
+                  uint64_t stride, unsigned long long *__restrict__ hist, unsigned long long *__restrict__ counts) {
+    using KT = KeyTraits<K>;
+    constexpr int E = KT::kPerVec;
+    extern __shared__ uint32_t sh[];  // [nbins]
+    __shared__ unsigned long long scount[4];
+    for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) sh[i] = 0u;
+    if (threadIdx.x < 4) scount[threadIdx.x] = 0ull;
+    __syncthreads();
+
+    uint32_t below = 0, above = 0, nonfin = 0, inwin = 0;
+    uint32_t cur_bin = 0xffffffffu, cur_cnt = 0;  // run-length cache against same-bin contention
+    auto classify = [&](uint32_t key) {
+        if (key >= KT::kInf) { ++nonfin; return; }
+        if (key < lo) { ++below; return; }
+        if (key > hi) { ++above; return; }
+        ++inwin;
+        const uint32_t bin = (key - lo) >> shift;
+        if (bin == cur_bin) { ++cur_cnt; return; }
+        if (cur_cnt) atomicAdd(&sh[cur_bin], cur_cnt);
+        cur_bin = bin;
+        cur_cnt = 1;
+    };
+
+    const uint64_t nvec = n / E;
+    const uint64_t nwork = stride ? (nvec + stride - 1) / stride : nvec;
+    const uint4 *v4 = reinterpret_cast<const uint4 *>(acts);
+    const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t step = stride ? stride : 1;
+    // main loop: kCalUnroll independent 16-byte loads in flight per thread
+    for (; i + (kCalUnroll - 1) * gstride < nwork; i += kCalUnroll * gstride) {
+        uint4 r[kCalUnroll];
+#pragma unroll
+        for (int u = 0; u < kCalUnroll; ++u) r[u] = ldg_stream(v4 + (i + u * gstride) * step);
+#pragma unroll
+        for (int u = 0; u < kCalUnroll; ++u)
+#pragma unroll
+            for (int e = 0; e < E; ++e) classify(KT::key(r[u], e));
+    }
+    for (; i < nwork; i += gstride) {
+        const uint4 r = ldg_stream(v4 + i * step);
+#pragma unroll
+        for (int e = 0; e < E; ++e) classify(KT::key(r, e));
+    }
+    // scalar tail (full passes only)
+    if (!stride && blockIdx.x == 0) {
+        for (uint64_t j = nvec * E + threadIdx.x; j < n; j += blockDim.x) classify((uint32_t)acts[j] & KT::kMask);
+    }
+    if (cur_cnt) atomicAdd(&sh[cur_bin], cur_cnt);
+
+    // block-reduce the register counters, one global atomic per counter per block
+    const unsigned long long c4[4] = {below, inwin, above, nonfin};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        unsigned long long v = c4[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&scount[q], v);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x)
+        if (sh[b]) atomicAdd(&hist[b], (unsigned long long)sh[b]);
+    if (threadIdx.x < 4 && scount[threadIdx.x]) atomicAdd(&counts[threadIdx.x], scount[threadIdx.x]);
+}
+
+cudaError_t launch_calib_hist(const void *acts, uint64_t n, cats_dtype_t dt, const cats_calib_window_t &w,
+                              uint64_t *hist, uint64_t *counts, cudaStream_t s) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = (size_t)w.nbins * 4;
+    const int per_vec = dt == CATS_BF16 ? 8 : 4;
+    const uint64_t nvec = n / per_vec;
+    const uint64_t nwork = w.sample_stride ? (nvec + w.sample_stride - 1) / w.sample_stride : nvec;
+    const int blocks_per_sm = smem <= 48 * 1024 ? 2 : 1;
+    uint64_t want = (nwork + kCalThreads - 1) / kCalThreads;
+    if (want < 1) want = 1;
+    const int grid = (int)std::min<uint64_t>(want, (uint64_t)nsm * blocks_per_sm);
+    auto *h = reinterpret_cast<unsigned long long *>(hist);
+    auto *c = reinterpret_cast<unsigned long long *>(counts);
+    if (dt == CATS_BF16) {
+        auto kern = calib_hist_kernel<uint16_t>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kCalThreads, smem, s>>>(static_cast<const uint16_t *>(acts), n, w.lo, w.hi, w.shift, w.nbins,
+                                             w.sample_stride, h, c);
+    } else {
+        auto kern = calib_hist_kernel<uint32_t>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kCalThreads, smem, s>>>(static_cast<const uint32_t *>(acts), n, w.lo, w.hi, w.shift, w.nbins,
+                                             w.sample_stride, h, c);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace cats

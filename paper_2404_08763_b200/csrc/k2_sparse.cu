@@ -1,0 +1,345 @@
+// k2_sparse.cu -- K2: fused sparse up x v and down projection; K3: deterministic split-K reduce.
+//
+// Paper: Custom GPU Kernel "MLP using CATS" lines 4-5:
+//     x1 <- (x W_up[Mask]) * v[Mask];   y <- x1 W_down[Mask]
+// with Optimization 1, the x v multiply fused into the x W_up tile so x1 never touches HBM
+// (P:305-306), and App. D eq. y = (v' * (x W'_up)) W'_down.
+//
+// B200 design:
+//  * Only active neurons' rows of W_up and of the neuron-major W_down are read: each is one
+//    contiguous 2d-byte row, moved HBM -> shared memory by the TMA bulk-copy engine
+//    (cp.async.bulk + mbarrier transaction counts) into an S-stage ring, NS neurons per stage.
+//  * The union active list produced by K1 (per-K1-CTA segments) is split into P equal,
+//    contiguous slices, one per persistent CTA: perfect load balance, no atomics.
+//  * Thread t owns fixed 16-byte column chunks {t, t+NT, ...} of d: it keeps x and its slice of
+//    the y partial in registers. The up dot products are reduced across the CTA in a fixed
+//    order (warp butterfly, then warps 0..NW-1), scaled by v (Optimization 1), and broadcast;
+//    the down projection is then a register axpy over the staged W_down rows.
+//  * The paper's fp16 tl.atomic_add into Y is replaced by a deterministic two-phase
+//    split-K: each CTA writes its fp32 partial y_p, K3 sums the P partials in a fixed order.
+#include "cats_device.cuh"
+#include "cats_internal.h"
+
+namespace cats {
+
+template <typename T, int B, int CPT, int NS, int NT>
+__global__ void __launch_bounds__(NT, 1)
+k2_sparse_up_down(const T *__restrict__ x, const T *__restrict__ Wu, const T *__restrict__ Wd, int d, int m,
+                  int g1, int p2, int stages, int l_max, const int32_t *__restrict__ idx,
+                  const float *__restrict__ vals, const int32_t *__restrict__ cnt, float *__restrict__ ypart) {
+    constexpr int VEC = VecTraits<T>::kVec;
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int p = blockIdx.x;
+    const int nch = d * (int)sizeof(T) / 16;
+    const uint32_t row_bytes = (uint32_t)d * (uint32_t)sizeof(T);
+    const uint32_t stage_bytes = (uint32_t)NS * 2u * row_bytes;
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char *ring = smem;                                                     // [stages][NS][2][row]
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * stage_bytes);  // [stages]
+    int *pref = reinterpret_cast<int *>(full + stages);                             // [g1 + 1]
+    int *slist = pref + (g1 + 1);                                                   // [l_max] neuron ids
+    float *svals = reinterpret_cast<float *>(slist + l_max);                        // [l_max][B]
+    float *red = svals + (size_t)l_max * B;                                         // [NW][NS][B]
+    float *as = red + (size_t)NW * NS * B;                                          // [NS][B]
+
+    pdl_launch_dependents();
+
+    if (tid == 0) {
+        for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+
+    // x -> registers (fp32), own chunks only. x is not written by K1, so this overlaps K1's tail.
+    float xr[B][CPT][VEC];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int ch = tid + k * NT;
+#pragma unroll
+        for (int tk = 0; tk < B; ++tk) {
+            if (ch < nch) {
+                const uint4 r = *reinterpret_cast<const uint4 *>(x + (size_t)tk * d + (size_t)ch * VEC);
+                unpack16(r, xr[tk][k]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) xr[tk][k][e] = 0.f;
+            }
+        }
+    }
+
+    // ---- wait for K1 (programmatic dependent launch) ----
+    pdl_wait_primary();
+
+    // prefix over K1's per-CTA active counts -> union size U and this CTA's slice [a0, a1)
+    for (int i = tid; i < g1; i += NT) pref[i + 1] = cnt[i];
+    if (tid == 0) pref[0] = 0;
+    __syncthreads();
+    if (warp == 0) {
+        const int per = (g1 + 31) / 32;
+        const int lo = lane * per, hi = min(g1, lo + per);
+        int s = 0;
+        for (int i = lo; i < hi; ++i) s += pref[i + 1];
+        int inc = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        int run = inc - s;
+        for (int i = lo; i < hi; ++i) {
+            run += pref[i + 1];
+            pref[i + 1] = run;
+        }
+    }
+    __syncthreads();
+    const int U = pref[g1];
+    const int a0 = (int)((int64_t)p * U / p2), a1 = (int)((int64_t)(p + 1) * U / p2);
+    const int L = a1 - a0;
+
+    // gather the slice's neuron ids and v values (global position q -> K1 segment)
+    for (int q = a0 + tid; q < a1; q += NT) {
+        int lo = 0, hi = g1 - 1;  // largest c with pref[c] <= q
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pref[mid] <= q) lo = mid; else hi = mid - 1;
+        }
+        const int64_t pos = k1_row0(lo, m, g1) + (q - pref[lo]);
+        slist[q - a0] = idx[pos];
+#pragma unroll
+        for (int tk = 0; tk < B; ++tk) svals[(size_t)(q - a0) * B + tk] = vals[(size_t)pos * B + tk];
+    }
+    __syncthreads();
+
+    const int ngroups = (L + NS - 1) / NS;
+    uint64_t policy = 0;
+    auto issue = [&](int g) {  // thread 0 only
+        const int s = g % stages;
+        const int n_in = min(NS, L - g * NS);
+        mbar_arrive_expect_tx(&full[s], (uint32_t)n_in * 2u * row_bytes);
+        unsigned char *dst = ring + (size_t)s * stage_bytes;
+        for (int i = 0; i < n_in; ++i) {
+            const size_t j = (size_t)slist[g * NS + i];
+            bulk_g2s(dst + (size_t)(2 * i) * row_bytes, Wu + j * d, row_bytes, &full[s], policy);
+            bulk_g2s(dst + (size_t)(2 * i + 1) * row_bytes, Wd + j * d, row_bytes, &full[s], policy);
+        }
+    };
+    if (tid == 0) {
+        policy = l2_evict_first_policy();
+        const int first = min(stages, ngroups);
+        for (int g = 0; g < first; ++g) issue(g);
+    }
+
+    float yr[B][CPT][VEC];
+#pragma unroll
+    for (int tk = 0; tk < B; ++tk)
+#pragma unroll
+        for (int k = 0; k < CPT; ++k)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) yr[tk][k][e] = 0.f;
+
+    for (int g = 0; g < ngroups; ++g) {
+        const int s = g % stages;
+        const int n_in = min(NS, L - g * NS);
+        mbar_wait(&full[s], (uint32_t)((g / stages) & 1));
+        const uint32_t sbase = smem_u32(ring + (size_t)s * stage_bytes);
+
+        // ---- up: partial dots of x with this thread's chunks of each staged W_up row ----
+        float part[NS][B];
+#pragma unroll
+        for (int i = 0; i < NS; ++i) {
+#pragma unroll
+            for (int tk = 0; tk < B; ++tk) part[i][tk] = 0.f;
+            if (i < n_in) {
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    const int ch = tid + k * NT;
+                    if (ch < nch) {
+                        float wf[VEC];
+                        unpack16(lds128(sbase + (uint32_t)(2 * i) * row_bytes + (uint32_t)ch * 16u), wf);
+#pragma unroll
+                        for (int tk = 0; tk < B; ++tk)
+#pragma unroll
+                            for (int e = 0; e < VEC; ++e) part[i][tk] = fmaf(xr[tk][k][e], wf[e], part[i][tk]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NS; ++i)
+#pragma unroll
+            for (int tk = 0; tk < B; ++tk) {
+                const float r = warp_allreduce_sum(part[i][tk]);
+                if (lane == 0) red[((size_t)warp * NS + i) * B + tk] = r;
+            }
+        __syncthreads();  // (A): every thread is past the down phase of group g-1
+        if (tid == 0 && g >= 1 && g - 1 + stages < ngroups) issue(g - 1 + stages);
+        if (tid < NS * B) {
+            const int i = tid / B, tk = tid % B;
+            if (i < n_in) {
+                float sum = 0.f;
+                for (int w = 0; w < NW; ++w) sum += red[((size_t)w * NS + i) * B + tk];
+                // x1 = (x W_up[j]) * v[j]  (Optimization 1; v = 0 for tokens whose |v| < t)
+                as[i * B + tk] = sum * svals[(size_t)(g * NS + i) * B + tk];
+            }
+        }
+        __syncthreads();  // (B)
+
+        // ---- down: y_p += x1_j * W_down[j, own chunks] ----
+#pragma unroll
+        for (int i = 0; i < NS; ++i) {
+            if (i < n_in) {
+                float a[B];
+#pragma unroll
+                for (int tk = 0; tk < B; ++tk) a[tk] = as[i * B + tk];
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    const int ch = tid + k * NT;
+                    if (ch < nch) {
+                        float wf[VEC];
+                        unpack16(lds128(sbase + (uint32_t)(2 * i + 1) * row_bytes + (uint32_t)ch * 16u), wf);
+#pragma unroll
+                        for (int tk = 0; tk < B; ++tk)
+#pragma unroll
+                            for (int e = 0; e < VEC; ++e) yr[tk][k][e] = fmaf(a[tk], wf[e], yr[tk][k][e]);
+                    }
+                }
+            }
+        }
+    }
+
+    // ---- phase 1 output: this CTA's fp32 partial y_p[b][d] ----
+    float *yp = ypart + (size_t)p * B * d;
+#pragma unroll
+    for (int tk = 0; tk < B; ++tk)
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const int ch = tid + k * NT;
+            if (ch < nch) {
+                float4 *dst = reinterpret_cast<float4 *>(yp + (size_t)tk * d + (size_t)ch * VEC);
+#pragma unroll
+                for (int q = 0; q < VEC / 4; ++q)
+                    dst[q] = make_float4(yr[tk][k][4 * q], yr[tk][k][4 * q + 1], yr[tk][k][4 * q + 2], yr[tk][k][4 * q + 3]);
+            }
+        }
+}
+
+// K3: y[b][d] = sum_{p=0}^{P-1} y_p[b][d] in a fixed order: lane l of the warp owning a float4
+// column group adds p = l, l+32, ... sequentially, then a fixed xor butterfly. Bit-reproducible.
+__global__ void __launch_bounds__(kK3Threads)
+k3_splitk_reduce(const float4 *__restrict__ ypart, int p2, int n4, float4 *__restrict__ y) {
+    pdl_wait_primary();
+    const int lane = threadIdx.x & 31;
+    const int f = (int)((blockIdx.x * (size_t)kK3Threads + threadIdx.x) >> 5);
+    if (f >= n4) return;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int pp = lane; pp < p2; pp += 32) {
+        const float4 v = ypart[(size_t)pp * n4 + f];
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    acc.x = warp_allreduce_sum(acc.x);
+    acc.y = warp_allreduce_sum(acc.y);
+    acc.z = warp_allreduce_sum(acc.z);
+    acc.w = warp_allreduce_sum(acc.w);
+    if (lane == 0) y[f] = acc;
+}
+
+size_t k2_smem_bytes(int esize, int d, int ns, int stages, int b, int l_max, int g1, int threads) {
+    size_t s = (size_t)stages * ns * 2 * (size_t)d * esize;   // ring
+    s += (size_t)stages * 8;                                   // mbarriers
+    s += (size_t)(g1 + 1) * 4;                                 // prefix
+    s += (size_t)l_max * 4 + (size_t)l_max * b * 4;            // slice ids + v
+    s += (size_t)(threads / 32) * ns * b * 4 + (size_t)ns * b * 4;
+    return (s + 127) & ~(size_t)127;
+}
+
+static cudaError_t launch_ex(const void *func, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                             void **args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelExC(&cfg, func, args);
+}
+
+template <typename T, int B, int CPT, int NS, int NT>
+static cudaError_t launch_k2_t(const PlanData &p, const void *x, const void *Wu, const void *Wd, void *ws,
+                               cudaStream_t s, bool pdl) {
+    auto kern = k2_sparse_up_down<T, B, CPT, NS, NT>;
+    const size_t smem = k2_smem_bytes((int)sizeof(T), p.d, NS, p.stages, B, p.l_max, p.g1, NT);
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    char *w = static_cast<char *>(ws);
+    const T *xp = static_cast<const T *>(x);
+    const T *wu = static_cast<const T *>(Wu);
+    const T *wd = static_cast<const T *>(Wd);
+    int d = p.d, m = p.m, g1 = p.g1, p2 = p.p2, stages = p.stages, l_max = p.l_max;
+    const int32_t *idx = reinterpret_cast<const int32_t *>(w + p.off_idx);
+    const float *vals = reinterpret_cast<const float *>(w + p.off_vals);
+    const int32_t *cnt = reinterpret_cast<const int32_t *>(w + p.off_cnt);
+    float *ypart = reinterpret_cast<float *>(w + p.off_ypart);
+    void *args[] = {&xp, &wu, &wd, &d, &m, &g1, &p2, &stages, &l_max, &idx, &vals, &cnt, &ypart};
+    return launch_ex(reinterpret_cast<const void *>(kern), dim3(p.p2), dim3(NT), smem, s, pdl, args);
+}
+
+// Dispatch: NS = 2 neurons per stage; NT = 256 threads for b <= 2 (x and y partials in
+// registers: 2*b*CPT*VEC floats per thread), 512 for larger batches.
+template <typename T, int B>
+static cudaError_t launch_k2_b(const PlanData &p, const void *x, const void *Wu, const void *Wd, void *ws,
+                               cudaStream_t s, bool pdl) {
+    constexpr int NT = B <= 2 ? 256 : 512;
+    switch (p.cpt) {
+        case 1: return launch_k2_t<T, B, 1, 2, NT>(p, x, Wu, Wd, ws, s, pdl);
+        case 2: return launch_k2_t<T, B, 2, 2, NT>(p, x, Wu, Wd, ws, s, pdl);
+        case 3: return launch_k2_t<T, B, 3, 2, NT>(p, x, Wu, Wd, ws, s, pdl);
+        case 4: return launch_k2_t<T, B, 4, 2, NT>(p, x, Wu, Wd, ws, s, pdl);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <typename T>
+static cudaError_t launch_k2_dt(const PlanData &p, const void *x, int b, const void *Wu, const void *Wd, void *ws,
+                                cudaStream_t s, bool pdl) {
+    switch (b) {
+        case 1: return launch_k2_b<T, 1>(p, x, Wu, Wd, ws, s, pdl);
+        case 2: return launch_k2_b<T, 2>(p, x, Wu, Wd, ws, s, pdl);
+        case 3: return launch_k2_b<T, 3>(p, x, Wu, Wd, ws, s, pdl);
+        case 4: return launch_k2_b<T, 4>(p, x, Wu, Wd, ws, s, pdl);
+        case 5: return launch_k2_b<T, 5>(p, x, Wu, Wd, ws, s, pdl);
+        case 6: return launch_k2_b<T, 6>(p, x, Wu, Wd, ws, s, pdl);
+        case 7: return launch_k2_b<T, 7>(p, x, Wu, Wd, ws, s, pdl);
+        case 8: return launch_k2_b<T, 8>(p, x, Wu, Wd, ws, s, pdl);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_k2(const PlanData &p, const void *x, int b, const void *Wu, const void *Wd, void *ws,
+                      cudaStream_t s, bool pdl) {
+    if (p.dt == CATS_BF16) return launch_k2_dt<bf16_bits>(p, x, b, Wu, Wd, ws, s, pdl);
+    return launch_k2_dt<float>(p, x, b, Wu, Wd, ws, s, pdl);
+}
+
+cudaError_t launch_k3(const PlanData &p, int b, const void *ws, float *y, cudaStream_t s, bool pdl) {
+    const char *w = static_cast<const char *>(ws);
+    const float4 *ypart = reinterpret_cast<const float4 *>(w + p.off_ypart);
+    int p2 = p.p2;
+    int n4 = b * p.d / 4;
+    float4 *y4 = reinterpret_cast<float4 *>(y);
+    const int warps_per_block = kK3Threads / 32;
+    const int grid = (n4 + warps_per_block - 1) / warps_per_block;
+    void *args[] = {&ypart, &p2, &n4, &y4};
+    return launch_ex(reinterpret_cast<const void *>(k3_splitk_reduce), dim3(grid), dim3(kK3Threads), 0, s, pdl,
+                     args);
+}
+
+}  // namespace cats

@@ -1,0 +1,209 @@
+"""C-ABI boundary tests that need no GPU: the library loads, exports every symbol include/cats.h
+declares, validates arguments before touching CUDA, plans shapes, and its host-side calibration
+logic (rank rule, window steering, refinement) converges to the oracle's order statistic when the
+device histogram pass is emulated with numpy."""
+import ctypes
+import math
+import os
+import re
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+import cats_synth
+import oracle
+import paper_2404_08763_b200 as cats
+from paper_2404_08763_b200 import _lib
+from tests.conftest import ROOT
+
+lib = _lib.load()
+FAKE = 0x10000  # 16-byte aligned non-null "device" pointer; validation never dereferences it
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "cats.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(cats_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported():
+    names = header_functions()
+    assert len(names) >= 18
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_lib.exported_symbols())
+    assert lib.cats_version() == 1
+
+
+def test_status_strings():
+    for code, name in enumerate(_lib.STATUS):
+        assert lib.cats_status_string(code).decode() == name
+    assert lib.cats_status_string(99).decode() == "CATS_E_UNKNOWN"
+
+
+def test_rank_rule_exact():
+    for k in [0.0, 0.1, 0.25, 0.5, 0.7, 0.9, 0.99, 1e-300, 5e-324, 0.9999999999999999]:
+        for n in [0, 1, 2, 3, 10, 1000, 2**31 + 7, 11272192000, 2**63 + 5]:
+            assert cats.cats_calib_rank(k, n) == math.ceil(Fraction(k) * n), (k, n)
+            assert cats.cats_calib_rank(k, n) == oracle.rank(k, n)
+    for bad in [1.0, 1.5, -0.1, float("nan")]:
+        with pytest.raises(cats.CatsError) as e:
+            cats.cats_calib_rank(bad, 10)
+        assert e.value.name == "CATS_E_SPARSITY"
+
+
+def test_plan_without_gpu():
+    p = cats.MlpPlan(4096, 14336, max_batch=1, dtype=torch.bfloat16, num_sms=148)
+    i = p.info
+    assert i["k1_grid"] == 148 and i["k2_grid"] == 148 and i["k2_stages"] >= 2
+    assert i["k2_smem"] <= 227 * 1024 and i["k1_smem_max"] <= 227 * 1024
+    assert i["workspace_bytes"] >= 148 * 4096 * 4
+    toy = cats.MlpPlan(64, 176, max_batch=1, dtype=torch.float32, num_sms=148)
+    assert toy.info["k1_grid"] == 148
+    small = cats.MlpPlan(64, 5, max_batch=8, dtype=torch.float32, num_sms=148)
+    assert small.info["k1_grid"] == 5
+
+
+@pytest.mark.parametrize("args,err", [
+    ((0, 100, 1, torch.bfloat16), "CATS_E_SHAPE"),
+    ((64, 0, 1, torch.bfloat16), "CATS_E_SHAPE"),
+    ((4100, 100, 1, torch.bfloat16), "CATS_E_ALIGN"),
+    ((66, 100, 1, torch.float32), "CATS_E_ALIGN"),
+    ((64, 100, 0, torch.bfloat16), "CATS_E_BATCH"),
+    ((64, 100, 9, torch.bfloat16), "CATS_E_BATCH"),
+    ((65536, 100, 1, torch.bfloat16), "CATS_E_UNSUPPORTED"),
+])
+def test_plan_errors(args, err):
+    with pytest.raises(cats.CatsError) as e:
+        cats.MlpPlan(*args, num_sms=148)
+    assert e.value.name == err
+
+
+def _decode_rc(plan, x=FAKE, b=1, wg=FAKE, wu=FAKE, wd=FAKE, t=0.1, y=FAKE, ws=FAKE, wsb=None):
+    wsb = plan.workspace_bytes if wsb is None else wsb
+    return lib.cats_status_string(lib.cats_mlp_decode(plan.handle, x, b, wg, wu, wd, t, y, ws, wsb, None)).decode()
+
+
+def test_decode_validation_precedes_cuda():
+    p = cats.MlpPlan(256, 512, max_batch=4, dtype=torch.bfloat16, num_sms=148)
+    assert _decode_rc(p, x=None) == "CATS_E_NULL"
+    assert _decode_rc(p, wd=None) == "CATS_E_NULL"
+    assert _decode_rc(p, y=None) == "CATS_E_NULL"
+    assert _decode_rc(p, b=0) == "CATS_E_BATCH"
+    assert _decode_rc(p, b=5) == "CATS_E_BATCH"
+    assert _decode_rc(p, wsb=p.workspace_bytes - 1) == "CATS_E_WORKSPACE"
+    assert _decode_rc(p, ws=None) == "CATS_E_WORKSPACE"
+    assert _decode_rc(p, x=FAKE + 8) == "CATS_E_ALIGN"
+    assert _decode_rc(p, wu=FAKE + 2) == "CATS_E_ALIGN"
+    assert _decode_rc(p, t=-0.5) == "CATS_E_THRESHOLD"
+    assert _decode_rc(p, t=float("nan")) == "CATS_E_THRESHOLD"
+    assert _decode_rc(p, t=float("inf")) == "CATS_E_THRESHOLD"
+    if not torch.cuda.is_available():
+        # valid arguments reach CUDA, which reports the missing device as a status, not a crash
+        assert _decode_rc(p) == "CATS_E_CUDA"
+        assert lib.cats_last_cuda_error().decode() != ""
+    rc = lib.cats_mlp_dense(p.handle, FAKE, 9, FAKE, FAKE, FAKE, FAKE, FAKE, p.workspace_bytes, None)
+    assert lib.cats_status_string(rc).decode() == "CATS_E_BATCH"
+    rc = lib.cats_mlp_gate_act(p.handle, None, 1, FAKE, FAKE, FAKE, p.workspace_bytes, None)
+    assert lib.cats_status_string(rc).decode() == "CATS_E_NULL"
+
+
+def test_calibrate_validation():
+    t = ctypes.c_float(-1.0)
+    wsb = cats.cats_calibrate_workspace_bytes(100, torch.bfloat16)
+    assert wsb >= 32768 * 8
+
+    def rc(acts=FAKE, n=100, dt=1, k=0.5, ws=FAKE, wsb=wsb, tout=ctypes.byref(t)):
+        return lib.cats_status_string(lib.cats_calibrate_threshold(acts, n, dt, k, ws, wsb, None, tout, None)).decode()
+
+    assert rc(acts=None) == "CATS_E_NULL"
+    assert rc(tout=None) == "CATS_E_NULL"
+    assert rc(dt=7) == "CATS_E_DTYPE"
+    assert rc(k=1.0) == "CATS_E_SPARSITY"
+    assert rc(k=-0.1) == "CATS_E_SPARSITY"
+    assert rc(k=float("nan")) == "CATS_E_SPARSITY"
+    assert rc(n=0) == "CATS_E_EMPTY"
+    assert rc(acts=FAKE + 4) == "CATS_E_ALIGN"
+    assert rc(wsb=wsb - 1) == "CATS_E_WORKSPACE"
+    assert t.value == -1.0  # untouched on error
+
+
+# ---------------------------------------------------------------- host calibration logic (numpy pass)
+
+def _keys(acts: np.ndarray):
+    if acts.dtype == np.uint16:
+        return (acts.astype(np.uint32) & 0x7FFF), 0x7F80, 8
+    return (acts.view(np.uint32) & 0x7FFFFFFF), 0x7F800000, 4
+
+
+def emulated_pass(acts: np.ndarray, w):
+    """numpy stand-in for the device pass cats_calib_hist (same contract as include/cats.h)."""
+    keys, inf, per = _keys(acts)
+    if w.sample_stride:
+        nvec = acts.size // per
+        vsel = np.arange(0, nvec, w.sample_stride)
+        keys = keys[: nvec * per].reshape(nvec, per)[vsel].reshape(-1)
+    fin = keys < inf
+    kf = keys[fin]
+    below = int((kf < w.lo).sum())
+    above = int((kf > w.hi).sum())
+    inw = kf[(kf >= w.lo) & (kf <= w.hi)]
+    hist = np.bincount(((inw - w.lo) >> w.shift).astype(np.int64), minlength=w.nbins).astype(np.uint64)
+    counts = np.array([below, inw.size, above, int((~fin).sum())], np.uint64)
+    return hist, counts
+
+
+def emulated_calibrate(acts: np.ndarray, k: float):
+    dtype = torch.bfloat16 if acts.dtype == np.uint16 else torch.float32
+    w = cats.cats_calib_window_init(acts.size, dtype)
+    passes = 0
+    for _ in range(32):
+        hist, counts = emulated_pass(acts, w)
+        if not w.sample_stride:
+            passes += 1
+        done, tb, lt, le = cats.cats_calib_step(hist, counts, acts.size, dtype, k, w)
+        if done:
+            bits = np.uint32(tb << 16) if dtype == torch.bfloat16 else np.uint32(tb)
+            return float(np.array([bits], np.uint32).view(np.float32)[0]), lt, le, passes
+    raise AssertionError("no convergence")
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("n", [1, 7, 1000, 50_000, 20_000_000])
+def test_host_select_matches_oracle(dtype, n):
+    if n > 1_000_000 and dtype == torch.float32:
+        n = 9_000_000
+    acts_t = cats_synth.calib_acts(n, dtype, seed=n % 97, heavy=(n % 2 == 0))
+    acts = cats_synth.to_oracle(acts_t)
+    ks = [0.0, 0.5, 0.9] if n > 1_000_000 else [0.0, 0.1, 0.5, 0.7, 0.9, 0.99]
+    for k in ks:
+        t, lt, le, passes = emulated_calibrate(acts, k)
+        if dtype == torch.bfloat16 and n > 1_000_000:
+            ref = oracle.calibrate_bf16_counts(oracle.bf16_counts(acts), k)
+        else:
+            ref = oracle.calibrate_sort(acts, k)
+        assert (t, lt, le) == (ref.t, ref.count_lt, ref.count_le), (k, t, ref)
+        if dtype == torch.bfloat16:
+            assert passes <= 2
+
+
+def test_host_select_adversarial():
+    # all equal, sorted, ties across the window, signed zeros, tiny subnormals
+    cases = [np.full(100_000, 0x3E00, np.uint16),
+             np.sort(cats_synth.bf16_bits(cats_synth.calib_acts(30_000_000, torch.bfloat16, seed=3))),
+             np.repeat(np.array([0x0000, 0x8000, 0x0001, 0x3F80], np.uint16), 5_000_000)]
+    for acts in cases:
+        for k in [0.0, 0.2, 0.5, 0.75, 0.999]:
+            t, lt, le, _ = emulated_calibrate(acts, k)
+            ref = oracle.calibrate_bf16_counts(oracle.bf16_counts(acts), k)
+            assert (t, lt, le) == (ref.t, ref.count_lt, ref.count_le)
+
+
+def test_host_select_nonfinite():
+    acts = cats_synth.bf16_bits(cats_synth.calib_acts(5000, torch.bfloat16, seed=1)).copy()
+    acts[1234] = 0x7FC0  # NaN
+    with pytest.raises(cats.CatsError) as e:
+        emulated_calibrate(acts, 0.5)
+    assert e.value.name == "CATS_E_NONFINITE"

@@ -1,0 +1,276 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on identical seeded inputs.
+
+Acceptance (BASELINE.json north_star):
+  * active-neuron sets bit-exact with the oracle except entries with ||SiLU64| - t| <= 1e-3 t;
+  * y relative L2 <= 2e-3 vs the oracle recomputed with the GPU's keep decisions substituted on
+    those band entries only (reading R9);
+  * calibration threshold bit-exact with the oracle's order statistic (and its counts).
+"""
+import numpy as np
+import pytest
+import torch
+
+import cats_synth
+import oracle
+import paper_2404_08763_b200 as cats
+
+pytestmark = pytest.mark.gpu
+
+BAND = 1e-3
+Y_TOL = 2e-3
+
+
+def _dev(t):
+    return t.to("cuda").contiguous()
+
+
+def _keep_from_gpu(idx, tm, b, m):
+    keep = np.zeros((b, m), np.uint8)
+    for tk in range(b):
+        keep[tk, idx[((tm >> tk) & 1).astype(bool)]] = 1
+    return keep
+
+
+def _rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def run_parity(d, m, b, dtype, k, seed=0, heavy=False, num_sms=0, check_y=True):
+    Wg, Wu, Wd = cats_synth.mlp_weights(d, m, dtype, layer=seed, heavy=heavy)
+    x = cats_synth.tokens(b, d, dtype, seed=1 + seed, heavy=heavy)
+    ox, og, ou, od = (cats_synth.to_oracle(a) for a in (x, Wg, Wu, Wd))
+    # threshold: Eq. 3 on the oracle's |SiLU| of these tokens (any t >= 0 is a valid test point)
+    _, v64, _ = oracle.mlp(ox, og, ou, od, t=0.0, mode=oracle.DENSE)
+    t = float(oracle.calibrate_sort(v64.astype(np.float32), k).t) if k > 0 else 0.0
+
+    plan = cats.MlpPlan(d, m, max_batch=b, dtype=dtype, num_sms=num_sms)
+    ws = plan.workspace()
+    dx, dg, du, dd = (_dev(a) for a in (x, Wg, Wu, Wd))
+    y = cats.cats_mlp_decode(plan, dx, dg, du, dd, t, ws=ws)
+    torch.cuda.synchronize()
+    idx, tm, per = cats.cats_mlp_last_active(plan, ws, b)
+    assert (np.diff(idx) > 0).all(), "active list must be strictly ascending"
+    assert (tm != 0).all()
+    keep_gpu = _keep_from_gpu(idx, tm, b, m)
+    assert (keep_gpu.sum(1) == per).all()
+
+    keep64 = (np.abs(v64) >= np.float64(t)).astype(np.uint8)
+    band = np.abs(np.abs(v64) - t) <= BAND * t
+    mism = (keep_gpu != keep64) & ~band
+    assert not mism.any(), f"{int(mism.sum())} active-set mismatches outside the band"
+    res = {"t": t, "band": int(band.sum()), "flips_in_band": int(((keep_gpu != keep64) & band).sum()),
+           "nnz_union": len(idx), "sparsity": 1 - keep_gpu.mean()}
+    if check_y:
+        keep_sub = np.where(band, keep_gpu, keep64).astype(np.uint8)
+        y_ref, _, _ = oracle.mlp(ox, og, ou, od, t=t, keep_in=keep_sub)
+        yg = y.cpu().numpy().astype(np.float64)
+        errs = [_rel_l2(yg[i], y_ref[i]) if np.abs(y_ref[i]).max() > 0 else float(np.abs(yg[i]).max())
+                for i in range(b)]
+        res["rel_l2_max"] = max(errs)
+        assert max(errs) <= Y_TOL, errs
+    return res, (plan, ws, dx, dg, du, dd, y)
+
+
+@pytest.mark.parametrize("d,m,b,dtype,k", [
+    (64, 176, 1, torch.float32, 0.5),        # BASELINE config 0 (toy)
+    (64, 176, 3, torch.float32, 0.7),
+    (264, 1000, 1, torch.bfloat16, 0.5),     # ragged: 33 chunks per row, m not a multiple of anything
+    (264, 1000, 2, torch.bfloat16, 0.9),
+    (512, 3001, 5, torch.bfloat16, 0.7),
+    (1024, 4096, 8, torch.bfloat16, 0.5),
+    (8192, 512, 1, torch.bfloat16, 0.5),     # widest supported row (4 chunks per K2 thread)
+    (128, 7, 4, torch.bfloat16, 0.5),        # m < number of SMs
+    (8, 1, 1, torch.float32, 0.0),           # a single neuron, one 32-byte row
+])
+def test_parity_small(d, m, b, dtype, k):
+    res, _ = run_parity(d, m, b, dtype, k, seed=d + m + b)
+    assert res["rel_l2_max"] <= Y_TOL
+
+
+@pytest.mark.parametrize("model,b,k,heavy", [
+    ("mistral-7b", 1, 0.5, False),           # BASELINE config 1 (bench workload)
+    ("mistral-7b", 8, 0.5, True),
+    ("llama2-7b", 1, 0.7, False),            # config 2
+    ("llama2-7b", 4, 0.9, True),
+    ("llama2-13b", 1, 0.5, False),           # config 3, unsharded
+])
+def test_parity_full_size(model, b, k, heavy):
+    d, m = cats_synth.MODELS[model]
+    res, _ = run_parity(d, m, b, torch.bfloat16, k, seed=7, heavy=heavy)
+    assert res["rel_l2_max"] <= Y_TOL
+    if b == 1:
+        assert abs(res["sparsity"] - k) < 0.01
+
+
+def test_t0_and_dense_path():
+    d, m, b = 512, 2000, 3
+    res, (plan, ws, dx, dg, du, dd, y) = run_parity(d, m, b, torch.bfloat16, 0.0, seed=3)
+    assert res["nnz_union"] == m
+    y_dense = cats.cats_mlp_dense(plan, dx, dg, du, dd, ws=ws)
+    y0 = cats.cats_mlp_decode(plan, dx, dg, du, dd, 0.0, ws=ws)
+    assert torch.equal(y_dense, y0)
+    # dense vs oracle Eq. 1
+    ox, og, ou, od = (cats_synth.to_oracle(a.cpu()) for a in (dx, dg, du, dd))
+    y_ref, _, _ = oracle.mlp(ox, og, ou, od, t=0.0, mode=oracle.DENSE)
+    assert _rel_l2(y_dense.cpu().numpy().astype(np.float64), y_ref) < 1e-5
+
+
+def test_threshold_above_every_activation_gives_zero():
+    d, m = 256, 600
+    Wg, Wu, Wd = (_dev(a) for a in cats_synth.mlp_weights(d, m, torch.bfloat16))
+    x = _dev(cats_synth.tokens(2, d, torch.bfloat16))
+    plan = cats.MlpPlan(d, m, max_batch=2)
+    ws = plan.workspace()
+    y = cats.cats_mlp_decode(plan, x, Wg, Wu, Wd, 1e30, ws=ws)
+    idx, tm, per = cats.cats_mlp_last_active(plan, ws, 2)
+    assert len(idx) == 0 and not per.any()
+    assert not y.any()
+
+
+def test_deterministic_bitwise():
+    d, m = 4096, 14336
+    Wg, Wu, Wd = (_dev(a) for a in cats_synth.mlp_weights(d, m, torch.bfloat16))
+    plan = cats.MlpPlan(d, m, max_batch=8)
+    ws = plan.workspace()
+    for b in (1, 8):
+        x = _dev(cats_synth.tokens(b, d, torch.bfloat16, seed=11))
+        ys = [cats.cats_mlp_decode(plan, x, Wg, Wu, Wd, 0.0994, ws=ws).clone() for _ in range(10)]
+        assert all(torch.equal(ys[0], yi) for yi in ys[1:])
+
+
+def test_gate_act_matches_oracle_silu():
+    d, m, b = 4096, 11008, 4
+    Wg, Wu, Wd = cats_synth.mlp_weights(d, m, torch.bfloat16)
+    x = cats_synth.tokens(b, d, torch.bfloat16, seed=5)
+    plan = cats.MlpPlan(d, m, max_batch=b)
+    acts = cats.cats_mlp_gate_act(plan, _dev(x), _dev(Wg)).cpu().numpy()
+    ox, og = cats_synth.to_oracle(x), cats_synth.to_oracle(Wg)
+    z = np.zeros((m, d), np.uint16)
+    _, v64, _ = oracle.mlp(ox, og, z, z, t=0.0, mode=oracle.DENSE)
+    err = np.abs(acts - v64)
+    assert err.max() < 1e-5 * np.abs(v64).max() + 1e-7
+
+
+def test_decode_host_equals_device_path():
+    d, m, b = 4096, 14336, 2
+    Wg, Wu, Wd = (_dev(a) for a in cats_synth.mlp_weights(d, m, torch.bfloat16))
+    x = cats_synth.tokens(b, d, torch.bfloat16, seed=9)
+    plan = cats.MlpPlan(d, m, max_batch=b)
+    ws = plan.workspace()
+    y_dev = cats.cats_mlp_decode(plan, _dev(x), Wg, Wu, Wd, 0.1, ws=ws).cpu()
+    y_host = cats.cats_mlp_decode_host(plan, x.pin_memory(), Wg, Wu, Wd, 0.1, ws=ws)
+    assert torch.equal(y_dev, y_host)
+
+
+def test_tensor_parallel_emulated_on_one_gpu():
+    """TP along m: P shard plans with the same layer-global t; the sum of the
+    partial y equals the unsharded oracle (the all-reduce is a plain sum)."""
+    d, m, b, P = 5120, 13824, 1, 4
+    Wg, Wu, Wd = cats_synth.mlp_weights(d, m, torch.bfloat16)
+    x = cats_synth.tokens(b, d, torch.bfloat16, seed=13)
+    ox, og, ou, od = (cats_synth.to_oracle(a) for a in (x, Wg, Wu, Wd))
+    _, v64, _ = oracle.mlp(ox, og, ou, od, t=0.0, mode=oracle.DENSE)
+    t = float(oracle.calibrate_sort(v64.astype(np.float32), 0.5).t)
+    ysum = torch.zeros(b, d, dtype=torch.float64)
+    keep_gpu = np.zeros((b, m), np.uint8)
+    ms = m // P
+    for r in range(P):
+        sl = slice(r * ms, (r + 1) * ms)
+        plan = cats.MlpPlan(d, ms, max_batch=b)
+        ws = plan.workspace()
+        y = cats.cats_mlp_decode(plan, _dev(x), _dev(Wg[sl]), _dev(Wu[sl]), _dev(Wd[sl]), t, ws=ws)
+        idx, tm, _ = cats.cats_mlp_last_active(plan, ws, b)
+        keep_gpu[:, sl] = _keep_from_gpu(idx, tm, b, ms)
+        ysum += y.cpu().double()
+    keep64 = (np.abs(v64) >= t).astype(np.uint8)
+    band = np.abs(np.abs(v64) - t) <= BAND * t
+    assert not ((keep_gpu != keep64) & ~band).any()
+    y_ref, _, _ = oracle.mlp(ox, og, ou, od, t=t, keep_in=np.where(band, keep_gpu, keep64).astype(np.uint8))
+    assert _rel_l2(ysum.numpy(), y_ref) <= Y_TOL
+
+
+# ------------------------------------------------------------------------------------ calibration
+
+def _oracle_t(acts_cpu, k):
+    a = cats_synth.to_oracle(acts_cpu)
+    if a.dtype == np.uint16 and a.size > 2_000_000:
+        return oracle.calibrate_bf16_counts(oracle.bf16_counts(a), k)
+    return oracle.calibrate_sort(a, k)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("n,heavy", [(1, False), (13, False), (45056, False), (1_000_003, True),
+                                     (40_000_001, False)])
+def test_calibration_bit_exact(dtype, n, heavy):
+    acts = cats_synth.calib_acts(n, dtype, seed=n % 101, heavy=heavy, device="cuda")
+    acts_cpu = acts.cpu()
+    for k in [0.0, 0.5, 0.7, 0.9, 0.99]:
+        t, info = cats.cats_calibrate_threshold(acts, k)
+        ref = _oracle_t(acts_cpu, k)
+        assert t == ref.t, (k, t, ref.t)
+        assert (info["count_lt"], info["count_le"], info["rank_r"]) == (ref.count_lt, ref.count_le, ref.r)
+        if dtype == torch.bfloat16 and n > 1000:
+            assert info["passes"] <= 2
+
+
+def test_calibration_adversarial_and_errors():
+    dev = "cuda"
+    # all equal; signed zeros + subnormals; sorted input (worst case for sampling)
+    cases = [torch.full((3_000_000,), 0.7, dtype=torch.bfloat16, device=dev),
+             torch.tensor([0.0, -0.0, 1e-40, -1e-39, 1.0] * 2_000_000, dtype=torch.float32, device=dev),
+             torch.sort(cats_synth.calib_acts(30_000_000, torch.bfloat16, seed=2, device=dev).abs())[0]]
+    for acts in cases:
+        for k in [0.0, 0.3, 0.5, 0.999]:
+            t, info = cats.cats_calibrate_threshold(acts, k)
+            ref = _oracle_t(acts.cpu(), k)
+            assert (t, info["count_lt"], info["count_le"]) == (ref.t, ref.count_lt, ref.count_le)
+    bad = cats_synth.calib_acts(100_000, torch.bfloat16, device=dev)
+    bad[77_777] = float("inf")
+    with pytest.raises(cats.CatsError) as e:
+        cats.cats_calibrate_threshold(bad, 0.5)
+    assert e.value.name == "CATS_E_NONFINITE"
+    with pytest.raises(cats.CatsError) as e:
+        cats.cats_calibrate_threshold(bad[1:], 0.5)  # misaligned view
+    assert e.value.name == "CATS_E_ALIGN"
+
+
+def test_calibration_achieved_sparsity_on_gpu_activations():
+    """Calibrate on GPU-collected |SiLU(x W_gate)| of 256 tokens, then the fraction of zeroed
+    entries on the calibration set obeys count_lt < kN <= count_le and held-out tokens reach ~k."""
+    d, m = 4096, 11008
+    Wg, Wu, Wd = (_dev(a) for a in cats_synth.mlp_weights(d, m, torch.bfloat16))
+    plan = cats.MlpPlan(d, m, max_batch=8)
+    ws = plan.workspace()
+    acts = torch.cat([cats.cats_mlp_gate_act(plan, _dev(cats_synth.tokens(8, d, torch.bfloat16, seed=100 + i)), Wg,
+                                             ws=ws) for i in range(32)])
+    for k in [0.5, 0.7, 0.9]:
+        t, info = cats.cats_calibrate_threshold(acts, k)
+        n = acts.numel()
+        assert info["count_lt"] < k * n <= info["count_le"]
+        assert int((acts.abs() < t).sum()) == info["count_lt"]
+        x = _dev(cats_synth.tokens(8, d, torch.bfloat16, seed=999))
+        cats.cats_mlp_decode(plan, x, Wg, Wu, Wd, t, ws=ws)
+        _, _, per = cats.cats_mlp_last_active(plan, ws, 8)
+        assert abs((1 - per / m).mean() - k) < 0.02
+
+
+@pytest.mark.slow
+def test_calibration_full_size_config4():
+    """BASELINE config 4: 500 samples x 2048 tokens x 11008 channels of bf16 (22.5 GB) on the GPU;
+    oracle = exact multiset order statistic over the identical bytes (streamed to host)."""
+    n = 500 * 2048 * 11008
+    free, _ = torch.cuda.mem_get_info()
+    if free < n * 2 + (4 << 30):
+        pytest.skip("not enough device memory")
+    acts = cats_synth.calib_acts(n, torch.bfloat16, seed=0, device="cuda")
+    counts = np.zeros(65536, np.uint64)
+    chunk = 1 << 30
+    for s in range(0, n, chunk):
+        oracle.bf16_counts(cats_synth.bf16_bits(acts[s:s + chunk].cpu()), counts)
+    for k in [0.5, 0.7, 0.9]:
+        t, info = cats.cats_calibrate_threshold(acts, k)
+        ref = oracle.calibrate_bf16_counts(counts, k)
+        assert (t, info["count_lt"], info["count_le"]) == (ref.t, ref.count_lt, ref.count_le)
+        assert info["passes"] <= 2
+    del acts
+    torch.cuda.empty_cache()
