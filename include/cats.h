@@ -22,7 +22,8 @@
  *   - Every device pointer is 16-byte aligned and d * sizeof(dtype) is a multiple of 16
  *     (d % 8 == 0 for bf16, d % 4 == 0 for fp32): 128-bit loads and cp.async.bulk need it.
  *   - Ownership: the caller owns every buffer (torch allocates them); a plan owns only host
- *     metadata. Workspace contents persist until the next call that uses the workspace.
+ *     metadata. A decode workspace is initialised once (cats_mlp_workspace_init); its contents
+ *     persist until the next call that uses it.
  *   - Concurrency: plans are immutable and may be shared by threads; concurrent calls need
  *     distinct workspaces and outputs.
  *   - Errors: every entry point returns a cats_status_t; nothing throws or aborts across the
@@ -162,6 +163,8 @@ typedef struct {
     cats_dtype_t w_dtype;
     int device, num_sms;
     int k1_grid, k1_threads;      /* K1: gate GEMV + SiLU + threshold + compaction */
+    int k1_rows_per_tile;         /* W_gate rows per dynamically scheduled tile (= ring stage) */
+    int k1_stages;                /* K1 ring depth */
     int k2_grid, k2_threads;      /* K2: sparse up x v + down, per-CTA split-K partials */
     int k2_neurons_per_stage;     /* neurons per smem ring stage (W_up row + W_down row each) */
     int k2_stages;                /* ring depth */
@@ -181,6 +184,10 @@ cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_dtype_t w_d
 void cats_mlp_plan_destroy(cats_mlp_plan_t *plan);
 cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_mlp_plan_info_t *info);
 cats_status_t cats_mlp_workspace_bytes(const cats_mlp_plan_t *plan, size_t *bytes);
+/* Initialise a freshly allocated workspace once (zeroes K1's tile-scheduler counters, which every
+ * K1 launch leaves zeroed again on exit). Required before the first call that uses `ws`.
+ * Asynchronous on s. Errors: CATS_E_NULL, CATS_E_WORKSPACE, CATS_E_ALIGN, CATS_E_CUDA. */
+cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, void *ws, size_t ws_bytes, cats_stream_t s);
 
 /* y[b][d] = CATS_t gated MLP of x[b][d] over this plan's m neurons (under tensor parallelism y
  * is the rank's partial; the caller all-reduces). t >= 0; t = 0 gives dense semantics.

@@ -153,8 +153,12 @@ class MlpPlan:
     def workspace_bytes(self) -> int:
         return self.info["workspace_bytes"]
 
-    def workspace(self) -> torch.Tensor:
-        return torch.empty(self.workspace_bytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+    def workspace(self, stream=None) -> torch.Tensor:
+        """Allocate and initialise (cats_mlp_workspace_init) a decode workspace."""
+        ws = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+        rc = self._lib.cats_mlp_workspace_init(self.handle, ws.data_ptr(), ws.numel(), _stream(stream, ws.device))
+        _check(rc, "cats_mlp_workspace_init")
+        return ws
 
     def __del__(self):
         h = getattr(self, "_h", None)

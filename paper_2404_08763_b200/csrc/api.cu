@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -278,6 +279,48 @@ extern "C" cats_status_t cats_calibrate_threshold(const void *acts, uint64_t n, 
 }
 
 // =============================================================================== planning
+namespace cats {
+
+static std::mutex g_attr_mu;
+static std::vector<std::pair<const void *, size_t>> g_attr;  // (kernel, configured smem) per process
+
+cudaError_t ensure_smem_attr(const void *func, size_t smem) {
+    if (smem <= 48 * 1024) return cudaSuccess;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const void *key = reinterpret_cast<const char *>(func) + dev;  // distinct per device
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    for (auto &kv : g_attr)
+        if (kv.first == key && kv.second >= smem) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    g_attr.emplace_back(key, smem);
+    return cudaSuccess;
+}
+
+int k1_stages(const PlanData &p, int b) {
+    const size_t stage = (size_t)k1_rows_per_tile(b) * p.d * p.esize;
+    const size_t extra = 2 * (size_t)(kK1Threads / 32) * k1_rows_per_tile(b) * b * 4 + 1024;
+    const size_t n = (kSmemBudget - extra) / (stage + 16);
+    return (int)std::min<size_t>(n, 12);
+}
+
+int k2_neurons_per_stage(const PlanData &p, int b) {
+    const size_t extra = k2_smem_bytes(p.esize, p.d, 4, 0, b, p.l_max, k1_ntiles(p.m, b)) + 8 * kMaxStages + 256;
+    const size_t stage4 = (size_t)4 * 2 * p.d * p.esize;
+    return extra + 2 * stage4 <= kSmemBudget ? 4 : 2;
+}
+
+int k2_stages(const PlanData &p, int b) {
+    const int ns = k2_neurons_per_stage(p, b);
+    const size_t extra = k2_smem_bytes(p.esize, p.d, ns, 0, b, p.l_max, k1_ntiles(p.m, b)) + 8 * kMaxStages + 256;
+    const size_t stage = (size_t)ns * 2 * p.d * p.esize;
+    if (extra >= kSmemBudget) return 0;
+    return (int)std::min<size_t>((kSmemBudget - extra) / stage, kMaxStages);
+}
+
+}  // namespace cats
+
 extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_dtype_t dt, int device, int num_sms,
                                               cats_mlp_plan_t **out) {
     if (!out) return CATS_E_NULL;
@@ -301,29 +344,24 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.esize = esize;
         p.vec = 16 / esize;
         p.nchunks = d * esize / 16;
-        // K1: one persistent CTA per SM over a contiguous neuron range
-        p.g1 = std::min(num_sms, m);
-        p.r_max = (m + p.g1 - 1) / p.g1;
-        if (k1_smem_bytes(p, max_batch) > kSmemBudget) return CATS_E_UNSUPPORTED;
+        p.cpt = (p.nchunks + 511) / 512;  // K1 and K2 both run 512 threads
+        if (p.cpt > kMaxCPT) return CATS_E_UNSUPPORTED;
+        // K1: one persistent CTA per SM pulling NR-row tiles from a global counter
+        p.g1 = std::min(num_sms, k1_ntiles(m, 1));
         // K2: one persistent CTA per SM; each owns 1/p2 of the active list
         p.p2 = num_sms;
-        p.k2_threads = max_batch <= 2 ? 256 : 512;
-        const int cpt256 = (p.nchunks + 255) / 256, cpt512 = (p.nchunks + 511) / 512;
-        if (cpt256 > kMaxCPT || cpt512 > kMaxCPT) return CATS_E_UNSUPPORTED;
-        p.cpt = p.k2_threads == 256 ? cpt256 : cpt512;
-        p.ns = 2;
         p.l_max = (m + p.p2 - 1) / p.p2;
-        const size_t stage = (size_t)p.ns * 2 * (size_t)d * esize;
-        const size_t extra = k2_smem_bytes(esize, d, p.ns, 0, max_batch, p.l_max, p.g1, 512) + 8 * 8;
-        if (extra + 2 * stage > kSmemBudget) return CATS_E_UNSUPPORTED;
-        p.stages = (int)std::min<size_t>(8, (kSmemBudget - extra) / stage);
-        p.k2_smem = k2_smem_bytes(esize, d, p.ns, p.stages, max_batch, p.l_max, p.g1, 512);
+        for (int b = 1; b <= max_batch; ++b) {
+            if (k1_stages(p, b) < 2 || k1_smem_bytes(p, b) > kSmemBudget) return CATS_E_UNSUPPORTED;
+            if (k2_stages(p, b) < 2) return CATS_E_UNSUPPORTED;
+        }
         // workspace
         size_t off = 0;
+        p.off_sched = off;   off = align_up(off + 64, 256);
         p.off_idx = off;     off = align_up(off + (size_t)m * 4, 256);
         p.off_tokmask = off; off = align_up(off + (size_t)m, 256);
         p.off_vals = off;    off = align_up(off + (size_t)m * max_batch * 4, 256);
-        p.off_cnt = off;     off = align_up(off + (size_t)p.g1 * 4, 256);
+        p.off_cnt = off;     off = align_up(off + (size_t)k1_ntiles(m, CATS_MAX_BATCH) * 4, 256);
         p.off_ypart = off;   off = align_up(off + (size_t)p.p2 * max_batch * d * 4, 256);
         p.off_xstage = off;  off = align_up(off + (size_t)max_batch * d * esize, 256);
         p.off_ystage = off;  off = align_up(off + (size_t)max_batch * d * 4, 256);
@@ -340,6 +378,7 @@ extern "C" void cats_mlp_plan_destroy(cats_mlp_plan_t *plan) { delete plan; }
 extern "C" cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_mlp_plan_info_t *info) {
     if (!plan || !info) return CATS_E_NULL;
     const PlanData &p = plan->p;
+    const int b = p.max_batch;
     info->d = p.d;
     info->m = p.m;
     info->max_batch = p.max_batch;
@@ -348,14 +387,17 @@ extern "C" cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_ml
     info->num_sms = p.num_sms;
     info->k1_grid = p.g1;
     info->k1_threads = kK1Threads;
+    info->k1_rows_per_tile = k1_rows_per_tile(b);
+    info->k1_stages = k1_stages(p, b);
     info->k2_grid = p.p2;
-    info->k2_threads = p.k2_threads;
-    info->k2_neurons_per_stage = p.ns;
-    info->k2_stages = p.stages;
+    info->k2_threads = kK2Threads;
+    info->k2_neurons_per_stage = k2_neurons_per_stage(p, b);
+    info->k2_stages = k2_stages(p, b);
     info->k3_grid = (p.max_batch * p.d / 4 + kK3Threads / 32 - 1) / (kK3Threads / 32);
     info->k3_threads = kK3Threads;
-    info->k1_smem_max = k1_smem_bytes(p, p.max_batch);
-    info->k2_smem = p.k2_smem;
+    info->k1_smem_max = k1_smem_bytes(p, b);
+    info->k2_smem = k2_smem_bytes(p.esize, p.d, info->k2_neurons_per_stage, info->k2_stages, b, p.l_max,
+                                  k1_ntiles(p.m, b));
     info->workspace_bytes = p.ws_bytes;
     return CATS_OK;
 }
@@ -364,6 +406,17 @@ extern "C" cats_status_t cats_mlp_workspace_bytes(const cats_mlp_plan_t *plan, s
     if (!plan || !bytes) return CATS_E_NULL;
     *bytes = plan->p.ws_bytes;
     return CATS_OK;
+}
+
+extern "C" cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, void *ws, size_t ws_bytes,
+                                                 cats_stream_t s) {
+    if (!plan) return CATS_E_NULL;
+    if (!ws || ws_bytes < plan->p.ws_bytes) return CATS_E_WORKSPACE;
+    if (!aligned16(ws)) return CATS_E_ALIGN;
+    cudaError_t e = cudaSetDevice(plan->p.device);
+    if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_sched, 0, 64,
+                                              static_cast<cudaStream_t>(s));
+    return cuda_status(e);
 }
 
 // =============================================================================== decode
@@ -473,19 +526,20 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
     CATS_TRY({
         cudaStream_t st = static_cast<cudaStream_t>(s);
         const char *w = static_cast<const char *>(ws);
-        std::vector<int32_t> idx(p.m), cnt(p.g1);
+        const int tr = k1_rows_per_tile(b), ntiles = k1_ntiles(p.m, b);
+        std::vector<int32_t> idx(p.m), cnt(ntiles);
         std::vector<uint8_t> tm(p.m);
         cudaError_t e = cudaSetDevice(p.device);
         if (e == cudaSuccess) e = cudaMemcpyAsync(idx.data(), w + p.off_idx, (size_t)p.m * 4, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaMemcpyAsync(tm.data(), w + p.off_tokmask, (size_t)p.m, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(cnt.data(), w + p.off_cnt, (size_t)p.g1 * 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(cnt.data(), w + p.off_cnt, (size_t)ntiles * 4, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return cuda_status(e);
         uint32_t k = 0;
         if (nnz_per_token) std::fill(nnz_per_token, nnz_per_token + b, 0u);
-        for (int c = 0; c < p.g1; ++c) {
-            const int64_t r0 = k1_row0(c, p.m, p.g1);
-            const int64_t R = k1_row0(c + 1, p.m, p.g1) - r0;
+        for (int c = 0; c < ntiles; ++c) {
+            const int64_t r0 = (int64_t)c * tr;
+            const int64_t R = std::min<int64_t>(tr, p.m - r0);
             if (cnt[c] < 0 || cnt[c] > R) return CATS_E_SHAPE;
             for (int i = 0; i < cnt[c]; ++i) {
                 idx_host[k] = idx[r0 + i];

@@ -9,10 +9,12 @@
 
 namespace cats {
 
-constexpr int kK1Threads = 512;       // 16 warps: one CTA per SM, persistent over its row range
+constexpr int kK1Threads = 512;       // 16 warps, one persistent CTA per SM
+constexpr int kK2Threads = 512;       // 16 warps, one persistent CTA per SM
 constexpr int kK3Threads = 256;
 constexpr size_t kSmemBudget = 227 * 1024;  // usable dynamic shared memory per CTA on sm_100
-constexpr int kMaxCPT = 4;            // K2: 16-byte chunks of a row owned per thread
+constexpr int kMaxCPT = 2;            // 16-byte chunks of a row owned per thread (d <= 8192 bf16)
+constexpr int kMaxStages = 8;
 
 struct PlanData {
     int d, m, max_batch;
@@ -21,28 +23,28 @@ struct PlanData {
     int esize;          // bytes per element
     int vec;            // elements per 16 bytes
     int nchunks;        // d * esize / 16
-    // K1
-    int g1;             // CTAs; CTA c owns neuron rows [c*m/g1, (c+1)*m/g1)
-    int r_max;          // max rows per CTA
-    // K2
-    int p2;             // CTAs (split-K slices of the active list)
-    int k2_threads;
-    int cpt;            // chunks per thread
-    int ns;             // neurons per ring stage
-    int stages;         // ring depth
-    size_t k2_smem;
+    int cpt;            // chunks per thread (K1 and K2, 512 threads)
+    int g1;             // K1 CTAs (dynamic tile scheduler)
+    int p2;             // K2 CTAs (split-K slices of the active list)
     int l_max;          // max active neurons per K2 CTA slice
-    // K3
-    int k3_grid_max;
     // workspace layout (byte offsets)
-    size_t off_idx, off_tokmask, off_vals, off_cnt, off_ypart, off_xstage, off_ystage, ws_bytes;
+    size_t off_sched, off_idx, off_tokmask, off_vals, off_cnt, off_ypart, off_xstage, off_ystage, ws_bytes;
 };
 
-// row range of K1 CTA c (shared by K1, K2 and the host introspection: the compaction layout)
-__host__ __device__ inline int64_t k1_row0(int c, int m, int g1) { return (int64_t)c * m / g1; }
+// K1 tile height (rows of W_gate per ring stage) for batch b: keeps the per-thread partial dot
+// products (rows x tokens) in registers.
+__host__ __device__ constexpr int k1_rows_per_tile_c(int b) { return b <= 2 ? 8 : (b <= 4 ? 4 : 2); }
+inline int k1_rows_per_tile(int b) { return k1_rows_per_tile_c(b); }
+inline int k1_ntiles(int m, int b) { return (m + k1_rows_per_tile(b) - 1) / k1_rows_per_tile(b); }
 
 size_t k1_smem_bytes(const PlanData &p, int b);
-size_t k2_smem_bytes(int dt_esize, int d, int ns, int stages, int b, int l_max, int g1, int threads);
+int k1_stages(const PlanData &p, int b);
+size_t k2_smem_bytes(int esize, int d, int ns, int stages, int b, int l_max, int ntiles);
+int k2_neurons_per_stage(const PlanData &p, int b);  // 4, or 2 for very wide rows
+int k2_stages(const PlanData &p, int b);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel / size (thread-safe)
+cudaError_t ensure_smem_attr(const void *func, size_t smem);
 
 // launchers: return cudaError_t of the launch
 cudaError_t launch_k1(const PlanData &p, const void *x, int b, const void *Wg, float t, int dense,

@@ -5,16 +5,17 @@
 // with Optimization 1, the x v multiply fused into the x W_up tile so x1 never touches HBM
 // (P:305-306), and App. D eq. y = (v' * (x W'_up)) W'_down.
 //
-// B200 design:
+// B200 design (K2/K3):
 //  * Only active neurons' rows of W_up and of the neuron-major W_down are read: each is one
 //    contiguous 2d-byte row, moved HBM -> shared memory by the TMA bulk-copy engine
 //    (cp.async.bulk + mbarrier transaction counts) into an S-stage ring, NS neurons per stage.
-//  * The union active list produced by K1 (per-K1-CTA segments) is split into P equal,
-//    contiguous slices, one per persistent CTA: perfect load balance, no atomics.
-//  * Thread t owns fixed 16-byte column chunks {t, t+NT, ...} of d: it keeps x and its slice of
-//    the y partial in registers. The up dot products are reduced across the CTA in a fixed
-//    order (warp butterfly, then warps 0..NW-1), scaled by v (Optimization 1), and broadcast;
-//    the down projection is then a register axpy over the staged W_down rows.
+//  * The union active list produced by K1 (per-tile segments) is split into P equal, contiguous
+//    slices, one per persistent CTA: static and balanced, so every CTA's partial sum has a fixed
+//    composition (bit-reproducible y), and no atomics.
+//  * Thread t owns fixed 16-byte column chunks {t, t+NT, ...} of d: it keeps x and its slice of the
+//    y partial in registers. Per stage: partial up-dots, a fixed xor butterfly per warp, ONE
+//    __syncthreads, then every warp forms the cross-warp sums itself (fixed tree; identical in all
+//    warps), scales by v (Optimization 1) and does the down axpy from the staged W_down rows.
 //  * The paper's fp16 tl.atomic_add into Y is replaced by a deterministic two-phase
 //    split-K: each CTA writes its fp32 partial y_p, K3 sums the P partials in a fixed order.
 #include "cats_device.cuh"
@@ -22,13 +23,16 @@
 
 namespace cats {
 
-template <typename T, int B, int CPT, int NS, int NT>
-__global__ void __launch_bounds__(NT, 1)
+template <typename T, int B, int CPT, int NS>
+__global__ void __launch_bounds__(kK2Threads, 1)
 k2_sparse_up_down(const T *__restrict__ x, const T *__restrict__ Wu, const T *__restrict__ Wd, int d, int m,
-                  int g1, int p2, int stages, int l_max, const int32_t *__restrict__ idx,
+                  int ntiles, int tile_rows, int p2, int stages, int l_max, const int32_t *__restrict__ idx,
                   const float *__restrict__ vals, const int32_t *__restrict__ cnt, float *__restrict__ ypart) {
     constexpr int VEC = VecTraits<T>::kVec;
+    constexpr int NT = kK2Threads;
     constexpr int NW = NT / 32;
+    constexpr int NP = NS * B;
+    static_assert(NW == 16, "cross-warp reduction assumes 16 warps");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int p = blockIdx.x;
     const int nch = d * (int)sizeof(T) / 16;
@@ -36,13 +40,12 @@ k2_sparse_up_down(const T *__restrict__ x, const T *__restrict__ Wu, const T *__
     const uint32_t stage_bytes = (uint32_t)NS * 2u * row_bytes;
 
     extern __shared__ __align__(128) unsigned char smem[];
-    unsigned char *ring = smem;                                                     // [stages][NS][2][row]
+    unsigned char *ring = smem;                                                          // [stages][NS][2][row]
     uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * stage_bytes);  // [stages]
-    int *pref = reinterpret_cast<int *>(full + stages);                             // [g1 + 1]
-    int *slist = pref + (g1 + 1);                                                   // [l_max] neuron ids
-    float *svals = reinterpret_cast<float *>(slist + l_max);                        // [l_max][B]
-    float *red = svals + (size_t)l_max * B;                                         // [NW][NS][B]
-    float *as = red + (size_t)NW * NS * B;                                          // [NS][B]
+    int *pref = reinterpret_cast<int *>(full + stages);                                  // [ntiles + 1]
+    int *slist = pref + (ntiles + 1);                                                    // [l_max] neuron ids
+    float *svals = reinterpret_cast<float *>(slist + l_max);                             // [l_max][B]
+    float *red = svals + (size_t)l_max * B;                                              // [2][NW][NP]
 
     pdl_launch_dependents();
 
@@ -59,8 +62,7 @@ k2_sparse_up_down(const T *__restrict__ x, const T *__restrict__ Wu, const T *__
 #pragma unroll
         for (int tk = 0; tk < B; ++tk) {
             if (ch < nch) {
-                const uint4 r = *reinterpret_cast<const uint4 *>(x + (size_t)tk * d + (size_t)ch * VEC);
-                unpack16(r, xr[tk][k]);
+                unpack16(*reinterpret_cast<const uint4 *>(x + (size_t)tk * d + (size_t)ch * VEC), xr[tk][k]);
             } else {
 #pragma unroll
                 for (int e = 0; e < VEC; ++e) xr[tk][k][e] = 0.f;
@@ -71,40 +73,45 @@ k2_sparse_up_down(const T *__restrict__ x, const T *__restrict__ Wu, const T *__
     // ---- wait for K1 (programmatic dependent launch) ----
     pdl_wait_primary();
 
-    // prefix over K1's per-CTA active counts -> union size U and this CTA's slice [a0, a1)
-    for (int i = tid; i < g1; i += NT) pref[i + 1] = cnt[i];
-    if (tid == 0) pref[0] = 0;
-    __syncthreads();
-    if (warp == 0) {
-        const int per = (g1 + 31) / 32;
-        const int lo = lane * per, hi = min(g1, lo + per);
+    // exclusive prefix over K1's per-tile active counts -> union size U and this CTA's slice
+    {
+        const int per = (ntiles + NT - 1) / NT;
+        const int lo = tid * per, hi = min(ntiles, lo + per);
         int s = 0;
-        for (int i = lo; i < hi; ++i) s += pref[i + 1];
+        for (int i = lo; i < hi; ++i) s += cnt[i];
+        // block exclusive scan of s (warp scan + warp totals)
         int inc = s;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += v;
         }
-        int run = inc - s;
+        __shared__ int wtot[NW];
+        if (lane == 31) wtot[warp] = inc;
+        __syncthreads();
+        int woff = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) woff += (w < warp) ? wtot[w] : 0;
+        int run = woff + inc - s;
         for (int i = lo; i < hi; ++i) {
-            run += pref[i + 1];
-            pref[i + 1] = run;
+            pref[i] = run;
+            run += cnt[i];
         }
+        if (tid == NT - 1) pref[ntiles] = run;
     }
     __syncthreads();
-    const int U = pref[g1];
+    const int U = pref[ntiles];
     const int a0 = (int)((int64_t)p * U / p2), a1 = (int)((int64_t)(p + 1) * U / p2);
     const int L = a1 - a0;
 
-    // gather the slice's neuron ids and v values (global position q -> K1 segment)
+    // gather the slice's neuron ids and v values (global position q -> K1 tile segment)
     for (int q = a0 + tid; q < a1; q += NT) {
-        int lo = 0, hi = g1 - 1;  // largest c with pref[c] <= q
+        int lo = 0, hi = ntiles - 1;  // largest tile with pref[tile] <= q
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (pref[mid] <= q) lo = mid; else hi = mid - 1;
         }
-        const int64_t pos = k1_row0(lo, m, g1) + (q - pref[lo]);
+        const int64_t pos = (int64_t)lo * tile_rows + (q - pref[lo]);
         slist[q - a0] = idx[pos];
 #pragma unroll
         for (int tk = 0; tk < B; ++tk) svals[(size_t)(q - a0) * B + tk] = vals[(size_t)pos * B + tk];
@@ -165,33 +172,37 @@ k2_sparse_up_down(const T *__restrict__ x, const T *__restrict__ Wu, const T *__
                 }
             }
         }
+        float *rb = red + (size_t)(g & 1) * NW * NP;
 #pragma unroll
         for (int i = 0; i < NS; ++i)
 #pragma unroll
             for (int tk = 0; tk < B; ++tk) {
                 const float r = warp_allreduce_sum(part[i][tk]);
-                if (lane == 0) red[((size_t)warp * NS + i) * B + tk] = r;
+                if (lane == 0) rb[warp * NP + i * B + tk] = r;
             }
-        __syncthreads();  // (A): every thread is past the down phase of group g-1
+        __syncthreads();  // red[g&1] complete; every thread is past the down phase of group g-1
         if (tid == 0 && g >= 1 && g - 1 + stages < ngroups) issue(g - 1 + stages);
-        if (tid < NS * B) {
-            const int i = tid / B, tk = tid % B;
-            if (i < n_in) {
-                float sum = 0.f;
-                for (int w = 0; w < NW; ++w) sum += red[((size_t)w * NS + i) * B + tk];
-                // x1 = (x W_up[j]) * v[j]  (Optimization 1; v = 0 for tokens whose |v| < t)
-                as[i * B + tk] = sum * svals[(size_t)(g * NS + i) * B + tk];
-            }
-        }
-        __syncthreads();  // (B)
 
-        // ---- down: y_p += x1_j * W_down[j, own chunks] ----
+        // ---- cross-warp sums, computed redundantly by every warp in one fixed tree:
+        //      lane l reads warp (l & 15)'s partial of pair 2c + (l >> 4); xor 8,4,2,1 sums the 16.
+        float a[NP];
+#pragma unroll
+        for (int c = 0; c < (NP + 1) / 2; ++c) {
+            const int pp = 2 * c + (lane >> 4);
+            float v = (pp < NP) ? rb[(lane & 15) * NP + pp] : 0.f;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            a[2 * c] = __shfl_sync(0xffffffffu, v, 0);
+            if (2 * c + 1 < NP) a[2 * c + 1] = __shfl_sync(0xffffffffu, v, 16);
+        }
+
+        // ---- down: y_p += x1_j * W_down[j, own chunks], x1_j = (x W_up[j]) * v_j (Optimization 1) ----
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
             if (i < n_in) {
-                float a[B];
+                float x1[B];
 #pragma unroll
-                for (int tk = 0; tk < B; ++tk) a[tk] = as[i * B + tk];
+                for (int tk = 0; tk < B; ++tk) x1[tk] = a[i * B + tk] * svals[(size_t)(g * NS + i) * B + tk];
 #pragma unroll
                 for (int k = 0; k < CPT; ++k) {
                     const int ch = tid + k * NT;
@@ -201,7 +212,7 @@ k2_sparse_up_down(const T *__restrict__ x, const T *__restrict__ Wu, const T *__
 #pragma unroll
                         for (int tk = 0; tk < B; ++tk)
 #pragma unroll
-                            for (int e = 0; e < VEC; ++e) yr[tk][k][e] = fmaf(a[tk], wf[e], yr[tk][k][e]);
+                            for (int e = 0; e < VEC; ++e) yr[tk][k][e] = fmaf(x1[tk], wf[e], yr[tk][k][e]);
                     }
                 }
             }
@@ -225,17 +236,27 @@ k2_sparse_up_down(const T *__restrict__ x, const T *__restrict__ Wu, const T *__
 }
 
 // K3: y[b][d] = sum_{p=0}^{P-1} y_p[b][d] in a fixed order: lane l of the warp owning a float4
-// column group adds p = l, l+32, ... sequentially, then a fixed xor butterfly. Bit-reproducible.
+// column group adds p = l, l+32, ... sequentially (all loads issued up front), then a fixed xor
+// butterfly. Bit-reproducible.
 __global__ void __launch_bounds__(kK3Threads)
 k3_splitk_reduce(const float4 *__restrict__ ypart, int p2, int n4, float4 *__restrict__ y) {
+    constexpr int kMaxPerLane = 8;
     pdl_wait_primary();
     const int lane = threadIdx.x & 31;
     const int f = (int)((blockIdx.x * (size_t)kK3Threads + threadIdx.x) >> 5);
     if (f >= n4) return;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int pp = lane; pp < p2; pp += 32) {
-        const float4 v = ypart[(size_t)pp * n4 + f];
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    for (int base = 0; base < p2; base += 32 * kMaxPerLane) {
+        float4 v[kMaxPerLane];
+#pragma unroll
+        for (int i = 0; i < kMaxPerLane; ++i) {
+            const int pp = base + lane + 32 * i;
+            v[i] = pp < p2 ? ypart[(size_t)pp * n4 + f] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < kMaxPerLane; ++i) {
+            acc.x += v[i].x; acc.y += v[i].y; acc.z += v[i].z; acc.w += v[i].w;
+        }
     }
     acc.x = warp_allreduce_sum(acc.x);
     acc.y = warp_allreduce_sum(acc.y);
@@ -244,12 +265,13 @@ k3_splitk_reduce(const float4 *__restrict__ ypart, int p2, int n4, float4 *__res
     if (lane == 0) y[f] = acc;
 }
 
-size_t k2_smem_bytes(int esize, int d, int ns, int stages, int b, int l_max, int g1, int threads) {
+size_t k2_smem_bytes(int esize, int d, int ns, int stages, int b, int l_max, int ntiles) {
     size_t s = (size_t)stages * ns * 2 * (size_t)d * esize;   // ring
     s += (size_t)stages * 8;                                   // mbarriers
-    s += (size_t)(g1 + 1) * 4;                                 // prefix
+    s += (size_t)(ntiles + 1) * 4;                             // prefix
     s += (size_t)l_max * 4 + (size_t)l_max * b * 4;            // slice ids + v
-    s += (size_t)(threads / 32) * ns * b * 4 + (size_t)ns * b * 4;
+    s = (s + 15) & ~(size_t)15;
+    s += (size_t)2 * (kK2Threads / 32) * ns * b * 4;           // cross-warp partials
     return (s + 127) & ~(size_t)127;
 }
 
@@ -268,41 +290,38 @@ static cudaError_t launch_ex(const void *func, dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelExC(&cfg, func, args);
 }
 
-template <typename T, int B, int CPT, int NS, int NT>
-static cudaError_t launch_k2_t(const PlanData &p, const void *x, const void *Wu, const void *Wd, void *ws,
+template <typename T, int B, int CPT, int NS>
+static cudaError_t launch_k2_t(const PlanData &p, int b, const void *x, const void *Wu, const void *Wd, void *ws,
                                cudaStream_t s, bool pdl) {
-    auto kern = k2_sparse_up_down<T, B, CPT, NS, NT>;
-    const size_t smem = k2_smem_bytes((int)sizeof(T), p.d, NS, p.stages, B, p.l_max, p.g1, NT);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
+    auto kern = k2_sparse_up_down<T, B, CPT, NS>;
+    const int tile_rows = k1_rows_per_tile(b);
+    int ntiles = k1_ntiles(p.m, b);
+    int stages = k2_stages(p, b);
+    const size_t smem = k2_smem_bytes((int)sizeof(T), p.d, NS, stages, B, p.l_max, ntiles);
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
+    if (e != cudaSuccess) return e;
     char *w = static_cast<char *>(ws);
     const T *xp = static_cast<const T *>(x);
     const T *wu = static_cast<const T *>(Wu);
     const T *wd = static_cast<const T *>(Wd);
-    int d = p.d, m = p.m, g1 = p.g1, p2 = p.p2, stages = p.stages, l_max = p.l_max;
+    int d = p.d, m = p.m, p2 = p.p2, l_max = p.l_max, tr = tile_rows;
     const int32_t *idx = reinterpret_cast<const int32_t *>(w + p.off_idx);
     const float *vals = reinterpret_cast<const float *>(w + p.off_vals);
     const int32_t *cnt = reinterpret_cast<const int32_t *>(w + p.off_cnt);
     float *ypart = reinterpret_cast<float *>(w + p.off_ypart);
-    void *args[] = {&xp, &wu, &wd, &d, &m, &g1, &p2, &stages, &l_max, &idx, &vals, &cnt, &ypart};
-    return launch_ex(reinterpret_cast<const void *>(kern), dim3(p.p2), dim3(NT), smem, s, pdl, args);
+    void *args[] = {&xp, &wu, &wd, &d, &m, &ntiles, &tr, &p2, &stages, &l_max, &idx, &vals, &cnt, &ypart};
+    return launch_ex(reinterpret_cast<const void *>(kern), dim3(p.p2), dim3(kK2Threads), smem, s, pdl, args);
 }
 
-// Dispatch: NS = 2 neurons per stage; NT = 256 threads for b <= 2 (x and y partials in
-// registers: 2*b*CPT*VEC floats per thread), 512 for larger batches.
 template <typename T, int B>
 static cudaError_t launch_k2_b(const PlanData &p, const void *x, const void *Wu, const void *Wd, void *ws,
                                cudaStream_t s, bool pdl) {
-    constexpr int NT = B <= 2 ? 256 : 512;
+    const bool ns4 = k2_neurons_per_stage(p, B) == 4;
     switch (p.cpt) {
-        case 1: return launch_k2_t<T, B, 1, 2, NT>(p, x, Wu, Wd, ws, s, pdl);
-        case 2: return launch_k2_t<T, B, 2, 2, NT>(p, x, Wu, Wd, ws, s, pdl);
-        case 3: return launch_k2_t<T, B, 3, 2, NT>(p, x, Wu, Wd, ws, s, pdl);
-        case 4: return launch_k2_t<T, B, 4, 2, NT>(p, x, Wu, Wd, ws, s, pdl);
+        case 1: return ns4 ? launch_k2_t<T, B, 1, 4>(p, B, x, Wu, Wd, ws, s, pdl)
+                           : launch_k2_t<T, B, 1, 2>(p, B, x, Wu, Wd, ws, s, pdl);
+        case 2: return ns4 ? launch_k2_t<T, B, 2, 4>(p, B, x, Wu, Wd, ws, s, pdl)
+                           : launch_k2_t<T, B, 2, 2>(p, B, x, Wu, Wd, ws, s, pdl);
         default: return cudaErrorInvalidValue;
     }
 }
