@@ -299,21 +299,21 @@ cudaError_t ensure_smem_attr(const void *func, size_t smem) {
 }
 
 int k1_stages(const PlanData &p, int b) {
-    const size_t stage = (size_t)k1_rows_per_tile(b) * p.d * p.esize;
-    const size_t extra = 2 * (size_t)(kK1Threads / 32) * k1_rows_per_tile(b) * b * 4 + 1024;
+    const size_t stage = (size_t)k1_rows_per_tile(p, b) * p.d * p.esize;
+    const size_t extra = 2 * (size_t)(kK1Threads / 32) * k1_rows_per_tile(p, b) * b * 4 + 1024;
     const size_t n = (kSmemBudget - extra) / (stage + 16);
     return (int)std::min<size_t>(n, 12);
 }
 
 int k2_neurons_per_stage(const PlanData &p, int b) {
-    const size_t extra = k2_smem_bytes(p.esize, p.d, 4, 0, b, p.l_max, k1_ntiles(p.m, b)) + 8 * kMaxStages + 256;
+    const size_t extra = k2_smem_bytes(p.esize, p.d, 4, 0, b, p.l_max, k1_ntiles(p, b)) + 8 * kMaxStages + 256;
     const size_t stage4 = (size_t)4 * 2 * p.d * p.esize;
     return extra + 2 * stage4 <= kSmemBudget ? 4 : 2;
 }
 
 int k2_stages(const PlanData &p, int b) {
     const int ns = k2_neurons_per_stage(p, b);
-    const size_t extra = k2_smem_bytes(p.esize, p.d, ns, 0, b, p.l_max, k1_ntiles(p.m, b)) + 8 * kMaxStages + 256;
+    const size_t extra = k2_smem_bytes(p.esize, p.d, ns, 0, b, p.l_max, k1_ntiles(p, b)) + 8 * kMaxStages + 256;
     const size_t stage = (size_t)ns * 2 * p.d * p.esize;
     if (extra >= kSmemBudget) return 0;
     return (int)std::min<size_t>((kSmemBudget - extra) / stage, kMaxStages);
@@ -347,7 +347,7 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.cpt = (p.nchunks + 511) / 512;  // K1 and K2 both run 512 threads
         if (p.cpt > kMaxCPT) return CATS_E_UNSUPPORTED;
         // K1: one persistent CTA per SM pulling NR-row tiles from a global counter
-        p.g1 = std::min(num_sms, k1_ntiles(m, 1));
+        p.g1 = std::min(num_sms, k1_ntiles(p, 1));
         // K2: one persistent CTA per SM; each owns 1/p2 of the active list
         p.p2 = num_sms;
         p.l_max = (m + p.p2 - 1) / p.p2;
@@ -361,7 +361,7 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.off_idx = off;     off = align_up(off + (size_t)m * 4, 256);
         p.off_tokmask = off; off = align_up(off + (size_t)m, 256);
         p.off_vals = off;    off = align_up(off + (size_t)m * max_batch * 4, 256);
-        p.off_cnt = off;     off = align_up(off + (size_t)k1_ntiles(m, CATS_MAX_BATCH) * 4, 256);
+        p.off_cnt = off;     off = align_up(off + (size_t)((m + 1) / 2) * 4, 256);
         p.off_ypart = off;   off = align_up(off + (size_t)p.p2 * max_batch * d * 4, 256);
         p.off_xstage = off;  off = align_up(off + (size_t)max_batch * d * esize, 256);
         p.off_ystage = off;  off = align_up(off + (size_t)max_batch * d * 4, 256);
@@ -387,7 +387,7 @@ extern "C" cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_ml
     info->num_sms = p.num_sms;
     info->k1_grid = p.g1;
     info->k1_threads = kK1Threads;
-    info->k1_rows_per_tile = k1_rows_per_tile(b);
+    info->k1_rows_per_tile = k1_rows_per_tile(p, b);
     info->k1_stages = k1_stages(p, b);
     info->k2_grid = p.p2;
     info->k2_threads = kK2Threads;
@@ -397,7 +397,7 @@ extern "C" cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_ml
     info->k3_threads = kK3Threads;
     info->k1_smem_max = k1_smem_bytes(p, b);
     info->k2_smem = k2_smem_bytes(p.esize, p.d, info->k2_neurons_per_stage, info->k2_stages, b, p.l_max,
-                                  k1_ntiles(p.m, b));
+                                  k1_ntiles(p, b));
     info->workspace_bytes = p.ws_bytes;
     return CATS_OK;
 }
@@ -526,7 +526,7 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
     CATS_TRY({
         cudaStream_t st = static_cast<cudaStream_t>(s);
         const char *w = static_cast<const char *>(ws);
-        const int tr = k1_rows_per_tile(b), ntiles = k1_ntiles(p.m, b);
+        const int tr = k1_rows_per_tile(p, b), ntiles = k1_ntiles(p, b);
         std::vector<int32_t> idx(p.m), cnt(ntiles);
         std::vector<uint8_t> tm(p.m);
         cudaError_t e = cudaSetDevice(p.device);

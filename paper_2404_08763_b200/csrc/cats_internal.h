@@ -32,10 +32,15 @@ struct PlanData {
 };
 
 // K1 tile height (rows of W_gate per ring stage) for batch b: keeps the per-thread partial dot
-// products (rows x tokens) in registers.
+// products (rows x tokens) in registers; halved for very wide rows so >= 3 stages fit in smem.
 __host__ __device__ constexpr int k1_rows_per_tile_c(int b) { return b <= 2 ? 8 : (b <= 4 ? 4 : 2); }
-inline int k1_rows_per_tile(int b) { return k1_rows_per_tile_c(b); }
-inline int k1_ntiles(int m, int b) { return (m + k1_rows_per_tile(b) - 1) / k1_rows_per_tile(b); }
+inline int k1_rows_per_tile(const PlanData &p, int b) {
+    int nr = k1_rows_per_tile_c(b);
+    const size_t row = (size_t)p.d * p.esize;
+    while (nr > 2 && 3 * (size_t)nr * row > kSmemBudget - 16 * 1024) nr /= 2;
+    return nr;
+}
+inline int k1_ntiles(const PlanData &p, int b) { return (p.m + k1_rows_per_tile(p, b) - 1) / k1_rows_per_tile(p, b); }
 
 size_t k1_smem_bytes(const PlanData &p, int b);
 int k1_stages(const PlanData &p, int b);

@@ -68,11 +68,8 @@ k1_gate_silu_cats_compact(const T *__restrict__ x, const T *__restrict__ Wg, int
     // ---- producer state (thread 0): prefetched next tile id ----
     uint64_t policy = 0;
     unsigned int next_tile = 0;
-    auto fill = [&](int g) {  // thread 0: stage g % stages <- tile next_tile (or end marker)
-        const int s = g % stages;
-        const unsigned int tile = next_tile;
+    auto fill = [&](int s, unsigned int tile) {  // thread 0: stage s <- tile (or end marker)
         if (tile < (unsigned)ntiles) {
-            next_tile = atomicAdd(&sched[0], 1u);  // consumed at the next fill: latency overlapped
             const int r0 = (int)tile * NR;
             const int nr = min(NR, m - r0);
             stile[s] = (int)tile;
@@ -87,42 +84,45 @@ k1_gate_silu_cats_compact(const T *__restrict__ x, const T *__restrict__ Wg, int
         for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
         fence_mbar_init();
         policy = l2_evict_first_policy();
-        next_tile = atomicAdd(&sched[0], 1u);
-        for (int g = 0; g < stages; ++g) {
-            fill(g);
-            if (stile[g] < 0) break;
-        }
+        const unsigned int base = atomicAdd(&sched[0], (unsigned)stages);  // first `stages` tiles at once
+        next_tile = atomicAdd(&sched[0], 1u);                              // prefetch: used at the next fill
+        for (int s = 0; s < stages; ++s) fill(s, base + s);
     }
     __syncthreads();
 
+    int s = 0;
+    uint32_t phase = 0;
     for (int g = 0;; ++g) {
-        const int s = g % stages;
-        mbar_wait(&full[s], (uint32_t)((g / stages) & 1));
+        mbar_wait(&full[s], phase);
         const int tile = stile[s];
         if (tile < 0) break;
         const int r0 = tile * NR;
         const int nr = min(NR, m - r0);
         const uint32_t sbase = smem_u32(ring + (size_t)s * stage_bytes);
 
-        // ---- u = x W_gate[:, j]: partial dots over own chunks, warp butterfly ----
+        // ---- u = x W_gate[:, j]: own chunks of the tile's rows -> registers, partial dots ----
+        uint4 wr[NR][CPT];
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) {
+                const int ch = tid + k * NT;
+                wr[r][k] = (r < nr && ch < nch) ? lds128(sbase + (uint32_t)r * row_bytes + (uint32_t)ch * 16u)
+                                                : make_uint4(0u, 0u, 0u, 0u);
+            }
         float part[NR][B];
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
 #pragma unroll
             for (int tk = 0; tk < B; ++tk) part[r][tk] = 0.f;
-            if (r < nr) {
 #pragma unroll
-                for (int k = 0; k < CPT; ++k) {
-                    const int ch = tid + k * NT;
-                    if (ch < nch) {
-                        float wf[VEC];
-                        unpack16(lds128(sbase + (uint32_t)r * row_bytes + (uint32_t)ch * 16u), wf);
+            for (int k = 0; k < CPT; ++k) {
+                float wf[VEC];
+                unpack16(wr[r][k], wf);
 #pragma unroll
-                        for (int tk = 0; tk < B; ++tk)
+                for (int tk = 0; tk < B; ++tk)
 #pragma unroll
-                            for (int e = 0; e < VEC; ++e) part[r][tk] = fmaf(xr[tk][k][e], wf[e], part[r][tk]);
-                    }
-                }
+                    for (int e = 0; e < VEC; ++e) part[r][tk] = fmaf(xr[tk][k][e], wf[e], part[r][tk]);
             }
         }
         float *rb = red + (size_t)(g & 1) * NW * NP;
@@ -133,8 +133,12 @@ k1_gate_silu_cats_compact(const T *__restrict__ x, const T *__restrict__ Wg, int
                 const float v = warp_allreduce_sum(part[r][tk]);
                 if (lane == 0) rb[warp * NP + r * B + tk] = v;
             }
-        __syncthreads();  // red[g&1] complete; every thread is done with stage (g-1) % stages
-        if (tid == 0 && g >= 1 && stile[(g - 1) % stages] >= 0) fill(g - 1 + stages);
+        __syncthreads();  // red[g&1] complete; every thread has read stage s -> refill it now
+        if (tid == 0) {
+            const unsigned int nt = next_tile;
+            if (nt < (unsigned)ntiles) next_tile = atomicAdd(&sched[0], 1u);
+            fill(s, nt);
+        }
 
         // ---- warp 0: u -> v = SiLU(u) (Eq. 2) -> keep = |v| >= t (Eq. 4) -> compaction ----
         if (warp == 0) {
@@ -165,6 +169,7 @@ k1_gate_silu_cats_compact(const T *__restrict__ x, const T *__restrict__ Wg, int
             }
             if (lane == 0) cnt[tile] = __popc(bal);
         }
+        if (++s == stages) { s = 0; phase ^= 1u; }
     }
 
     // ---- last CTA out resets the tile scheduler for the next launch ----
@@ -180,7 +185,7 @@ k1_gate_silu_cats_compact(const T *__restrict__ x, const T *__restrict__ Wg, int
 }
 
 size_t k1_smem_bytes(const PlanData &p, int b) {
-    const int nr = k1_rows_per_tile(b);
+    const int nr = k1_rows_per_tile(p, b);
     const int stages = k1_stages(p, b);
     size_t s = (size_t)stages * nr * (size_t)p.d * p.esize;
     s += (size_t)stages * 8 + (size_t)stages * 4;
@@ -189,10 +194,9 @@ size_t k1_smem_bytes(const PlanData &p, int b) {
     return (s + 127) & ~(size_t)127;
 }
 
-template <typename T, int B, int CPT>
+template <typename T, int B, int NR, int CPT>
 static cudaError_t launch_k1_t(const PlanData &p, const void *x, const void *Wg, float t, int dense, float *acts,
                                void *ws, cudaStream_t s) {
-    constexpr int NR = k1_rows_per_tile_c(B);
     auto kern = k1_gate_silu_cats_compact<T, B, NR, CPT>;
     const size_t smem = k1_smem_bytes(p, B);
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
@@ -207,13 +211,24 @@ static cudaError_t launch_k1_t(const PlanData &p, const void *x, const void *Wg,
     return cudaGetLastError();
 }
 
+template <typename T, int B, int NR>
+static cudaError_t launch_k1_r(const PlanData &p, const void *x, const void *Wg, float t, int dense, float *acts,
+                               void *ws, cudaStream_t s) {
+    switch (p.cpt) {
+        case 1: return launch_k1_t<T, B, NR, 1>(p, x, Wg, t, dense, acts, ws, s);
+        case 2: return launch_k1_t<T, B, NR, 2>(p, x, Wg, t, dense, acts, ws, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 template <typename T, int B>
 static cudaError_t launch_k1_c(const PlanData &p, const void *x, const void *Wg, float t, int dense, float *acts,
                                void *ws, cudaStream_t s) {
-    const int cpt = (p.nchunks + kK1Threads - 1) / kK1Threads;
-    switch (cpt) {
-        case 1: return launch_k1_t<T, B, 1>(p, x, Wg, t, dense, acts, ws, s);
-        case 2: return launch_k1_t<T, B, 2>(p, x, Wg, t, dense, acts, ws, s);
+    constexpr int NR0 = k1_rows_per_tile_c(B);
+    switch (k1_rows_per_tile(p, B)) {
+        case NR0: return launch_k1_r<T, B, NR0>(p, x, Wg, t, dense, acts, ws, s);
+        case (NR0 > 2 ? NR0 / 2 : 1): return launch_k1_r<T, B, (NR0 > 2 ? NR0 / 2 : 2)>(p, x, Wg, t, dense, acts, ws, s);
+        case (NR0 > 4 ? NR0 / 4 : 0): return launch_k1_r<T, B, (NR0 > 4 ? NR0 / 4 : 2)>(p, x, Wg, t, dense, acts, ws, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -121,7 +121,7 @@ k2_sparse_up_down(const T *__restrict__ x, const T *__restrict__ Wu, const T *__
     const int ngroups = (L + NS - 1) / NS;
     uint64_t policy = 0;
     auto issue = [&](int g) {  // thread 0 only
-        const int s = g % stages;
+        const int s = g % stages;  // (once per stage refill)
         const int n_in = min(NS, L - g * NS);
         mbar_arrive_expect_tx(&full[s], (uint32_t)n_in * 2u * row_bytes);
         unsigned char *dst = ring + (size_t)s * stage_bytes;
@@ -145,31 +145,39 @@ k2_sparse_up_down(const T *__restrict__ x, const T *__restrict__ Wu, const T *__
 #pragma unroll
             for (int e = 0; e < VEC; ++e) yr[tk][k][e] = 0.f;
 
+    int s = 0;
+    uint32_t phase = 0;
     for (int g = 0; g < ngroups; ++g) {
-        const int s = g % stages;
         const int n_in = min(NS, L - g * NS);
-        mbar_wait(&full[s], (uint32_t)((g / stages) & 1));
+        mbar_wait(&full[s], phase);
         const uint32_t sbase = smem_u32(ring + (size_t)s * stage_bytes);
 
-        // ---- up: partial dots of x with this thread's chunks of each staged W_up row ----
+        // ---- own chunks of the staged W_up and W_down rows -> registers (frees the stage early) ----
+        uint4 wu[NS][CPT], wd[NS][CPT];
+#pragma unroll
+        for (int i = 0; i < NS; ++i)
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) {
+                const int ch = tid + k * NT;
+                const bool ok = i < n_in && ch < nch;
+                wu[i][k] = ok ? lds128(sbase + (uint32_t)(2 * i) * row_bytes + (uint32_t)ch * 16u) : make_uint4(0u, 0u, 0u, 0u);
+                wd[i][k] = ok ? lds128(sbase + (uint32_t)(2 * i + 1) * row_bytes + (uint32_t)ch * 16u) : make_uint4(0u, 0u, 0u, 0u);
+            }
+
+        // ---- up: partial dots of x with this thread's chunks of each W_up row ----
         float part[NS][B];
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
 #pragma unroll
             for (int tk = 0; tk < B; ++tk) part[i][tk] = 0.f;
-            if (i < n_in) {
 #pragma unroll
-                for (int k = 0; k < CPT; ++k) {
-                    const int ch = tid + k * NT;
-                    if (ch < nch) {
-                        float wf[VEC];
-                        unpack16(lds128(sbase + (uint32_t)(2 * i) * row_bytes + (uint32_t)ch * 16u), wf);
+            for (int k = 0; k < CPT; ++k) {
+                float wf[VEC];
+                unpack16(wu[i][k], wf);
 #pragma unroll
-                        for (int tk = 0; tk < B; ++tk)
+                for (int tk = 0; tk < B; ++tk)
 #pragma unroll
-                            for (int e = 0; e < VEC; ++e) part[i][tk] = fmaf(xr[tk][k][e], wf[e], part[i][tk]);
-                    }
-                }
+                    for (int e = 0; e < VEC; ++e) part[i][tk] = fmaf(xr[tk][k][e], wf[e], part[i][tk]);
             }
         }
         float *rb = red + (size_t)(g & 1) * NW * NP;
@@ -180,8 +188,8 @@ k2_sparse_up_down(const T *__restrict__ x, const T *__restrict__ Wu, const T *__
                 const float r = warp_allreduce_sum(part[i][tk]);
                 if (lane == 0) rb[warp * NP + i * B + tk] = r;
             }
-        __syncthreads();  // red[g&1] complete; every thread is past the down phase of group g-1
-        if (tid == 0 && g >= 1 && g - 1 + stages < ngroups) issue(g - 1 + stages);
+        __syncthreads();  // red[g&1] complete; every thread has read stage s -> refill it now
+        if (tid == 0 && g + stages < ngroups) issue(g + stages);
 
         // ---- cross-warp sums, computed redundantly by every warp in one fixed tree:
         //      lane l reads warp (l & 15)'s partial of pair 2c + (l >> 4); xor 8,4,2,1 sums the 16.
@@ -205,18 +213,16 @@ k2_sparse_up_down(const T *__restrict__ x, const T *__restrict__ Wu, const T *__
                 for (int tk = 0; tk < B; ++tk) x1[tk] = a[i * B + tk] * svals[(size_t)(g * NS + i) * B + tk];
 #pragma unroll
                 for (int k = 0; k < CPT; ++k) {
-                    const int ch = tid + k * NT;
-                    if (ch < nch) {
-                        float wf[VEC];
-                        unpack16(lds128(sbase + (uint32_t)(2 * i + 1) * row_bytes + (uint32_t)ch * 16u), wf);
+                    float wf[VEC];
+                    unpack16(wd[i][k], wf);
 #pragma unroll
-                        for (int tk = 0; tk < B; ++tk)
+                    for (int tk = 0; tk < B; ++tk)
 #pragma unroll
-                            for (int e = 0; e < VEC; ++e) yr[tk][k][e] = fmaf(x1[tk], wf[e], yr[tk][k][e]);
-                    }
+                        for (int e = 0; e < VEC; ++e) yr[tk][k][e] = fmaf(x1[tk], wf[e], yr[tk][k][e]);
                 }
             }
         }
+        if (++s == stages) { s = 0; phase ^= 1u; }
     }
 
     // ---- phase 1 output: this CTA's fp32 partial y_p[b][d] ----
@@ -294,8 +300,8 @@ template <typename T, int B, int CPT, int NS>
 static cudaError_t launch_k2_t(const PlanData &p, int b, const void *x, const void *Wu, const void *Wd, void *ws,
                                cudaStream_t s, bool pdl) {
     auto kern = k2_sparse_up_down<T, B, CPT, NS>;
-    const int tile_rows = k1_rows_per_tile(b);
-    int ntiles = k1_ntiles(p.m, b);
+    const int tile_rows = k1_rows_per_tile(p, b);
+    int ntiles = k1_ntiles(p, b);
     int stages = k2_stages(p, b);
     const size_t smem = k2_smem_bytes((int)sizeof(T), p.d, NS, stages, B, p.l_max, ntiles);
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
