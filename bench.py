@@ -272,16 +272,15 @@ def main():
 
     # ---- per-kernel times (profiled variant: events between kernels) -> roofline
     n_prof = min(args.steps, 500)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_prof)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n_prof)]
     for i in range(10):
         cats.cats_mlp_decode_profiled(plan, xs[i % 64], *copies[i % len(copies)], t, evs[0], y=y, ws=ws)
     torch.cuda.synchronize(dev)
     for i in range(n_prof):
         cats.cats_mlp_decode_profiled(plan, xs[i % 64], *copies[i % len(copies)], t, evs[i], y=y, ws=ws)
     torch.cuda.synchronize(dev)
-    k1 = statistics.mean(e[0].elapsed_time(e[1]) for e in evs) * 1e3
-    k2 = statistics.mean(e[1].elapsed_time(e[2]) for e in evs) * 1e3
-    k3 = statistics.mean(e[2].elapsed_time(e[3]) for e in evs) * 1e3
+    k12 = statistics.mean(e[0].elapsed_time(e[1]) for e in evs) * 1e3
+    k3 = statistics.mean(e[1].elapsed_time(e[2]) for e in evs) * 1e3
 
     # ---- dense path of the same library (speedup denominator), and cuBLAS dense for context
     def dense_step(i):
@@ -318,12 +317,10 @@ def main():
     # ---- roofline of the dominant kernel (algorithmic bytes / live CUDA-event duration)
     hbm_peak, peak_kind = peaks()
     esz = 2
-    k1_bytes = 2 * d * ms + b * d * esz                  # all W_gate rows + x
-    k2_bytes = 4 * d * nnz_local + b * d * esz           # active W_up + W_down rows + x
-    step_bytes = k1_bytes + k2_bytes
-    kern = {"K1": (k1, k1_bytes), "K2": (k2, k2_bytes)}
-    dom = max(kern, key=lambda n: kern[n][0])
-    dom_us, dom_bytes = kern[dom]
+    # K12 algorithmic bytes: every W_gate row (2d B per neuron) + the active neurons' W_up and
+    # W_down rows (4d B per active neuron) + x
+    step_bytes = 2 * d * ms + 4 * d * nnz_local + b * d * esz
+    dom, dom_us, dom_bytes = "K12", k12, step_bytes
     achieved = dom_bytes / (dom_us * 1e-6) / 1e9
     traffic = None
     tp_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -354,17 +351,15 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_ms * 1e3 / b, 3), "unit": UNIT, "h2d_bytes_per_step": b * d * esz,
                     "d2h_bytes_per_step": b * d * 4},
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": 2 * args.steps,
             "clocks": clocks,
             "detail": {
                 "t": t, "nnz_union_per_rank": nnz_local, "nnz_union_total": U, "m_per_rank": ms,
                 "realized_sparsity": round(1 - U / m, 4),
-                "k1_us": round(k1, 3), "k2_us": round(k2, 3), "k3_us": round(k3, 3),
+                "k12_us": round(k12, 3), "k3_us": round(k3, 3),
                 "effective_bytes_per_step": step_bytes,
                 "effective_GBps": round(step_bytes / (us_step * 1e-6) / 1e9, 1),
                 "frac_of_8TBps": round(step_bytes / (us_step * 1e-6) / 1e9 / NOMINAL_HBM_GBS, 4),
-                "k1_GBps": round(k1_bytes / (k1 * 1e-6) / 1e9, 1),
-                "k2_GBps": round(k2_bytes / (k2 * 1e-6) / 1e9, 1),
                 "dense_us": round(dense_ms * 1e3, 3),
                 "speedup_vs_dense": round(dense_ms / ms_step, 4),
                 "dense_GBps": round(6 * d * ms / (dense_ms * 1e-3) / 1e9, 1),

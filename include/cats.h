@@ -162,14 +162,11 @@ typedef struct {
     int d, m, max_batch;
     cats_dtype_t w_dtype;
     int device, num_sms;
-    int k1_grid, k1_threads;      /* K1: gate GEMV + SiLU + threshold + compaction */
-    int k1_rows_per_tile;         /* W_gate rows per dynamically scheduled tile (= ring stage) */
-    int k1_stages;                /* K1 ring depth */
-    int k2_grid, k2_threads;      /* K2: sparse up x v + down, per-CTA split-K partials */
-    int k2_neurons_per_stage;     /* neurons per smem ring stage (W_up row + W_down row each) */
-    int k2_stages;                /* ring depth */
-    int k3_grid, k3_threads;      /* K3: fixed-order split-K reduction of the partials */
-    size_t k1_smem_max, k2_smem;  /* dynamic shared memory bytes */
+    int grid, threads;            /* K12 fused dataflow kernel: persistent CTAs (one per SM) */
+    int rows_per_tile;            /* W_gate rows per GATE job; a UD job carries rows_per_tile/2 neurons */
+    int stages;                   /* shared-memory ring depth (one job per stage) */
+    size_t smem;                  /* K12 dynamic shared memory bytes (at max_batch) */
+    int k3_grid, k3_threads;      /* K3: exact fixed-point split-K reduction of the CTA partials */
     size_t workspace_bytes;
 } cats_mlp_plan_info_t;
 
@@ -191,8 +188,9 @@ cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, void *ws, siz
 
 /* y[b][d] = CATS_t gated MLP of x[b][d] over this plan's m neurons (under tensor parallelism y
  * is the rank's partial; the caller all-reduces). t >= 0; t = 0 gives dense semantics.
- * Launches K1 -> K2 -> K3 on s (programmatic dependent launch between them). Deterministic:
- * bit-identical y for identical inputs.
+ * Launches K12 (gate GEMV + SiLU + threshold + compaction + sparse up x v + down, one persistent
+ * dataflow kernel) then K3 (reduction) on s, with programmatic dependent launch. Deterministic:
+ * bit-identical y for identical inputs, whatever the dynamic tile schedule.
  * Errors: CATS_E_NULL, CATS_E_ALIGN, CATS_E_BATCH, CATS_E_THRESHOLD, CATS_E_WORKSPACE,
  *         CATS_E_CUDA. */
 cats_status_t cats_mlp_decode(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
@@ -211,11 +209,10 @@ cats_status_t cats_mlp_decode_host(const cats_mlp_plan_t *plan, const void *x_ho
                                    const void *W_gate, const void *W_up, const void *W_down_nm,
                                    float t, float *y_host, void *ws, size_t ws_bytes, cats_stream_t s);
 
-/* Measurement variant of cats_mlp_decode: identical launches, plus events[0..3] (cudaEvent_t,
- * created by the caller with timing enabled) recorded on s before K1, between K1 and K2, between K2
- * and K3, and after K3 -- per-kernel device time for the roofline report. The recorded events break
- * the programmatic-dependent-launch overlap between the kernels, so the sum of the three intervals
- * is an upper bound of a cats_mlp_decode call. */
+/* Measurement variant of cats_mlp_decode: identical launches, plus events[0..2] (cudaEvent_t,
+ * created by the caller with timing enabled) recorded on s before K12, between K12 and K3, and after
+ * K3 -- per-kernel device time for the roofline report. The recorded events break the
+ * programmatic-dependent-launch overlap, so the sum of the intervals bounds a cats_mlp_decode call. */
 cats_status_t cats_mlp_decode_profiled(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
                                        const void *W_up, const void *W_down_nm, float t, float *y,
                                        void *ws, size_t ws_bytes, cats_stream_t s, void *const *events);
@@ -232,6 +229,13 @@ cats_status_t cats_mlp_gate_act(const cats_mlp_plan_t *plan, const void *x, int 
 cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const void *ws, int b, int32_t *idx_host,
                                    uint8_t *tokmask_host, uint32_t *nnz_union, uint32_t *nnz_per_token,
                                    cats_stream_t s);
+
+/* Diagnostics. When the environment variable CATS_TRACE=1 is set at plan creation, the kernels
+ * record %globaltimer stamps (ns) per CTA into a trace area of the workspace:
+ * uint64 trace[3][512 CTAs][8 slots] at byte `offset` (bytes = 0 when tracing is off).
+ * [0] K12 slots: 0 start, 1 ring primed, 2 jobs done, 3 exit. [1] K3: 0 start, 1 K12 visible,
+ * 2 exit. */
+cats_status_t cats_mlp_trace_info(const cats_mlp_plan_t *plan, size_t *offset, size_t *bytes);
 
 #ifdef __cplusplus
 }

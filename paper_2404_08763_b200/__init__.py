@@ -190,12 +190,12 @@ def cats_mlp_decode(plan: MlpPlan, x, W_gate, W_up, W_down_nm, t: float, y=None,
 
 def cats_mlp_decode_profiled(plan: MlpPlan, x, W_gate, W_up, W_down_nm, t: float, events, y=None, ws=None,
                              stream=None):
-    """cats_mlp_decode with 4 torch.cuda.Event(enable_timing=True) recorded around K1, K2, K3."""
+    """cats_mlp_decode with 3 torch.cuda.Event(enable_timing=True) recorded around K12 and K3."""
     x, b, y, ws = _prep(plan, x, y, ws)
     for e in events:
         if e.cuda_event == 0:
             e.record()  # materialise the lazily created event on this device
-    arr = (ctypes.c_void_p * 4)(*[e.cuda_event for e in events])
+    arr = (ctypes.c_void_p * 3)(*[e.cuda_event for e in events])
     rc = plan._lib.cats_mlp_decode_profiled(plan.handle, _dev_ptr(x, "x"), b, _dev_ptr(W_gate, "W_gate"),
                                             _dev_ptr(W_up, "W_up"), _dev_ptr(W_down_nm, "W_down_nm"), float(t),
                                             _dev_ptr(y, "y"), _dev_ptr(ws, "ws"), ws.numel(),

@@ -28,11 +28,9 @@ class CalibWindow(ctypes.Structure):
 
 class PlanInfo(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int), ("m", ctypes.c_int), ("max_batch", ctypes.c_int), ("w_dtype", ctypes.c_int),
-                ("device", ctypes.c_int), ("num_sms", ctypes.c_int), ("k1_grid", ctypes.c_int),
-                ("k1_threads", ctypes.c_int), ("k1_rows_per_tile", ctypes.c_int), ("k1_stages", ctypes.c_int),
-                ("k2_grid", ctypes.c_int), ("k2_threads", ctypes.c_int),
-                ("k2_neurons_per_stage", ctypes.c_int), ("k2_stages", ctypes.c_int), ("k3_grid", ctypes.c_int),
-                ("k3_threads", ctypes.c_int), ("k1_smem_max", ctypes.c_size_t), ("k2_smem", ctypes.c_size_t),
+                ("device", ctypes.c_int), ("num_sms", ctypes.c_int), ("grid", ctypes.c_int),
+                ("threads", ctypes.c_int), ("rows_per_tile", ctypes.c_int), ("stages", ctypes.c_int),
+                ("smem", ctypes.c_size_t), ("k3_grid", ctypes.c_int), ("k3_threads", ctypes.c_int),
                 ("workspace_bytes", ctypes.c_size_t)]
 
 
@@ -62,6 +60,7 @@ _SIGS = {
     "cats_mlp_decode_host": (I, [P, P, I, P, P, P, F, P, P, SZ, P]),
     "cats_mlp_gate_act": (I, [P, P, I, P, P, P, SZ, P]),
     "cats_mlp_last_active": (I, [P, P, I, P, P, P, P, P]),
+    "cats_mlp_trace_info": (I, [P, P, P]),
 }
 
 

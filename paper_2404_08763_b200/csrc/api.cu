@@ -5,12 +5,14 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
 #include <string>
 #include <vector>
 
+#include "cats_device.cuh"
 #include "cats_internal.h"
 
 using namespace cats;
@@ -298,27 +300,6 @@ cudaError_t ensure_smem_attr(const void *func, size_t smem) {
     return cudaSuccess;
 }
 
-int k1_stages(const PlanData &p, int b) {
-    const size_t stage = (size_t)k1_rows_per_tile(p, b) * p.d * p.esize;
-    const size_t extra = 2 * (size_t)(kK1Threads / 32) * k1_rows_per_tile(p, b) * b * 4 + 1024;
-    const size_t n = (kSmemBudget - extra) / (stage + 16);
-    return (int)std::min<size_t>(n, 12);
-}
-
-int k2_neurons_per_stage(const PlanData &p, int b) {
-    const size_t extra = k2_smem_bytes(p.esize, p.d, 4, 0, b, p.l_max, k1_ntiles(p, b)) + 8 * kMaxStages + 256;
-    const size_t stage4 = (size_t)4 * 2 * p.d * p.esize;
-    return extra + 2 * stage4 <= kSmemBudget ? 4 : 2;
-}
-
-int k2_stages(const PlanData &p, int b) {
-    const int ns = k2_neurons_per_stage(p, b);
-    const size_t extra = k2_smem_bytes(p.esize, p.d, ns, 0, b, p.l_max, k1_ntiles(p, b)) + 8 * kMaxStages + 256;
-    const size_t stage = (size_t)ns * 2 * p.d * p.esize;
-    if (extra >= kSmemBudget) return 0;
-    return (int)std::min<size_t>((kSmemBudget - extra) / stage, kMaxStages);
-}
-
 }  // namespace cats
 
 extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_dtype_t dt, int device, int num_sms,
@@ -344,17 +325,13 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.esize = esize;
         p.vec = 16 / esize;
         p.nchunks = d * esize / 16;
-        p.cpt = (p.nchunks + 511) / 512;  // K1 and K2 both run 512 threads
+        p.cpt = (p.nchunks + kConsumers - 1) / kConsumers;  // chunks per column-owning consumer thread
         if (p.cpt > kMaxCPT) return CATS_E_UNSUPPORTED;
-        // K1: one persistent CTA per SM pulling NR-row tiles from a global counter
-        p.g1 = std::min(num_sms, k1_ntiles(p, 1));
-        // K2: one persistent CTA per SM; each owns 1/p2 of the active list
-        p.p2 = num_sms;
-        p.l_max = (m + p.p2 - 1) / p.p2;
-        for (int b = 1; b <= max_batch; ++b) {
-            if (k1_stages(p, b) < 2 || k1_smem_bytes(p, b) > kSmemBudget) return CATS_E_UNSUPPORTED;
-            if (k2_stages(p, b) < 2) return CATS_E_UNSUPPORTED;
-        }
+        // K12: one persistent CTA per SM pulling NR-row tiles from a global counter
+        p.g1 = std::min(num_sms * kCtasPerSm, k12_ntiles(p, 1));
+        for (int b = 1; b <= max_batch; ++b)
+            if (k12_stages(p, b) < 3 || k12_smem_bytes(p, b, k12_stages(p, b)) > kSmemBudget)
+                return CATS_E_UNSUPPORTED;
         // workspace
         size_t off = 0;
         p.off_sched = off;   off = align_up(off + 64, 256);
@@ -362,9 +339,14 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.off_tokmask = off; off = align_up(off + (size_t)m, 256);
         p.off_vals = off;    off = align_up(off + (size_t)m * max_batch * 4, 256);
         p.off_cnt = off;     off = align_up(off + (size_t)((m + 1) / 2) * 4, 256);
-        p.off_ypart = off;   off = align_up(off + (size_t)p.p2 * max_batch * d * 4, 256);
+        p.off_ypart = off;   off = align_up(off + (size_t)p.g1 * max_batch * d * 8, 256);  // int64 partials
         p.off_xstage = off;  off = align_up(off + (size_t)max_batch * d * esize, 256);
         p.off_ystage = off;  off = align_up(off + (size_t)max_batch * d * 4, 256);
+        const char *tr = std::getenv("CATS_TRACE");
+        p.trace = tr && tr[0] == '1';
+        p.off_trace = off;
+        p.trace_bytes = p.trace ? (size_t)kTraceKernels * kTraceCtas * kTraceSlots * 8 : 0;
+        off = align_up(off + p.trace_bytes, 256);
         p.ws_bytes = off;
         cats_mlp_plan *plan = new cats_mlp_plan;
         plan->p = p;
@@ -385,19 +367,13 @@ extern "C" cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_ml
     info->w_dtype = p.dt;
     info->device = p.device;
     info->num_sms = p.num_sms;
-    info->k1_grid = p.g1;
-    info->k1_threads = kK1Threads;
-    info->k1_rows_per_tile = k1_rows_per_tile(p, b);
-    info->k1_stages = k1_stages(p, b);
-    info->k2_grid = p.p2;
-    info->k2_threads = kK2Threads;
-    info->k2_neurons_per_stage = k2_neurons_per_stage(p, b);
-    info->k2_stages = k2_stages(p, b);
-    info->k3_grid = (p.max_batch * p.d / 4 + kK3Threads / 32 - 1) / (kK3Threads / 32);
+    info->grid = p.g1;
+    info->threads = kK12Threads;
+    info->rows_per_tile = k12_rows_per_tile(p, b);
+    info->stages = k12_stages(p, b);
+    info->smem = k12_smem_bytes(p, b, info->stages);
+    info->k3_grid = (p.max_batch * p.d / 2 + 7) / 8;
     info->k3_threads = kK3Threads;
-    info->k1_smem_max = k1_smem_bytes(p, b);
-    info->k2_smem = k2_smem_bytes(p.esize, p.d, info->k2_neurons_per_stage, info->k2_stages, b, p.l_max,
-                                  k1_ntiles(p, b));
     info->workspace_bytes = p.ws_bytes;
     return CATS_OK;
 }
@@ -435,8 +411,7 @@ cats_status_t validate_common(const cats_mlp_plan_t *plan, const void *x, int b,
 cats_status_t run_mlp(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd, float t,
                       int dense, float *y, void *ws, cudaStream_t st) {
     cudaError_t e = cudaSetDevice(p.device);
-    if (e == cudaSuccess) e = launch_k1(p, x, b, Wg, t, dense, nullptr, ws, st);
-    if (e == cudaSuccess) e = launch_k2(p, x, b, Wu, Wd, ws, st, /*pdl=*/true);
+    if (e == cudaSuccess) e = launch_k12(p, x, b, Wg, Wu, Wd, t, dense ? kModeDense : kModeCats, nullptr, ws, st);
     if (e == cudaSuccess) e = launch_k3(p, b, ws, y, st, /*pdl=*/true);
     return cuda_status(e);
 }
@@ -458,20 +433,18 @@ extern "C" cats_status_t cats_mlp_decode_profiled(const cats_mlp_plan_t *plan, c
                                                   void *const *events) {
     cats_status_t rc = validate_common(plan, x, b, W_gate, W_up, W_down_nm, y, ws, ws_bytes);
     if (rc != CATS_OK) return rc;
-    if (!events || !events[0] || !events[1] || !events[2] || !events[3]) return CATS_E_NULL;
+    if (!events || !events[0] || !events[1] || !events[2]) return CATS_E_NULL;
     if (!(t >= 0.0f) || std::isinf(t)) return CATS_E_THRESHOLD;
     const PlanData &p = plan->p;
     cudaStream_t st = static_cast<cudaStream_t>(s);
-    cudaEvent_t ev[4];
-    for (int i = 0; i < 4; ++i) ev[i] = static_cast<cudaEvent_t>(events[i]);
+    cudaEvent_t ev[3];
+    for (int i = 0; i < 3; ++i) ev[i] = static_cast<cudaEvent_t>(events[i]);
     cudaError_t e = cudaSetDevice(p.device);
     if (e == cudaSuccess) e = cudaEventRecord(ev[0], st);
-    if (e == cudaSuccess) e = launch_k1(p, x, b, W_gate, t, 0, nullptr, ws, st);
+    if (e == cudaSuccess) e = launch_k12(p, x, b, W_gate, W_up, W_down_nm, t, kModeCats, nullptr, ws, st);
     if (e == cudaSuccess) e = cudaEventRecord(ev[1], st);
-    if (e == cudaSuccess) e = launch_k2(p, x, b, W_up, W_down_nm, ws, st, /*pdl=*/true);
-    if (e == cudaSuccess) e = cudaEventRecord(ev[2], st);
     if (e == cudaSuccess) e = launch_k3(p, b, ws, y, st, /*pdl=*/true);
-    if (e == cudaSuccess) e = cudaEventRecord(ev[3], st);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[2], st);
     return cuda_status(e);
 }
 
@@ -513,7 +486,10 @@ extern "C" cats_status_t cats_mlp_gate_act(const cats_mlp_plan_t *plan, const vo
     if (!ws || ws_bytes < plan->p.ws_bytes) return CATS_E_WORKSPACE;
     if (!aligned16(x) || !aligned16(W_gate) || !aligned16(ws)) return CATS_E_ALIGN;
     cudaError_t e = cudaSetDevice(plan->p.device);
-    if (e == cudaSuccess) e = launch_k1(plan->p, x, b, W_gate, 0.0f, 1, acts, ws, static_cast<cudaStream_t>(s));
+    if (e == cudaSuccess)
+        e = launch_k12(plan->p, x, b, W_gate, W_gate, W_gate, 0.0f, kModeGateOnly, acts, ws, static_cast<cudaStream_t>(s));
+    if (e == cudaSuccess)  // re-arm K1's tile scheduler (no K2 follows)
+        e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_sched, 0, 8, static_cast<cudaStream_t>(s));
     return cuda_status(e);
 }
 
@@ -526,7 +502,7 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
     CATS_TRY({
         cudaStream_t st = static_cast<cudaStream_t>(s);
         const char *w = static_cast<const char *>(ws);
-        const int tr = k1_rows_per_tile(p, b), ntiles = k1_ntiles(p, b);
+        const int tr = k12_rows_per_tile(p, b), ntiles = k12_ntiles(p, b);
         std::vector<int32_t> idx(p.m), cnt(ntiles);
         std::vector<uint8_t> tm(p.m);
         cudaError_t e = cudaSetDevice(p.device);
@@ -552,4 +528,11 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
         *nnz_union = k;
         return CATS_OK;
     })
+}
+
+extern "C" cats_status_t cats_mlp_trace_info(const cats_mlp_plan_t *plan, size_t *offset, size_t *bytes) {
+    if (!plan || !offset || !bytes) return CATS_E_NULL;
+    *offset = plan->p.off_trace;
+    *bytes = plan->p.trace_bytes;
+    return CATS_OK;
 }

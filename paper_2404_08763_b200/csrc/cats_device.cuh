@@ -100,6 +100,31 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait_primary() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// ---- diagnostics: per-CTA %globaltimer stamps into the workspace trace area (null = off) ----
+constexpr int kTraceCtas = 512, kTraceSlots = 8, kTraceKernels = 3;
+__device__ __forceinline__ void trace_stamp(unsigned long long *tr, int kernel, int slot) {
+    if (tr != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceCtas) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tr[((size_t)kernel * kTraceCtas + blockIdx.x) * kTraceSlots + slot] = t;
+    }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace_put(unsigned long long *tr, int kernel, int slot, unsigned long long v) {
+    if (tr != nullptr && blockIdx.x < kTraceCtas) tr[((size_t)kernel * kTraceCtas + blockIdx.x) * kTraceSlots + slot] = v;
+}
+
+// ---- exact 64-bit fixed point for order-independent (deterministic) accumulation ----
+template <int SHIFT>
+__device__ __forceinline__ long long to_fixed_s(float v) { return __float2ll_rn(v * (float)(1ull << SHIFT)); }
+template <int SHIFT>
+__device__ __forceinline__ float from_fixed_s(long long v) { return (float)((double)v * (1.0 / (double)(1ull << SHIFT))); }
+
 // ---- warp reductions (fixed xor-butterfly: every lane ends with the same, order-fixed sum) ----
 __device__ __forceinline__ float warp_allreduce_sum(float v) {
 #pragma unroll

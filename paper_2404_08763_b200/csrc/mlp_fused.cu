@@ -1,0 +1,613 @@
+// mlp_fused.cu -- the CATS-MLP decode as ONE persistent dataflow kernel (K12) + a tiny reduce (K3).
+//
+// Paper: Custom GPU Kernel "MLP using CATS":
+//     v <- SiLU(x W_gate); Mask <- |v| >= t; x1 <- (x W_up[Mask]) * v[Mask]; y <- x1 W_down[Mask]
+// Eq. 1, Eq. 2 SiLU, Eq. 4/5 CATS_t, Optimization 1 -- the x v
+// multiply fused into the up tile so x1 never touches HBM, and App. D
+// Alg. 1 line 4 "idcs <- indices where Mask = 1" done per tile with a warp ballot (no
+// atomic appends).
+//
+// B200 design:
+//  * Work unit = a tile of NR consecutive neurons. Persistent CTAs (one per SM) pull tiles from a
+//    global counter, so SMs with more bandwidth take more tiles: no static-partition tail, and no
+//    grid-wide barrier between the gate GEMV and the sparse up/down projection.
+//  * Each CTA runs a ring of S shared-memory stages fed by the TMA bulk-copy engine
+//    (cp.async.bulk + mbarrier transaction counts). A stage holds one JOB:
+//        GATE(tile): the tile's NR rows of W_gate (neuron-major, contiguous);
+//        UD(<= NU active neurons of one tile): their W_up and W_down rows (contiguous 2d-byte rows).
+//  * Warp specialisation: 16 consumer warps do the arithmetic; one producer warp retires jobs in
+//    order (full/empty mbarrier pair per stage), turns a GATE job's partial dot products into
+//    u -> v = SiLU(u) -> keep = |v| >= t -> ballot compaction, queues the tile's active neurons as
+//    UD jobs, and refills freed stages (UD jobs first, else a new GATE tile). UD rows are requested
+//    S-1 jobs before they are consumed, so the mask -> load dependency is hidden and only active
+//    neurons' W_up / W_down rows are ever read (the paper's memory saving).
+//  * Consumer thread t owns 16-byte column chunks {t, t+512, ...} of d: x stays in registers (fp32);
+//    dot products are per-thread partials, a fixed xor butterfly per warp, then a fixed-order sum
+//    over the 16 warps. GATE jobs need no consumer barrier; UD jobs one named barrier.
+//  * Determinism under dynamic scheduling: a UD job's contribution y_job[c] = sum_i x1_i Wd[i][c]
+//    (<= NU neurons of ONE tile, ascending, fp32, fixed order) is converted once to a 64-bit
+//    fixed-point integer (scale 2^kFixShift) and added to the thread's integer accumulator. Integer
+//    addition is associative, so y does not depend on which CTA took which tile or in which order:
+//    bit-reproducible. (Replaces the paper's fp16 tl.atomic_add into Y.)
+//  * K3 sums the per-CTA integer partials (exact) and converts to fp32 once.
+//
+// Workspace outputs for introspection: tile tau's cnt[tau] active neurons are written ascending at
+// positions [tau*NR, tau*NR + cnt[tau]) of idx / tokmask / vals (v in fp32, 0 where |v| < t).
+#include "cats_device.cuh"
+#include "cats_internal.h"
+
+namespace cats {
+
+enum : int { kJobEnd = 0, kJobGate = 1, kJobUD = 2 };
+static_assert(kK12Threads == kConsumers + 32, "consumer warps + 1 producer warp");
+static_assert(32 % kConsumerWarps == 0, "cross-warp reduction packs 32 / NW pairs per round");
+
+__device__ __forceinline__ long long to_fixed(float v) { return to_fixed_s<kFixShift>(v); }
+__device__ __forceinline__ float from_fixed(long long v) { return from_fixed_s<kFixShift>(v); }
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumer_barrier() {  // named barrier 1: the consumer threads only
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+}
+
+template <int NU, int B>
+struct JobDesc {
+    int type;        // kJobEnd / kJobGate / kJobUD
+    int tile;        // tile id
+    int n;           // rows (GATE) or neurons (UD) in the stage
+    int id[NU];      // UD: neuron ids, ascending
+    float v[NU][B];  // UD: v = SiLU(u) per token, 0 where the token's |v| < t
+};
+
+template <typename T, int B, int NR, int CPT>
+__global__ void __launch_bounds__(kK12Threads, kCtasPerSm)
+k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restrict__ Wu, const T *__restrict__ Wd,
+             int d, int m, int stages, float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask,
+             float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
+             long long *__restrict__ ypart, unsigned int *__restrict__ sched, unsigned long long *__restrict__ trace) {
+    constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
+    constexpr int VEC = VecTraits<T>::kVec;
+    constexpr int NC = kConsumers;
+    constexpr int NW = kConsumerWarps;
+    constexpr int NPG = NR * B;  // (row, token) gate dot products per GATE job
+    constexpr int NPU = NU * B;  // (neuron, token) up dot products per UD job
+    constexpr int NPMAX = NPG > NPU ? NPG : NPU;
+    constexpr int QCAP = 64;     // pending UD jobs (each retired GATE adds <= 2, each refill takes 1)
+    static_assert(NR <= 32, "a GATE tile is compacted by one warp ballot");
+    using Desc = JobDesc<NU, B>;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nch = d * (int)sizeof(T) / 16;
+    const uint32_t row_bytes = (uint32_t)d * (uint32_t)sizeof(T);
+    const uint32_t stage_bytes = (uint32_t)NR * row_bytes;
+    const int ntiles = (m + NR - 1) / NR;
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char *ring = smem;                                                           // [stages][stage_bytes]
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * stage_bytes);   // [stages]
+    uint64_t *empty = full + stages;                                                      // [stages]
+    Desc *desc = reinterpret_cast<Desc *>(empty + stages);                                // [stages]
+    Desc *queue = desc + stages;                                                          // [QCAP]
+    float *red = reinterpret_cast<float *>(queue + QCAP);                                 // [stages][NW][NPMAX]
+
+    trace_stamp(trace, 0, 0);
+    pdl_launch_dependents();  // K3 may be scheduled early; it waits for this grid to complete
+
+    if (tid == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == NW) {
+        // ===================================== PRODUCER WARP =====================================
+        const bool dense = mode == kModeDense;
+        const bool gate_only = mode == kModeGateOnly;
+        const uint64_t policy = l2_evict_first_policy();
+        // tile ids, software-pipelined two deep (lane 0): t_next is resolved, t_pend is an atomic in
+        // flight. A GATE issue uses t_next, then moves t_pend -> t_next (its round trip overlapped
+        // one full GATE interval) and starts a new atomic. No select ever reads the newest atomic.
+        unsigned int t_next = 0, t_pend = 0;
+        int prod = 0;                // jobs issued; job j lives in stage j % stages
+        int ps = 0;                  // = prod % stages
+        int retire = 0;              // jobs retired (consumed and post-processed), in order
+        int q_head = 0, q_tail = 0;  // pending UD jobs
+        int gates_inflight = 0;      // GATE jobs issued, not yet retired
+        bool ended = false;
+        unsigned long long p_wait = 0, p_busy = 0, p_issue = 0;  // diagnostics (CATS_TRACE)
+
+        // issue job `prod` into its stage; returns false if nothing can be issued yet
+        auto issue_job = [&]() -> bool {
+            const int s = ps;
+            Desc &D = desc[s];
+            unsigned char *dst = ring + (size_t)s * stage_bytes;
+            if (q_head != q_tail) {  // UD job: W_up and W_down rows of <= NU active neurons
+                const Desc &Q = queue[q_head % QCAP];
+                const int qn = Q.n;
+                if (lane == 0) {
+                    D = Q;
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)qn * 2u * row_bytes);
+                }
+                __syncwarp();
+                if (lane < 2 * qn) {  // one bulk copy per lane: row (lane & 1) of neuron lane >> 1
+                    const int i = lane >> 1;
+                    const size_t j = (size_t)Q.id[i];
+                    bulk_g2s(dst + (size_t)lane * row_bytes, ((lane & 1) ? Wd : Wu) + j * d, row_bytes, &full[s],
+                             policy);
+                }
+                ++q_head;
+            } else {
+                const unsigned int tile = __shfl_sync(0xffffffffu, t_next, 0);
+                if (tile < (unsigned)ntiles) {  // GATE job: a new tile of W_gate rows
+                    const int r0 = (int)tile * NR;
+                    const int nr = min(NR, m - r0);
+                    if (lane == 0) {
+                        t_next = t_pend;
+                        t_pend = atomicAdd(&sched[0], 1u);
+                        D.type = kJobGate;
+                        D.tile = (int)tile;
+                        D.n = nr;
+                        mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
+                        bulk_g2s(dst, Wg + (size_t)r0 * d, (uint32_t)nr * row_bytes, &full[s], policy);
+                    }
+                    ++gates_inflight;
+                } else if (gates_inflight == 0) {  // no tiles left and no GATE job can create UD work
+                    if (lane == 0) {
+                        D.type = kJobEnd;
+                        D.n = 0;
+                        mbar_arrive_expect_tx(&full[s], 0u);
+                    }
+                    ended = true;
+                } else {
+                    return false;  // an in-flight GATE job will produce UD work: fill later
+                }
+            }
+            __syncwarp();
+            ++prod;
+            if (++ps == stages) ps = 0;
+            return true;
+        };
+
+        if (lane == 0) {
+            // prime the ring with a batch of consecutive GATE tiles (one atomic), at most the
+            // CTA's fair share so small layers still spread over all CTAs
+            const int batch = max(1, min(stages, ntiles / (int)gridDim.x));
+            const unsigned int base = atomicAdd(&sched[0], (unsigned)batch);
+            t_next = atomicAdd(&sched[0], 1u);
+            t_pend = atomicAdd(&sched[0], 1u);
+            for (int s = 0; s < batch; ++s) {
+                const unsigned int tile = base + s;
+                if (tile >= (unsigned)ntiles) break;
+                const int r0 = (int)tile * NR;
+                const int nr = min(NR, m - r0);
+                desc[s].type = kJobGate;
+                desc[s].tile = (int)tile;
+                desc[s].n = nr;
+                mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
+                bulk_g2s(ring + (size_t)s * stage_bytes, Wg + (size_t)r0 * d, (uint32_t)nr * row_bytes, &full[s],
+                         policy);
+                ++prod;
+            }
+        }
+        prod = __shfl_sync(0xffffffffu, prod, 0);
+        ps = prod % stages;
+        gates_inflight = prod;
+        while (!ended && prod < retire + stages && issue_job()) {
+        }
+        trace_stamp(trace, 0, 1);
+
+        int rs = 0;                  // = retire % stages
+        uint32_t rphase = 0;         // = (retire / stages) & 1
+        while (!ended) {
+            // ---- retire job `retire` in order ----
+            const unsigned long long tw0 = trace ? gtimer() : 0ull;
+            mbar_wait(&empty[rs], rphase);
+            const unsigned long long tw1 = trace ? gtimer() : 0ull;
+            p_wait += tw1 - tw0;
+            if (desc[rs].type == kJobGate) {
+                // u (fixed-order sum over the 16 consumer warps) -> v = SiLU(u) (Eq. 2) ->
+                // keep = |v| >= t (Eq. 4, ties kept) -> ballot compaction of the tile
+                const int tile = desc[rs].tile, n = desc[rs].n, r0 = tile * NR;
+                const float *rb = red + (size_t)rs * NW * NPMAX;
+                uint32_t bits = 0;
+                float vrow[B];
+#pragma unroll
+                for (int tk = 0; tk < B; ++tk) {
+                    float u = 0.f;
+                    if (lane < n) {
+#pragma unroll
+                        for (int w = 0; w < NW; ++w) u += rb[w * NPMAX + lane * B + tk];
+                    }
+                    const float v = __fdividef(u, 1.0f + __expf(-u));
+                    vrow[tk] = v;
+                    const bool keep = dense || gate_only || (fabsf(v) >= t);
+                    bits |= (keep ? 1u : 0u) << tk;
+                    if (acts && lane < n) acts[(size_t)tk * m + (size_t)(r0 + lane)] = v;
+                }
+                const bool act = (lane < n) && bits != 0u;
+                const uint32_t bal = __ballot_sync(0xffffffffu, act);
+                const int rank = __popc(bal & ((1u << lane) - 1u));
+                const int nact = __popc(bal);
+                if (act) {
+                    const int pos = r0 + rank;
+                    idx[pos] = r0 + lane;
+                    tokmask[pos] = (uint8_t)bits;
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) vals[(size_t)pos * B + tk] = ((bits >> tk) & 1u) ? vrow[tk] : 0.0f;
+                    if (!gate_only) {  // queue the tile's active neurons, NU per UD job, ascending
+                        Desc &Q = queue[(q_tail + rank / NU) % QCAP];
+                        const int i = rank % NU;
+                        Q.id[i] = r0 + lane;
+#pragma unroll
+                        for (int tk = 0; tk < B; ++tk) Q.v[i][tk] = ((bits >> tk) & 1u) ? vrow[tk] : 0.0f;
+                        if (i == 0) {
+                            Q.type = kJobUD;
+                            Q.tile = tile;
+                            Q.n = min(NU, nact - rank);
+                        }
+                    }
+                }
+                if (lane == 0) cnt[tile] = nact;
+                if (!gate_only) q_tail += (nact + NU - 1) / NU;
+                --gates_inflight;
+                __syncwarp();
+            }
+            ++retire;
+            if (++rs == stages) { rs = 0; rphase ^= 1u; }
+            const unsigned long long tw2 = trace ? gtimer() : 0ull;
+            // ---- refill every free stage (UD jobs first, else new GATE tiles, else END) ----
+            while (!ended && prod < retire + stages && issue_job()) {
+            }
+            if (trace) {
+                const unsigned long long tw3 = gtimer();
+                p_busy += tw3 - tw1;
+                p_issue += tw3 - tw2;
+            }
+        }
+        if (lane == 0) {
+            trace_put(trace, 2, 0, p_wait);
+            trace_put(trace, 2, 1, p_busy);
+            trace_put(trace, 2, 2, (unsigned long long)retire);
+            trace_put(trace, 2, 6, p_issue);
+        }
+    } else {
+        // ===================================== CONSUMER WARPS ====================================
+        float xr[B][CPT][VEC];  // x, own chunks, fp32
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const int ch = tid + k * NC;
+#pragma unroll
+            for (int tk = 0; tk < B; ++tk) {
+                if (ch < nch) {
+                    unpack16(*reinterpret_cast<const uint4 *>(x + (size_t)tk * d + (size_t)ch * VEC), xr[tk][k]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) xr[tk][k][e] = 0.f;
+                }
+            }
+        }
+        long long yacc[B][CPT][VEC];  // exact fixed-point partial of y, own chunks
+#pragma unroll
+        for (int tk = 0; tk < B; ++tk)
+#pragma unroll
+            for (int k = 0; k < CPT; ++k)
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) yacc[tk][k][e] = 0;
+
+        int s = 0;
+        uint32_t phase = 0;
+        unsigned long long c_wait = 0;
+        int n_gate = 0, n_ud = 0;
+        for (;;) {
+            const unsigned long long cw0 = trace ? gtimer() : 0ull;
+            mbar_wait(&full[s], phase);
+            if (trace) c_wait += gtimer() - cw0;
+            const int type = desc[s].type;
+            if (type == kJobEnd) break;
+            const int n = desc[s].n;
+            const uint32_t sbase = smem_u32(ring + (size_t)s * stage_bytes);
+            float *rb = red + (size_t)s * NW * NPMAX;
+
+            if (type == kJobGate) {
+                ++n_gate;
+                // ---- u = x W_gate[:, j] partials for the tile's rows ----
+                uint4 wr[NR][CPT];
+#pragma unroll
+                for (int r = 0; r < NR; ++r)
+#pragma unroll
+                    for (int k = 0; k < CPT; ++k) {
+                        const int ch = tid + k * NC;
+                        wr[r][k] = (r < n && ch < nch) ? lds128(sbase + (uint32_t)r * row_bytes + (uint32_t)ch * 16u)
+                                                       : make_uint4(0u, 0u, 0u, 0u);
+                    }
+                float part[NR][B];
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) part[r][tk] = 0.f;
+#pragma unroll
+                    for (int k = 0; k < CPT; ++k) {
+                        float wf[VEC];
+                        unpack16(wr[r][k], wf);
+#pragma unroll
+                        for (int tk = 0; tk < B; ++tk)
+#pragma unroll
+                            for (int e = 0; e < VEC; ++e) part[r][tk] = fmaf(xr[tk][k][e], wf[e], part[r][tk]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < NR; ++r)
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) {
+                        const float v = warp_allreduce_sum(part[r][tk]);
+                        if (lane == 0) rb[warp * NPMAX + r * B + tk] = v;
+                    }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);  // stage read + partials written -> producer
+            } else {  // kJobUD
+                ++n_ud;
+                float vj[NU][B];  // descriptor -> registers before releasing the stage
+#pragma unroll
+                for (int i = 0; i < NU; ++i)
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) vj[i][tk] = desc[s].v[i][tk];
+                uint4 wu[NU][CPT], wd[NU][CPT];
+#pragma unroll
+                for (int i = 0; i < NU; ++i)
+#pragma unroll
+                    for (int k = 0; k < CPT; ++k) {
+                        const int ch = tid + k * NC;
+                        const bool ok = i < n && ch < nch;
+                        wu[i][k] = ok ? lds128(sbase + (uint32_t)(2 * i) * row_bytes + (uint32_t)ch * 16u)
+                                      : make_uint4(0u, 0u, 0u, 0u);
+                        wd[i][k] = ok ? lds128(sbase + (uint32_t)(2 * i + 1) * row_bytes + (uint32_t)ch * 16u)
+                                      : make_uint4(0u, 0u, 0u, 0u);
+                    }
+                // ---- up: partial dots x . W_up[j] ----
+                float part[NU][B];
+#pragma unroll
+                for (int i = 0; i < NU; ++i) {
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) part[i][tk] = 0.f;
+#pragma unroll
+                    for (int k = 0; k < CPT; ++k) {
+                        float wf[VEC];
+                        unpack16(wu[i][k], wf);
+#pragma unroll
+                        for (int tk = 0; tk < B; ++tk)
+#pragma unroll
+                            for (int e = 0; e < VEC; ++e) part[i][tk] = fmaf(xr[tk][k][e], wf[e], part[i][tk]);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < NU; ++i)
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) {
+                        const float v = warp_allreduce_sum(part[i][tk]);
+                        if (lane == 0) rb[warp * NPMAX + i * B + tk] = v;
+                    }
+                consumer_barrier();  // all 16 warps' partials are in red[s]
+                // ---- cross-warp sums (fixed tree, identical in every warp): lane l reads warp
+                //      (l % NW)'s partial of pair c*PPR + l/NW; an xor butterfly over NW lanes sums them.
+                constexpr int PPR = 32 / NW;
+                float a[NPU];
+#pragma unroll
+                for (int c = 0; c < (NPU + PPR - 1) / PPR; ++c) {
+                    const int pp = c * PPR + lane / NW;
+                    float v = (pp < NPU) ? rb[(lane % NW) * NPMAX + pp] : 0.f;
+#pragma unroll
+                    for (int o = NW / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+#pragma unroll
+                    for (int q = 0; q < PPR; ++q)
+                        if (c * PPR + q < NPU) a[c * PPR + q] = __shfl_sync(0xffffffffu, v, q * NW);
+                }
+                // stage data, descriptor and red[s] are no longer needed: release the stage
+                if (lane == 0) mbar_arrive(&empty[s]);
+                // x1_j = (x W_up[j]) * v_j  (Optimization 1)
+                float x1[NU][B];
+#pragma unroll
+                for (int i = 0; i < NU; ++i)
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) x1[i][tk] = (i < n) ? a[i * B + tk] * vj[i][tk] : 0.f;
+                // ---- down: y_job[c] = sum_i x1_i W_down[i][c] (fp32, fixed order) -> fixed point ----
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    float wf[NU][VEC];
+#pragma unroll
+                    for (int i = 0; i < NU; ++i) unpack16(wd[i][k], wf[i]);
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk)
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            float yj = 0.f;
+#pragma unroll
+                            for (int i = 0; i < NU; ++i) yj = fmaf(x1[i][tk], wf[i][e], yj);
+                            yacc[tk][k][e] += to_fixed(yj);
+                        }
+                }
+            }
+            if (++s == stages) { s = 0; phase ^= 1u; }
+        }
+        trace_stamp(trace, 0, 2);
+        if (tid == 0) {
+            trace_put(trace, 2, 3, c_wait);
+            trace_put(trace, 2, 4, (unsigned long long)n_gate);
+            trace_put(trace, 2, 5, (unsigned long long)n_ud);
+        }
+
+        // ---- this CTA's exact integer partial of y ----
+        if (mode != kModeGateOnly) {
+            long long *yp = ypart + (size_t)blockIdx.x * B * d;
+#pragma unroll
+            for (int tk = 0; tk < B; ++tk)
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    const int ch = tid + k * NC;
+                    if (ch < nch) {
+                        longlong2 *dst = reinterpret_cast<longlong2 *>(yp + (size_t)tk * d + (size_t)ch * VEC);
+#pragma unroll
+                        for (int q = 0; q < VEC / 2; ++q)
+                            dst[q] = make_longlong2(yacc[tk][k][2 * q], yacc[tk][k][2 * q + 1]);
+                    }
+                }
+        }
+        trace_stamp(trace, 0, 3);
+    }
+}
+
+// K3: y[b][d] = (sum_p ypart[p][b][d]) * 2^-kFixShift -- exact integer sum (any order), one
+// rounding to fp32. A 256-thread block owns 8 consecutive 16-byte columns; its 32 groups of 8 lanes
+// each sum the partials p = g, g+32, ... (one 128-byte line per partial, all loads in flight), then
+// the 32 group sums meet in shared memory. Many small blocks spread the L2 reads over every SM.
+// Re-arms K12's tile scheduler (K12 has completed).
+__global__ void __launch_bounds__(kK3Threads)
+k3_fixed_reduce(const longlong2 *__restrict__ ypart, int p2, int n2, float2 *__restrict__ y,
+                unsigned int *__restrict__ sched, unsigned long long *__restrict__ trace) {
+    constexpr int kCols = 8, kGroups = kK3Threads / kCols, kPerLane = 12;
+    __shared__ longlong2 sacc[kGroups][kCols];
+    trace_stamp(trace, 1, 0);
+    pdl_wait_primary();
+    trace_stamp(trace, 1, 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) sched[0] = 0u;
+    const int c = threadIdx.x % kCols, g = threadIdx.x / kCols;
+    const int f = blockIdx.x * kCols + c;
+    long long ax = 0, ay = 0;
+    if (f < n2) {
+        for (int base = g; base < p2; base += kGroups * kPerLane) {
+            longlong2 v[kPerLane];
+#pragma unroll
+            for (int i = 0; i < kPerLane; ++i) {
+                const int pp = base + kGroups * i;
+                v[i] = pp < p2 ? ypart[(size_t)pp * n2 + f] : make_longlong2(0, 0);
+            }
+#pragma unroll
+            for (int i = 0; i < kPerLane; ++i) {
+                ax += v[i].x;
+                ay += v[i].y;
+            }
+        }
+    }
+    sacc[g][c] = make_longlong2(ax, ay);
+    __syncthreads();
+    if (threadIdx.x < kCols && f < n2) {
+        long long sx = 0, sy = 0;
+#pragma unroll 8
+        for (int w = 0; w < kGroups; ++w) {
+            sx += sacc[w][c].x;
+            sy += sacc[w][c].y;
+        }
+        y[f] = make_float2(from_fixed(sx), from_fixed(sy));
+    }
+    trace_stamp(trace, 1, 2);
+}
+
+size_t k12_smem_bytes(const PlanData &p, int b, int stages) {
+    const int nr = k12_rows_per_tile(p, b);
+    const int nu = nr / 2;
+    size_t s = (size_t)stages * nr * (size_t)p.d * p.esize;  // ring
+    s += (size_t)stages * 16;                                // full + empty mbarriers
+    const size_t desc = (size_t)(3 + nu) * 4 + (size_t)nu * b * 4;
+    s += (size_t)(stages + 64) * desc;                       // stage descriptors + UD queue
+    s = (s + 15) & ~(size_t)15;
+    s += (size_t)stages * kConsumerWarps * std::max(nr, nu) * b * 4;  // per-stage warp partials
+    return (s + 127) & ~(size_t)127;
+}
+
+template <typename T, int B, int NR, int CPT>
+static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
+                                float t, int mode, float *acts, void *ws, cudaStream_t s) {
+    auto kern = k12_cats_mlp<T, B, NR, CPT>;
+    const int stages = k12_stages(p, B);
+    const size_t smem = k12_smem_bytes(p, B, stages);
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
+    if (e != cudaSuccess) return e;
+    char *w = static_cast<char *>(ws);
+    kern<<<p.g1, kK12Threads, smem, s>>>(
+        static_cast<const T *>(x), static_cast<const T *>(Wg), static_cast<const T *>(Wu), static_cast<const T *>(Wd),
+        p.d, p.m, stages, t, mode, reinterpret_cast<int32_t *>(w + p.off_idx),
+        reinterpret_cast<uint8_t *>(w + p.off_tokmask), reinterpret_cast<float *>(w + p.off_vals),
+        reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<long long *>(w + p.off_ypart),
+        reinterpret_cast<unsigned int *>(w + p.off_sched),
+        p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
+    return cudaGetLastError();
+}
+
+template <typename T, int B, int NR>
+static cudaError_t launch_k12_r(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
+                                float t, int mode, float *acts, void *ws, cudaStream_t s) {
+    switch (p.cpt) {
+        case 1: return launch_k12_t<T, B, NR, 1>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 2: return launch_k12_t<T, B, NR, 2>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 3: return launch_k12_t<T, B, NR, 3>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 4: return launch_k12_t<T, B, NR, 4>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <typename T, int B>
+static cudaError_t launch_k12_b(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
+                                float t, int mode, float *acts, void *ws, cudaStream_t s) {
+    switch (k12_rows_per_tile(p, B)) {
+        case 4: return launch_k12_r<T, B, 4>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 2: return launch_k12_r<T, B, 2>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <typename T>
+static cudaError_t launch_k12_dt(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu,
+                                 const void *Wd, float t, int mode, float *acts, void *ws, cudaStream_t s) {
+    switch (b) {
+        case 1: return launch_k12_b<T, 1>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 2: return launch_k12_b<T, 2>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 3: return launch_k12_b<T, 3>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 4: return launch_k12_b<T, 4>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 5: return launch_k12_b<T, 5>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 6: return launch_k12_b<T, 6>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 7: return launch_k12_b<T, 7>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 8: return launch_k12_b<T, 8>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_k12(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd,
+                       float t, int mode, float *acts, void *ws, cudaStream_t s) {
+    if (p.dt == CATS_BF16) return launch_k12_dt<bf16_bits>(p, x, b, Wg, Wu, Wd, t, mode, acts, ws, s);
+    return launch_k12_dt<float>(p, x, b, Wg, Wu, Wd, t, mode, acts, ws, s);
+}
+
+static cudaError_t launch_ex(const void *func, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                             void **args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelExC(&cfg, func, args);
+}
+
+cudaError_t launch_k3(const PlanData &p, int b, void *ws, float *y, cudaStream_t s, bool pdl) {
+    char *w = static_cast<char *>(ws);
+    const longlong2 *ypart = reinterpret_cast<const longlong2 *>(w + p.off_ypart);
+    int p2 = p.g1;
+    int n2 = b * p.d / 2;
+    float2 *y2 = reinterpret_cast<float2 *>(y);
+    unsigned int *sched = reinterpret_cast<unsigned int *>(w + p.off_sched);
+    unsigned long long *trace = p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr;
+    const int grid = (n2 + 7) / 8;
+    void *args[] = {&ypart, &p2, &n2, &y2, &sched, &trace};
+    return launch_ex(reinterpret_cast<const void *>(k3_fixed_reduce), dim3(grid), dim3(kK3Threads), 0, s, pdl,
+                     args);
+}
+
+}  // namespace cats

@@ -1,0 +1,77 @@
+"""Per-CTA timeline of one pipelined decode step (CATS_TRACE=1 globaltimer stamps).
+
+    CATS_TRACE=1 python scripts/trace_decode.py [--model mistral-7b] [--batch 1] [--graph]
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+os.environ["CATS_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import cats_synth
+import paper_2404_08763_b200 as cats
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--model", default="mistral-7b")
+ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--k", type=float, default=0.5)
+ap.add_argument("--dense", action="store_true")
+ap.add_argument("--json")
+a = ap.parse_args()
+d, m = cats_synth.MODELS[a.model]
+dev = torch.device("cuda:0")
+W = [w.to(dev) for w in cats_synth.mlp_weights(d, m, torch.bfloat16)]
+copies = [W] + [[w.clone() for w in W] for _ in range(3)]
+plan = cats.MlpPlan(d, m, max_batch=8)
+ws = plan.workspace()
+off, nbytes = ctypes.c_size_t(), ctypes.c_size_t()
+plan._lib.cats_mlp_trace_info(plan.handle, ctypes.byref(off), ctypes.byref(nbytes))
+assert nbytes.value > 0, "tracing off"
+xc = cats_synth.tokens(64, d, torch.bfloat16, seed=0).to(dev)
+acts = torch.cat([cats.cats_mlp_gate_act(plan, xc[i:i + 8], W[0], ws=ws) for i in range(0, 64, 8)])
+t, _ = cats.cats_calibrate_threshold(acts, a.k)
+x = cats_synth.tokens(a.batch, d, torch.bfloat16, seed=1).to(dev)
+y = torch.empty(a.batch, d, device=dev)
+
+
+def step(i):
+    c = copies[i % 4]
+    if a.dense:
+        cats.cats_mlp_dense(plan, x, c[0], c[1], c[2], y=y, ws=ws)
+    else:
+        cats.cats_mlp_decode(plan, x, c[0], c[1], c[2], t, y=y, ws=ws)
+
+
+for i in range(20):
+    step(i)
+torch.cuda.synchronize()
+ws[off.value:off.value + nbytes.value].zero_()
+step(20)
+torch.cuda.synchronize()
+tr = ws[off.value:off.value + nbytes.value].cpu().numpy().view(np.uint64).reshape(3, 512, 8).astype(np.int64)
+info = plan.info
+grids = [info["grid"], (a.batch * d // 2 + 7) // 8]
+t0 = tr[0, :grids[0], 0].min()
+rep = {}
+names = {0: ["start", "primed", "jobs_done", "exit"], 1: ["start", "k12_visible", "exit"]}
+for k in range(2):
+    g = min(grids[k], 512)
+    print(f"K{k + 1} ({g} CTAs), us relative to first K1 CTA start:")
+    for sidx, nm in enumerate(names[k]):
+        v = (tr[k, :g, sidx] - t0) / 1e3
+        v = v[tr[k, :g, sidx] > 0]
+        if len(v):
+            print(f"   {nm:12s} min {v.min():8.2f}  avg {v.mean():8.2f}  max {v.max():8.2f}")
+            rep[f"K{k + 1}.{nm}"] = [float(v.min()), float(v.mean()), float(v.max())]
+g = grids[0]
+st = tr[2, :g, :7].astype(np.float64)
+print("K12 per-CTA stats (avg/min/max):")
+for i, nm in enumerate(["producer wait ns", "producer busy ns", "jobs retired", "consumer wait ns", "gate jobs", "ud jobs", "producer issue ns"]):
+    print(f"   {nm:18s} {st[:, i].mean():10.1f} {st[:, i].min():10.1f} {st[:, i].max():10.1f}")
+if a.json:
+    json.dump(rep, open(a.json, "w"), indent=1)

@@ -57,15 +57,16 @@ def test_rank_rule_exact():
 def test_plan_without_gpu():
     p = cats.MlpPlan(4096, 14336, max_batch=1, dtype=torch.bfloat16, num_sms=148)
     i = p.info
-    assert i["k1_grid"] == 148 and i["k2_grid"] == 148 and i["k2_stages"] >= 2 and i["k1_stages"] >= 2
-    assert i["k2_smem"] <= 227 * 1024 and i["k1_smem_max"] <= 227 * 1024
+    assert i["grid"] == 2 * 148 and i["stages"] >= 3 and i["rows_per_tile"] == 4
+    assert 2 * (i["smem"] + 1024) <= 228 * 1024      # two K12 CTAs per SM
     assert i["workspace_bytes"] >= 148 * 4096 * 4
     toy = cats.MlpPlan(64, 176, max_batch=1, dtype=torch.float32, num_sms=148)
-    assert toy.info["k1_grid"] == 176 // 8           # no more CTAs than K1 tiles
+    assert toy.info["grid"] == 176 // 4              # no more CTAs than tiles
     small = cats.MlpPlan(64, 5, max_batch=8, dtype=torch.float32, num_sms=148)
-    assert small.info["k1_grid"] == 1
+    assert small.info["grid"] == 2
     for b in range(1, 9):                            # every batch size fits the shared-memory budget
-        assert cats.MlpPlan(5120, 13824, max_batch=b, num_sms=148).info["k2_smem"] <= 227 * 1024
+        assert cats.MlpPlan(5120, 13824, max_batch=b, num_sms=148).info["smem"] <= 113 * 1024
+    assert cats.MlpPlan(8192, 1000, max_batch=8, num_sms=148).info["stages"] >= 3
 
 
 @pytest.mark.parametrize("args,err", [
