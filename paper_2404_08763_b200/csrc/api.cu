@@ -325,13 +325,14 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.esize = esize;
         p.vec = 16 / esize;
         p.nchunks = d * esize / 16;
-        p.cpt = (p.nchunks + kConsumers - 1) / kConsumers;  // chunks per column-owning consumer thread
-        if (p.cpt > kMaxCPT) return CATS_E_UNSUPPORTED;
-        // K12: one persistent CTA per SM pulling NR-row tiles from a global counter
-        p.g1 = std::min(num_sms * kCtasPerSm, k12_ntiles(p, 1));
-        for (int b = 1; b <= max_batch; ++b)
-            if (k12_stages(p, b) < 3 || k12_smem_bytes(p, b, k12_stages(p, b)) > kSmemBudget)
+        // K12: persistent CTAs pulling NR-row tiles from a global counter
+        p.g1 = 0;
+        for (int b = 1; b <= max_batch; ++b) {
+            if (k12_cpt(p, b) > (b == 1 ? kMaxCPT : 2)) return CATS_E_UNSUPPORTED;
+            if (k12_stages(p, b) < 3 || k12_smem_bytes(p, b, k12_stages(p, b)) > k12_smem_budget_c(b))
                 return CATS_E_UNSUPPORTED;
+            p.g1 = std::max(p.g1, k12_grid(p, b));
+        }
         // workspace
         size_t off = 0;
         p.off_sched = off;   off = align_up(off + 64, 256);
@@ -367,8 +368,8 @@ extern "C" cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_ml
     info->w_dtype = p.dt;
     info->device = p.device;
     info->num_sms = p.num_sms;
-    info->grid = p.g1;
-    info->threads = kK12Threads;
+    info->grid = k12_grid(p, b);
+    info->threads = k12_threads_c(b);
     info->rows_per_tile = k12_rows_per_tile(p, b);
     info->stages = k12_stages(p, b);
     info->smem = k12_smem_bytes(p, b, info->stages);

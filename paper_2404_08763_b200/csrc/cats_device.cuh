@@ -119,11 +119,36 @@ __device__ __forceinline__ void trace_put(unsigned long long *tr, int kernel, in
     if (tr != nullptr && blockIdx.x < kTraceCtas) tr[((size_t)kernel * kTraceCtas + blockIdx.x) * kTraceSlots + slot] = v;
 }
 
-// ---- exact 64-bit fixed point for order-independent (deterministic) accumulation ----
-template <int SHIFT>
-__device__ __forceinline__ long long to_fixed_s(float v) { return __float2ll_rn(v * (float)(1ull << SHIFT)); }
-template <int SHIFT>
-__device__ __forceinline__ float from_fixed_s(long long v) { return (float)((double)v * (1.0 / (double)(1ull << SHIFT))); }
+// ---- exact fixed point for order-independent (deterministic) accumulation ----
+// A value y is accumulated as the integer q = round(y * 2^30) held in two int32 halves,
+// q = hi * 2^22 + lo. The split uses the fp32 "magic number" rounding trick (all full-rate FADD /
+// IADD, no slow float->int64 conversion): t = y * 2^8 is pre-scaled by the caller (exact),
+// hi = round(t) via t + 1.5*2^23, the exact remainder f = t - hi (|f| <= 1/2), lo = round(f * 2^22).
+// Only lo is rounded, so q = round(y * 2^30) exactly (|t| < 2^21). Larger |t| take a slow path.
+constexpr int kFixLoBits = 22;
+constexpr float kFixPre = 256.0f;                  // 2^8: callers pre-scale y by this (exact)
+constexpr float kFixMagic = 12582912.0f;           // 1.5 * 2^23
+constexpr int kFixMagicBits = 0x4B400000;
+__device__ __forceinline__ void fix_acc(int &hi, int &lo, float t) {
+    if (fabsf(t) < 2097152.0f) {  // 2^21
+        const float h = t + kFixMagic;
+        hi += __float_as_int(h) - kFixMagicBits;
+        const float f = t - (h - kFixMagic);
+        lo += __float_as_int(fmaf(f, 4194304.0f, kFixMagic)) - kFixMagicBits;  // round(f * 2^22)
+    } else {
+        const long long q = __float2ll_rn(t * 4194304.0f);
+        hi += (int)(q >> kFixLoBits);
+        lo += (int)(q & ((1ll << kFixLoBits) - 1));
+    }
+}
+__device__ __forceinline__ void fix_renorm(int &hi, int &lo) {  // keep |lo| < 2^22 (exact)
+    const int c = lo >> kFixLoBits;
+    hi += c;
+    lo -= c << kFixLoBits;
+}
+__device__ __forceinline__ long long fix_value(int hi, int lo) { return ((long long)hi << kFixLoBits) + lo; }
+constexpr int kFixShift = 30;  // q is in units of 2^-30
+__device__ __forceinline__ float fix_to_float(long long q) { return (float)((double)q * (1.0 / 1073741824.0)); }
 
 // ---- warp reductions (fixed xor-butterfly: every lane ends with the same, order-fixed sum) ----
 __device__ __forceinline__ float warp_allreduce_sum(float v) {

@@ -11,15 +11,17 @@
 
 namespace cats {
 
-constexpr int kConsumerWarps = 8;     // K12: consumer warps per CTA (column owners)
-constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kK12Threads = kConsumers + 32;  // + 1 producer warp
-constexpr int kCtasPerSm = 2;         // two independent job streams per SM hide per-job latency
+// K12 CTA shapes: b = 1 runs two CTAs per SM with 8 consumer warps each (two independent job streams
+// hide per-job latency); b >= 2 runs one CTA per SM with 16 consumer warps (half the columns per
+// thread, so x and the fixed-point y partials of every token fit in registers).
+constexpr int k12_consumer_warps_c(int b) { return b == 1 ? 8 : 16; }
+constexpr int k12_ctas_per_sm_c(int b) { return b == 1 ? 2 : 1; }
+constexpr int k12_threads_c(int b) { return k12_consumer_warps_c(b) * 32 + 32; }  // + 1 producer warp
+constexpr size_t k12_smem_budget_c(int b) { return b == 1 ? 112 * 1024 : 224 * 1024; }
 constexpr int kK3Threads = 256;
-constexpr size_t kSmemBudget = 112 * 1024;  // dynamic shared memory per K12 CTA (2 per SM)
+constexpr size_t kSmemBudget = 224 * 1024;  // dynamic shared memory per CTA, one CTA per SM
 constexpr int kMaxCPT = 4;            // 16-byte chunks of a row owned per consumer (d <= 8192 bf16)
 constexpr int kMaxStages = 8;
-constexpr int kFixShift = 36;         // y partials: exact 64-bit fixed point, resolution 2^-36
 
 // K12 launch modes
 constexpr int kModeCats = 0;          // CATS_t decode
@@ -33,8 +35,7 @@ struct PlanData {
     int esize;          // bytes per element
     int vec;            // elements per 16 bytes
     int nchunks;        // d * esize / 16
-    int cpt;            // chunks per consumer thread
-    int g1;             // K12 CTAs (persistent, dynamic tile scheduler)
+    int g1;             // max K12 CTAs over batch sizes (sizes the partial buffer)
     // workspace layout (byte offsets)
     size_t off_sched, off_idx, off_tokmask, off_vals, off_cnt, off_ypart, off_xstage, off_ystage, ws_bytes;
     bool trace;         // CATS_TRACE=1 at plan creation: kernels stamp %globaltimer into the workspace
@@ -44,16 +45,22 @@ struct PlanData {
 // K12 tile height NR (W_gate rows per GATE job; a UD job carries NR/2 neurons = the same bytes).
 inline int k12_rows_per_tile(const PlanData &p, int b) {
     const size_t row = (size_t)p.d * p.esize;
-    (void)b;
-    return 4 * row * 3 <= kSmemBudget - 8 * 1024 ? 4 : 2;
+    return 4 * row * 3 <= k12_smem_budget_c(b) - 8 * 1024 ? 4 : 2;
 }
 inline int k12_ntiles(const PlanData &p, int b) { return (p.m + k12_rows_per_tile(p, b) - 1) / k12_rows_per_tile(p, b); }
+inline int k12_cpt(const PlanData &p, int b) {
+    const int nc = k12_consumer_warps_c(b) * 32;
+    return (p.nchunks + nc - 1) / nc;
+}
+inline int k12_grid(const PlanData &p, int b) {
+    return std::min(p.num_sms * k12_ctas_per_sm_c(b), k12_ntiles(p, b));
+}
 size_t k12_smem_bytes(const PlanData &p, int b, int stages);
 inline int k12_stages(const PlanData &p, int b) {
     const size_t stage = (size_t)k12_rows_per_tile(p, b) * p.d * p.esize;
     const size_t extra = k12_smem_bytes(p, b, 0) + kMaxStages * 256;
-    if (extra >= kSmemBudget) return 0;
-    return (int)std::min<size_t>((kSmemBudget - extra) / stage, kMaxStages);
+    if (extra >= k12_smem_budget_c(b)) return 0;
+    return (int)std::min<size_t>((k12_smem_budget_c(b) - extra) / stage, kMaxStages);
 }
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel / size (thread-safe)

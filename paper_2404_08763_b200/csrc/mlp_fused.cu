@@ -25,8 +25,9 @@
 //    dot products are per-thread partials, a fixed xor butterfly per warp, then a fixed-order sum
 //    over the 16 warps. GATE jobs need no consumer barrier; UD jobs one named barrier.
 //  * Determinism under dynamic scheduling: a UD job's contribution y_job[c] = sum_i x1_i Wd[i][c]
-//    (<= NU neurons of ONE tile, ascending, fp32, fixed order) is converted once to a 64-bit
-//    fixed-point integer (scale 2^kFixShift) and added to the thread's integer accumulator. Integer
+//    (<= NU neurons of ONE tile, ascending, fp32, fixed order) is converted once to an exact
+//    fixed-point integer round(y_job * 2^30) (split into two int32 halves, cats_device.cuh
+//    fix_acc) and added to the thread's integer accumulator. Integer
 //    addition is associative, so y does not depend on which CTA took which tile or in which order:
 //    bit-reproducible. (Replaces the paper's fp16 tl.atomic_add into Y.)
 //  * K3 sums the per-CTA integer partials (exact) and converts to fp32 once.
@@ -39,17 +40,14 @@
 namespace cats {
 
 enum : int { kJobEnd = 0, kJobGate = 1, kJobUD = 2 };
-static_assert(kK12Threads == kConsumers + 32, "consumer warps + 1 producer warp");
-static_assert(32 % kConsumerWarps == 0, "cross-warp reduction packs 32 / NW pairs per round");
 
-__device__ __forceinline__ long long to_fixed(float v) { return to_fixed_s<kFixShift>(v); }
-__device__ __forceinline__ float from_fixed(long long v) { return from_fixed_s<kFixShift>(v); }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+template <int NTHREADS>
 __device__ __forceinline__ void consumer_barrier() {  // named barrier 1: the consumer threads only
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(NTHREADS) : "memory");
 }
 
 template <int NU, int B>
@@ -62,15 +60,16 @@ struct JobDesc {
 };
 
 template <typename T, int B, int NR, int CPT>
-__global__ void __launch_bounds__(kK12Threads, kCtasPerSm)
+__global__ void __launch_bounds__(k12_threads_c(B), k12_ctas_per_sm_c(B))
 k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restrict__ Wu, const T *__restrict__ Wd,
              int d, int m, int stages, float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask,
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
              long long *__restrict__ ypart, unsigned int *__restrict__ sched, unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
-    constexpr int NC = kConsumers;
-    constexpr int NW = kConsumerWarps;
+    constexpr int NW = k12_consumer_warps_c(B);
+    constexpr int NC = NW * 32;
+    static_assert(32 % NW == 0, "cross-warp reduction packs 32 / NW pairs per round");
     constexpr int NPG = NR * B;  // (row, token) gate dot products per GATE job
     constexpr int NPU = NU * B;  // (neuron, token) up dot products per UD job
     constexpr int NPMAX = NPG > NPU ? NPG : NPU;
@@ -291,13 +290,14 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 }
             }
         }
-        long long yacc[B][CPT][VEC];  // exact fixed-point partial of y, own chunks
+        int yhi[B][CPT][VEC], ylo[B][CPT][VEC];  // exact fixed-point partial of y (units 2^-30), own chunks
 #pragma unroll
         for (int tk = 0; tk < B; ++tk)
 #pragma unroll
             for (int k = 0; k < CPT; ++k)
 #pragma unroll
-                for (int e = 0; e < VEC; ++e) yacc[tk][k][e] = 0;
+                for (int e = 0; e < VEC; ++e) yhi[tk][k][e] = ylo[tk][k][e] = 0;
+        int n_since_renorm = 0;
 
         int s = 0;
         uint32_t phase = 0;
@@ -391,7 +391,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                         const float v = warp_allreduce_sum(part[i][tk]);
                         if (lane == 0) rb[warp * NPMAX + i * B + tk] = v;
                     }
-                consumer_barrier();  // all 16 warps' partials are in red[s]
+                consumer_barrier<NC>();  // all 16 warps' partials are in red[s]
                 // ---- cross-warp sums (fixed tree, identical in every warp): lane l reads warp
                 //      (l % NW)'s partial of pair c*PPR + l/NW; an xor butterfly over NW lanes sums them.
                 constexpr int PPR = 32 / NW;
@@ -408,12 +408,13 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 }
                 // stage data, descriptor and red[s] are no longer needed: release the stage
                 if (lane == 0) mbar_arrive(&empty[s]);
-                // x1_j = (x W_up[j]) * v_j  (Optimization 1)
+                // x1_j = (x W_up[j]) * v_j  (Optimization 1), pre-scaled by 2^8 for the fixed-point split
+                // (a power of two: the fp32 products and sums below are exactly 2^8 times unscaled ones)
                 float x1[NU][B];
 #pragma unroll
                 for (int i = 0; i < NU; ++i)
 #pragma unroll
-                    for (int tk = 0; tk < B; ++tk) x1[i][tk] = (i < n) ? a[i * B + tk] * vj[i][tk] : 0.f;
+                    for (int tk = 0; tk < B; ++tk) x1[i][tk] = (i < n) ? (a[i * B + tk] * vj[i][tk]) * kFixPre : 0.f;
                 // ---- down: y_job[c] = sum_i x1_i W_down[i][c] (fp32, fixed order) -> fixed point ----
 #pragma unroll
                 for (int k = 0; k < CPT; ++k) {
@@ -427,8 +428,17 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                             float yj = 0.f;
 #pragma unroll
                             for (int i = 0; i < NU; ++i) yj = fmaf(x1[i][tk], wf[i][e], yj);
-                            yacc[tk][k][e] += to_fixed(yj);
+                            fix_acc(yhi[tk][k][e], ylo[tk][k][e], yj);
                         }
+                }
+                if (++n_since_renorm == 256) {  // keep the low halves far from int32 overflow
+                    n_since_renorm = 0;
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk)
+#pragma unroll
+                        for (int k = 0; k < CPT; ++k)
+#pragma unroll
+                            for (int e = 0; e < VEC; ++e) fix_renorm(yhi[tk][k][e], ylo[tk][k][e]);
                 }
             }
             if (++s == stages) { s = 0; phase ^= 1u; }
@@ -452,7 +462,8 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                         longlong2 *dst = reinterpret_cast<longlong2 *>(yp + (size_t)tk * d + (size_t)ch * VEC);
 #pragma unroll
                         for (int q = 0; q < VEC / 2; ++q)
-                            dst[q] = make_longlong2(yacc[tk][k][2 * q], yacc[tk][k][2 * q + 1]);
+                            dst[q] = make_longlong2(fix_value(yhi[tk][k][2 * q], ylo[tk][k][2 * q]),
+                                                    fix_value(yhi[tk][k][2 * q + 1], ylo[tk][k][2 * q + 1]));
                     }
                 }
         }
@@ -460,7 +471,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     }
 }
 
-// K3: y[b][d] = (sum_p ypart[p][b][d]) * 2^-kFixShift -- exact integer sum (any order), one
+// K3: y[b][d] = (sum_p ypart[p][b][d]) * 2^-30 -- exact integer sum (any order), one
 // rounding to fp32. A 256-thread block owns 8 consecutive 16-byte columns; its 32 groups of 8 lanes
 // each sum the partials p = g, g+32, ... (one 128-byte line per partial, all loads in flight), then
 // the 32 group sums meet in shared memory. Many small blocks spread the L2 reads over every SM.
@@ -501,7 +512,7 @@ k3_fixed_reduce(const longlong2 *__restrict__ ypart, int p2, int n2, float2 *__r
             sx += sacc[w][c].x;
             sy += sacc[w][c].y;
         }
-        y[f] = make_float2(from_fixed(sx), from_fixed(sy));
+        y[f] = make_float2(fix_to_float(sx), fix_to_float(sy));
     }
     trace_stamp(trace, 1, 2);
 }
@@ -514,7 +525,7 @@ size_t k12_smem_bytes(const PlanData &p, int b, int stages) {
     const size_t desc = (size_t)(3 + nu) * 4 + (size_t)nu * b * 4;
     s += (size_t)(stages + 64) * desc;                       // stage descriptors + UD queue
     s = (s + 15) & ~(size_t)15;
-    s += (size_t)stages * kConsumerWarps * std::max(nr, nu) * b * 4;  // per-stage warp partials
+    s += (size_t)stages * k12_consumer_warps_c(b) * std::max(nr, nu) * b * 4;  // per-stage warp partials
     return (s + 127) & ~(size_t)127;
 }
 
@@ -527,7 +538,7 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
     if (e != cudaSuccess) return e;
     char *w = static_cast<char *>(ws);
-    kern<<<p.g1, kK12Threads, smem, s>>>(
+    kern<<<k12_grid(p, B), k12_threads_c(B), smem, s>>>(
         static_cast<const T *>(x), static_cast<const T *>(Wg), static_cast<const T *>(Wu), static_cast<const T *>(Wd),
         p.d, p.m, stages, t, mode, reinterpret_cast<int32_t *>(w + p.off_idx),
         reinterpret_cast<uint8_t *>(w + p.off_tokmask), reinterpret_cast<float *>(w + p.off_vals),
@@ -540,11 +551,13 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
 template <typename T, int B, int NR>
 static cudaError_t launch_k12_r(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
                                 float t, int mode, float *acts, void *ws, cudaStream_t s) {
-    switch (p.cpt) {
+    switch (k12_cpt(p, B)) {
         case 1: return launch_k12_t<T, B, NR, 1>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
         case 2: return launch_k12_t<T, B, NR, 2>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
-        case 3: return launch_k12_t<T, B, NR, 3>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
-        case 4: return launch_k12_t<T, B, NR, 4>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 3: return B == 1 ? launch_k12_t<T, B, NR, (B == 1 ? 3 : 2)>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s)
+                              : cudaErrorInvalidValue;
+        case 4: return B == 1 ? launch_k12_t<T, B, NR, (B == 1 ? 4 : 2)>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s)
+                              : cudaErrorInvalidValue;
         default: return cudaErrorInvalidValue;
     }
 }
@@ -599,7 +612,7 @@ static cudaError_t launch_ex(const void *func, dim3 grid, dim3 block, size_t sme
 cudaError_t launch_k3(const PlanData &p, int b, void *ws, float *y, cudaStream_t s, bool pdl) {
     char *w = static_cast<char *>(ws);
     const longlong2 *ypart = reinterpret_cast<const longlong2 *>(w + p.off_ypart);
-    int p2 = p.g1;
+    int p2 = k12_grid(p, b);
     int n2 = b * p.d / 2;
     float2 *y2 = reinterpret_cast<float2 *>(y);
     unsigned int *sched = reinterpret_cast<unsigned int *>(w + p.off_sched);
