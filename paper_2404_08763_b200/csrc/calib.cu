@@ -18,7 +18,7 @@
 namespace cats {
 
 constexpr int kCalThreads = 512;
-constexpr int kCalUnroll = 4;
+constexpr int kCalUnroll = 8;
 
 template <typename K> struct KeyTraits;
 template <> struct KeyTraits<uint16_t> {  // bf16
@@ -50,18 +50,26 @@ calib_hist_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint32_t 
     if (threadIdx.x < 4) scount[threadIdx.x] = 0ull;
     __syncthreads();
 
-    uint32_t below = 0, above = 0, nonfin = 0, inwin = 0;
+    // Branch-free counters on the common path (no divergence); only keys inside the window (a small
+    // fraction after the sample pass) take the histogram path. above = seen - below - inwin - nonfin.
+    uint32_t below = 0, nonfin = 0, inwin = 0, seen = 0;
     uint32_t cur_bin = 0xffffffffu, cur_cnt = 0;  // run-length cache against same-bin contention
+    const uint32_t span = hi - lo;
     auto classify = [&](uint32_t key) {
-        if (key >= KT::kInf) { ++nonfin; return; }
-        if (key < lo) { ++below; return; }
-        if (key > hi) { ++above; return; }
-        ++inwin;
-        const uint32_t bin = (key - lo) >> shift;
-        if (bin == cur_bin) { ++cur_cnt; return; }
-        if (cur_cnt) atomicAdd(&sh[cur_bin], cur_cnt);
-        cur_bin = bin;
-        cur_cnt = 1;
+        below += key < lo ? 1u : 0u;
+        nonfin += key >= KT::kInf ? 1u : 0u;
+        const uint32_t rel = key - lo;  // unsigned: wraps for key < lo
+        if (rel <= span) {
+            ++inwin;
+            const uint32_t bin = rel >> shift;
+            if (bin == cur_bin) {
+                ++cur_cnt;
+            } else {
+                if (cur_cnt) atomicAdd(&sh[cur_bin], cur_cnt);
+                cur_bin = bin;
+                cur_cnt = 1;
+            }
+        }
     };
 
     const uint64_t nvec = n / E;
@@ -79,16 +87,22 @@ calib_hist_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint32_t 
         for (int u = 0; u < kCalUnroll; ++u)
 #pragma unroll
             for (int e = 0; e < E; ++e) classify(KT::key(r[u], e));
+        seen += kCalUnroll * E;
     }
     for (; i < nwork; i += gstride) {
         const uint4 r = ldg_stream(v4 + i * step);
 #pragma unroll
         for (int e = 0; e < E; ++e) classify(KT::key(r, e));
+        seen += E;
     }
     // scalar tail (full passes only)
     if (!stride && blockIdx.x == 0) {
-        for (uint64_t j = nvec * E + threadIdx.x; j < n; j += blockDim.x) classify((uint32_t)acts[j] & KT::kMask);
+        for (uint64_t j = nvec * E + threadIdx.x; j < n; j += blockDim.x) {
+            classify((uint32_t)acts[j] & KT::kMask);
+            ++seen;
+        }
     }
+    const uint32_t above = seen - below - inwin - nonfin;
     if (cur_cnt) atomicAdd(&sh[cur_bin], cur_cnt);
 
     // block-reduce the register counters, one global atomic per counter per block
