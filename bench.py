@@ -186,7 +186,8 @@ def workload_config(args, d, m):
             "model_shape": {"d": d, "m": m}, "batch": args.batch, "sparsity": args.sparsity,
             "tp": args.gpus, "storage": "bf16", "accumulate": "f32",
             "l2": f"inputs larger than L2: {args.copies} rotated weight copies per rank",
-            "timing": "CUDA events on the launching stream, max over ranks"}
+            "timing": "CUDA events on the launching stream, max over ranks; steps replayed from a CUDA graph "
+                      "of 8 decode calls (eager launches reported in detail.eager_us_per_step)"}
 
 
 # ---------------------------------------------------------------------------------------- GPU arm
@@ -231,11 +232,38 @@ def main():
     xs = cats_synth.tokens(64 * b, d, torch.bfloat16, seed=1).to(dev).view(64, b, d)
     y = torch.empty((b, d), dtype=torch.float32, device=dev)
 
-    def step(i):
+    def step(i, st=stream):
         W = copies[i % len(copies)]
-        cats.cats_mlp_decode(plan, xs[i % 64], W[0], W[1], W[2], t, y=y, ws=ws, stream=stream)
+        cats.cats_mlp_decode(plan, xs[i % 64], W[0], W[1], W[2], t, y=y, ws=ws, stream=st)
         if world > 1:
             dist.all_reduce(y)
+
+    # CUDA graph of G consecutive steps (the library calls are stream-ordered, allocation- and
+    # sync-free, so they capture as-is); replayed K/G times in the timed region
+    G = 8
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream(dev)
+    cap.wait_stream(stream)
+    with torch.cuda.stream(cap):
+        for i in range(G):  # warm the capture stream
+            step(i, st=cap)
+    stream.wait_stream(cap)
+    torch.cuda.synchronize(dev)
+    with torch.cuda.graph(graph, stream=cap):
+        for i in range(G):
+            step(i, st=cap)
+    torch.cuda.synchronize(dev)
+
+    def make_graph_step(k_total):
+        full = k_total // G * G
+
+        def graph_step(i):  # exactly k_total steps: k_total // G replays + k_total % G eager steps
+            if i < full:
+                if i % G == 0:
+                    graph.replay()
+            else:
+                step(i)
+        return graph_step
 
     def timed(fn, steps, warmup):
         for i in range(warmup):
@@ -258,7 +286,8 @@ def main():
 
     sampler = ClockSampler(local)
     with sampler:
-        ms_step = timed(step, args.steps, max(3, args.warmup))
+        ms_step = timed(make_graph_step(args.steps), args.steps, max(3, args.warmup))
+        ms_eager = timed(step, args.steps, max(3, args.warmup))
     clocks = sampler.summary()
 
     # realized sparsity of this step's token (union over b)
@@ -356,6 +385,7 @@ def main():
             "detail": {
                 "t": t, "nnz_union_per_rank": nnz_local, "nnz_union_total": U, "m_per_rank": ms,
                 "realized_sparsity": round(1 - U / m, 4),
+                "eager_us_per_step": round(ms_eager * 1e3, 3), "graph_steps_per_replay": G,
                 "k12_us": round(k12, 3), "k3_us": round(k3, 3),
                 "effective_bytes_per_step": step_bytes,
                 "effective_GBps": round(step_bytes / (us_step * 1e-6) / 1e9, 1),
