@@ -3,9 +3,9 @@
 
 Workload (BASELINE.json configs[1]): one Mistral-7B MLP layer (d=4096, m=14336), bf16 weights and
 activations, batch 1, 50% sparsity, threshold calibrated on 2048 held-apart synthetic tokens with
-the library's own calibration path. A step = one pass of the whole hot path (K1 gate/SiLU/CATS/
-compaction -> K2 sparse up x v + down -> K3 split-K reduce [-> NCCL all-reduce when N > 1]) for one
-token. N > 1: tensor parallel along m (each rank m/N neurons, same t), "strong" scaling.
+the library's own calibration path. A step = one pass of the whole hot path (one K12 launch: gate
+GEMV, SiLU, CATS threshold, compaction, sparse up x v, down projection, split-K reduction [-> NCCL
+all-reduce when N > 1]) for one token. N > 1: tensor parallel along m (each rank m/N neurons, same t), "strong" scaling.
 
 Timing: W warm-up steps, then exactly K steps between barrier + synchronize, CUDA events on the
 launching stream, max over ranks. L2 defeated by rotating 4 device copies of the weights (1.41 GB
@@ -309,7 +309,6 @@ def main():
         cats.cats_mlp_decode_profiled(plan, xs[i % 64], *copies[i % len(copies)], t, evs[i], y=y, ws=ws)
     torch.cuda.synchronize(dev)
     k12 = statistics.mean(e[0].elapsed_time(e[1]) for e in evs) * 1e3
-    k3 = statistics.mean(e[1].elapsed_time(e[2]) for e in evs) * 1e3
 
     # ---- dense path of the same library (speedup denominator), and cuBLAS dense for context
     def dense_step(i):
@@ -380,13 +379,13 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_ms * 1e3 / b, 3), "unit": UNIT, "h2d_bytes_per_step": b * d * esz,
                     "d2h_bytes_per_step": b * d * 4},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": args.steps,
             "clocks": clocks,
             "detail": {
                 "t": t, "nnz_union_per_rank": nnz_local, "nnz_union_total": U, "m_per_rank": ms,
                 "realized_sparsity": round(1 - U / m, 4),
                 "eager_us_per_step": round(ms_eager * 1e3, 3), "graph_steps_per_replay": G,
-                "k12_us": round(k12, 3), "k3_us": round(k3, 3),
+                "k12_us": round(k12, 3),
                 "effective_bytes_per_step": step_bytes,
                 "effective_GBps": round(step_bytes / (us_step * 1e-6) / 1e9, 1),
                 "frac_of_8TBps": round(step_bytes / (us_step * 1e-6) / 1e9 / NOMINAL_HBM_GBS, 4),

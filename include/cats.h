@@ -166,7 +166,6 @@ typedef struct {
     int rows_per_tile;            /* W_gate rows per GATE job; a UD job carries rows_per_tile/2 neurons */
     int stages;                   /* shared-memory ring depth (one job per stage) */
     size_t smem;                  /* K12 dynamic shared memory bytes (at max_batch) */
-    int k3_grid, k3_threads;      /* K3: exact fixed-point split-K reduction of the CTA partials */
     size_t workspace_bytes;
 } cats_mlp_plan_info_t;
 
@@ -188,9 +187,10 @@ cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, void *ws, siz
 
 /* y[b][d] = CATS_t gated MLP of x[b][d] over this plan's m neurons (under tensor parallelism y
  * is the rank's partial; the caller all-reduces). t >= 0; t = 0 gives dense semantics.
- * Launches K12 (gate GEMV + SiLU + threshold + compaction + sparse up x v + down, one persistent
- * dataflow kernel) then K3 (reduction) on s, with programmatic dependent launch. Deterministic:
- * bit-identical y for identical inputs, whatever the dynamic tile schedule.
+ * ONE kernel launch on s (K12): a persistent dataflow kernel doing the gate GEMV, SiLU, threshold,
+ * compaction, sparse up x v, down projection and the split-K reduction (TMA bulk-reduce of exact
+ * fixed-point partials; the last CTA writes y). Deterministic: bit-identical y for identical
+ * inputs, whatever the dynamic tile schedule.
  * Errors: CATS_E_NULL, CATS_E_ALIGN, CATS_E_BATCH, CATS_E_THRESHOLD, CATS_E_WORKSPACE,
  *         CATS_E_CUDA. */
 cats_status_t cats_mlp_decode(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
@@ -209,10 +209,9 @@ cats_status_t cats_mlp_decode_host(const cats_mlp_plan_t *plan, const void *x_ho
                                    const void *W_gate, const void *W_up, const void *W_down_nm,
                                    float t, float *y_host, void *ws, size_t ws_bytes, cats_stream_t s);
 
-/* Measurement variant of cats_mlp_decode: identical launches, plus events[0..2] (cudaEvent_t,
- * created by the caller with timing enabled) recorded on s before K12, between K12 and K3, and after
- * K3 -- per-kernel device time for the roofline report. The recorded events break the
- * programmatic-dependent-launch overlap, so the sum of the intervals bounds a cats_mlp_decode call. */
+/* Measurement variant of cats_mlp_decode: the identical launch bracketed by events[0] and events[1]
+ * (cudaEvent_t created by the caller with timing enabled; events[2] is recorded right after
+ * events[1]) -- the kernel's device time for the roofline report. */
 cats_status_t cats_mlp_decode_profiled(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
                                        const void *W_up, const void *W_down_nm, float t, float *y,
                                        void *ws, size_t ws_bytes, cats_stream_t s, void *const *events);
@@ -233,8 +232,8 @@ cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const void *ws, 
 /* Diagnostics. When the environment variable CATS_TRACE=1 is set at plan creation, the kernels
  * record %globaltimer stamps (ns) per CTA into a trace area of the workspace:
  * uint64 trace[3][512 CTAs][8 slots] at byte `offset` (bytes = 0 when tracing is off).
- * [0] K12 slots: 0 start, 1 ring primed, 2 jobs done, 3 exit. [1] K3: 0 start, 1 K12 visible,
- * 2 exit. */
+ * [0] K12 slots: 0 start, 1 ring primed, 2 jobs done, 3 exit (after the split-K reduction);
+ * [2] per-CTA producer/consumer statistics (see scripts/trace_decode.py). */
 cats_status_t cats_mlp_trace_info(const cats_mlp_plan_t *plan, size_t *offset, size_t *bytes);
 
 #ifdef __cplusplus

@@ -30,8 +30,7 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int), ("m", ctypes.c_int), ("max_batch", ctypes.c_int), ("w_dtype", ctypes.c_int),
                 ("device", ctypes.c_int), ("num_sms", ctypes.c_int), ("grid", ctypes.c_int),
                 ("threads", ctypes.c_int), ("rows_per_tile", ctypes.c_int), ("stages", ctypes.c_int),
-                ("smem", ctypes.c_size_t), ("k3_grid", ctypes.c_int), ("k3_threads", ctypes.c_int),
-                ("workspace_bytes", ctypes.c_size_t)]
+                ("smem", ctypes.c_size_t), ("workspace_bytes", ctypes.c_size_t)]
 
 
 _lock = threading.Lock()

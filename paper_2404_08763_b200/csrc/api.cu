@@ -340,7 +340,7 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.off_tokmask = off; off = align_up(off + (size_t)m, 256);
         p.off_vals = off;    off = align_up(off + (size_t)m * max_batch * 4, 256);
         p.off_cnt = off;     off = align_up(off + (size_t)((m + 1) / 2) * 4, 256);
-        p.off_ypart = off;   off = align_up(off + (size_t)p.g1 * max_batch * d * 8, 256);  // int64 partials
+        p.off_ypart = off;   off = align_up(off + (size_t)max_batch * d * 8, 256);  // int64 y accumulator
         p.off_xstage = off;  off = align_up(off + (size_t)max_batch * d * esize, 256);
         p.off_ystage = off;  off = align_up(off + (size_t)max_batch * d * 4, 256);
         const char *tr = std::getenv("CATS_TRACE");
@@ -373,8 +373,6 @@ extern "C" cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_ml
     info->rows_per_tile = k12_rows_per_tile(p, b);
     info->stages = k12_stages(p, b);
     info->smem = k12_smem_bytes(p, b, info->stages);
-    info->k3_grid = (p.max_batch * p.d / 2 + 7) / 8;
-    info->k3_threads = kK3Threads;
     info->workspace_bytes = p.ws_bytes;
     return CATS_OK;
 }
@@ -393,6 +391,9 @@ extern "C" cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, vo
     cudaError_t e = cudaSetDevice(plan->p.device);
     if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_sched, 0, 64,
                                               static_cast<cudaStream_t>(s));
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_ypart, 0, (size_t)plan->p.max_batch * plan->p.d * 8,
+                            static_cast<cudaStream_t>(s));
     return cuda_status(e);
 }
 
@@ -412,8 +413,7 @@ cats_status_t validate_common(const cats_mlp_plan_t *plan, const void *x, int b,
 cats_status_t run_mlp(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd, float t,
                       int dense, float *y, void *ws, cudaStream_t st) {
     cudaError_t e = cudaSetDevice(p.device);
-    if (e == cudaSuccess) e = launch_k12(p, x, b, Wg, Wu, Wd, t, dense ? kModeDense : kModeCats, nullptr, ws, st);
-    if (e == cudaSuccess) e = launch_k3(p, b, ws, y, st, /*pdl=*/true);
+    if (e == cudaSuccess) e = launch_k12(p, x, b, Wg, Wu, Wd, t, dense ? kModeDense : kModeCats, nullptr, y, ws, st);
     return cuda_status(e);
 }
 
@@ -442,10 +442,9 @@ extern "C" cats_status_t cats_mlp_decode_profiled(const cats_mlp_plan_t *plan, c
     for (int i = 0; i < 3; ++i) ev[i] = static_cast<cudaEvent_t>(events[i]);
     cudaError_t e = cudaSetDevice(p.device);
     if (e == cudaSuccess) e = cudaEventRecord(ev[0], st);
-    if (e == cudaSuccess) e = launch_k12(p, x, b, W_gate, W_up, W_down_nm, t, kModeCats, nullptr, ws, st);
+    if (e == cudaSuccess) e = launch_k12(p, x, b, W_gate, W_up, W_down_nm, t, kModeCats, nullptr, y, ws, st);
     if (e == cudaSuccess) e = cudaEventRecord(ev[1], st);
-    if (e == cudaSuccess) e = launch_k3(p, b, ws, y, st, /*pdl=*/true);
-    if (e == cudaSuccess) e = cudaEventRecord(ev[2], st);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[2], st);  // (single kernel: the reduction is inside K12)
     return cuda_status(e);
 }
 
@@ -488,9 +487,8 @@ extern "C" cats_status_t cats_mlp_gate_act(const cats_mlp_plan_t *plan, const vo
     if (!aligned16(x) || !aligned16(W_gate) || !aligned16(ws)) return CATS_E_ALIGN;
     cudaError_t e = cudaSetDevice(plan->p.device);
     if (e == cudaSuccess)
-        e = launch_k12(plan->p, x, b, W_gate, W_gate, W_gate, 0.0f, kModeGateOnly, acts, ws, static_cast<cudaStream_t>(s));
-    if (e == cudaSuccess)  // re-arm K1's tile scheduler (no K2 follows)
-        e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_sched, 0, 8, static_cast<cudaStream_t>(s));
+        e = launch_k12(plan->p, x, b, W_gate, W_gate, W_gate, 0.0f, kModeGateOnly, acts, nullptr, ws,
+                       static_cast<cudaStream_t>(s));
     return cuda_status(e);
 }
 

@@ -18,7 +18,6 @@ constexpr int k12_consumer_warps_c(int b) { return b == 1 ? 8 : 16; }
 constexpr int k12_ctas_per_sm_c(int b) { return b == 1 ? 2 : 1; }
 constexpr int k12_threads_c(int b) { return k12_consumer_warps_c(b) * 32 + 32; }  // + 1 producer warp
 constexpr size_t k12_smem_budget_c(int b) { return b == 1 ? 112 * 1024 : 224 * 1024; }
-constexpr int kK3Threads = 256;
 constexpr size_t kSmemBudget = 224 * 1024;  // dynamic shared memory per CTA, one CTA per SM
 constexpr int kMaxCPT = 4;            // 16-byte chunks of a row owned per consumer (d <= 8192 bf16)
 constexpr int kMaxStages = 8;
@@ -67,9 +66,9 @@ inline int k12_stages(const PlanData &p, int b) {
 cudaError_t ensure_smem_attr(const void *func, size_t smem);
 
 // launchers: return cudaError_t of the launch
+// K12 = the whole decode (gate ... down projection and the split-K reduction; y written by the last CTA)
 cudaError_t launch_k12(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd,
-                       float t, int mode, float *acts, void *ws, cudaStream_t s);
-cudaError_t launch_k3(const PlanData &p, int b, void *ws, float *y, cudaStream_t s, bool pdl);
+                       float t, int mode, float *acts, float *y, void *ws, cudaStream_t s);
 
 cudaError_t launch_calib_hist(const void *acts, uint64_t n, cats_dtype_t dt, const cats_calib_window_t &w,
                               uint64_t *hist, uint64_t *counts, cudaStream_t s);

@@ -1,4 +1,4 @@
-// mlp_fused.cu -- the CATS-MLP decode as ONE persistent dataflow kernel (K12) + a tiny reduce (K3).
+// mlp_fused.cu -- the CATS-MLP decode as ONE persistent dataflow kernel (K12).
 //
 // Paper: Custom GPU Kernel "MLP using CATS":
 //     v <- SiLU(x W_gate); Mask <- |v| >= t; x1 <- (x W_up[Mask]) * v[Mask]; y <- x1 W_down[Mask]
@@ -30,7 +30,8 @@
 //    fix_acc) and added to the thread's integer accumulator. Integer
 //    addition is associative, so y does not depend on which CTA took which tile or in which order:
 //    bit-reproducible. (Replaces the paper's fp16 tl.atomic_add into Y.)
-//  * K3 sums the per-CTA integer partials (exact) and converts to fp32 once.
+//  * Split-K reduction: each CTA bulk-reduces (TMA cp.reduce.async.bulk .add.u64) its integer
+//    partial into one global accumulator; the last CTA converts it to fp32 once and writes y.
 //
 // Workspace outputs for introspection: tile tau's cnt[tau] active neurons are written ascending at
 // positions [tau*NR, tau*NR + cnt[tau]) of idx / tokmask / vals (v in fp32, 0 where |v| < t).
@@ -64,7 +65,8 @@ __global__ void __launch_bounds__(k12_threads_c(B), k12_ctas_per_sm_c(B))
 k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restrict__ Wu, const T *__restrict__ Wd,
              int d, int m, int stages, float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask,
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
-             long long *__restrict__ ypart, unsigned int *__restrict__ sched, unsigned long long *__restrict__ trace) {
+             unsigned long long *__restrict__ yacc, float *__restrict__ y, unsigned int *__restrict__ sched,
+             unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
     constexpr int NW = k12_consumer_warps_c(B);
@@ -92,7 +94,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     float *red = reinterpret_cast<float *>(queue + QCAP);                                 // [stages][NW][NPMAX]
 
     trace_stamp(trace, 0, 0);
-    pdl_launch_dependents();  // K3 may be scheduled early; it waits for this grid to complete
+    pdl_launch_dependents();  // a PDL successor may be scheduled once every CTA has started
 
     if (tid == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -450,71 +452,66 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             trace_put(trace, 2, 5, (unsigned long long)n_ud);
         }
 
-        // ---- this CTA's exact integer partial of y ----
+        // ---- split-K reduction through the TMA bulk-reduce engine ----
+        // The CTA's exact int64 partial is staged in shared memory (the ring is idle after END)
+        // and added into the global accumulator yacc[b][d] with cp.reduce.async.bulk .add.u64
+        // (integer adds performed at L2, any order -> deterministic). The last CTA to finish converts
+        // yacc to fp32 once, writes y, and re-zeroes yacc and the tile scheduler for the next call.
+        __shared__ unsigned int s_last;
         if (mode != kModeGateOnly) {
-            long long *yp = ypart + (size_t)blockIdx.x * B * d;
+            unsigned long long *sbuf = reinterpret_cast<unsigned long long *>(ring);
+            const int tpc = min(B, (int)(((size_t)stages * stage_bytes) / ((size_t)d * 8)));  // tokens per chunk
+            for (int t0 = 0; t0 < B; t0 += tpc) {
+                const int tn = min(tpc, B - t0);
 #pragma unroll
-            for (int tk = 0; tk < B; ++tk)
+                for (int tk = 0; tk < B; ++tk) {
+                    if (tk < t0 || tk >= t0 + tn) continue;
 #pragma unroll
-                for (int k = 0; k < CPT; ++k) {
-                    const int ch = tid + k * NC;
-                    if (ch < nch) {
-                        longlong2 *dst = reinterpret_cast<longlong2 *>(yp + (size_t)tk * d + (size_t)ch * VEC);
+                    for (int k = 0; k < CPT; ++k) {
+                        const int ch = tid + k * NC;
+                        if (ch < nch) {
+                            ulonglong2 *dst =
+                                reinterpret_cast<ulonglong2 *>(sbuf + (size_t)(tk - t0) * d + (size_t)ch * VEC);
 #pragma unroll
-                        for (int q = 0; q < VEC / 2; ++q)
-                            dst[q] = make_longlong2(fix_value(yhi[tk][k][2 * q], ylo[tk][k][2 * q]),
-                                                    fix_value(yhi[tk][k][2 * q + 1], ylo[tk][k][2 * q + 1]));
+                            for (int q = 0; q < VEC / 2; ++q)
+                                dst[q] = make_ulonglong2(
+                                    (unsigned long long)fix_value(yhi[tk][k][2 * q], ylo[tk][k][2 * q]),
+                                    (unsigned long long)fix_value(yhi[tk][k][2 * q + 1], ylo[tk][k][2 * q + 1]));
+                        }
                     }
                 }
+                fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk engine
+                consumer_barrier<NC>();
+                if (tid == 0) {
+                    bulk_reduce_add_u64(yacc + (size_t)t0 * d, sbuf, (uint32_t)((size_t)tn * d * 8));
+                    bulk_commit_and_wait_all();
+                }
+                consumer_barrier<NC>();  // sbuf reusable
+            }
+            if (tid == 0) {
+                fence_proxy_async_global();
+                __threadfence();
+            }
+        }
+        consumer_barrier<NC>();
+        if (tid == 0) s_last = (atomicAdd(&sched[1], 1u) == gridDim.x - 1) ? 1u : 0u;
+        consumer_barrier<NC>();
+        if (s_last) {
+            __threadfence();
+            if (mode != kModeGateOnly) {
+                for (int c = tid; c < B * d / 2; c += NC) {
+                    const longlong2 v = __ldcg(reinterpret_cast<const longlong2 *>(yacc) + c);
+                    reinterpret_cast<float2 *>(y)[c] = make_float2(fix_to_float(v.x), fix_to_float(v.y));
+                    reinterpret_cast<longlong2 *>(yacc)[c] = make_longlong2(0, 0);
+                }
+            }
+            if (tid == 0) {
+                sched[0] = 0u;
+                sched[1] = 0u;
+            }
         }
         trace_stamp(trace, 0, 3);
     }
-}
-
-// K3: y[b][d] = (sum_p ypart[p][b][d]) * 2^-30 -- exact integer sum (any order), one
-// rounding to fp32. A 256-thread block owns 8 consecutive 16-byte columns; its 32 groups of 8 lanes
-// each sum the partials p = g, g+32, ... (one 128-byte line per partial, all loads in flight), then
-// the 32 group sums meet in shared memory. Many small blocks spread the L2 reads over every SM.
-// Re-arms K12's tile scheduler (K12 has completed).
-__global__ void __launch_bounds__(kK3Threads)
-k3_fixed_reduce(const longlong2 *__restrict__ ypart, int p2, int n2, float2 *__restrict__ y,
-                unsigned int *__restrict__ sched, unsigned long long *__restrict__ trace) {
-    constexpr int kCols = 8, kGroups = kK3Threads / kCols, kPerLane = 12;
-    __shared__ longlong2 sacc[kGroups][kCols];
-    trace_stamp(trace, 1, 0);
-    pdl_wait_primary();
-    trace_stamp(trace, 1, 1);
-    if (blockIdx.x == 0 && threadIdx.x == 0) sched[0] = 0u;
-    const int c = threadIdx.x % kCols, g = threadIdx.x / kCols;
-    const int f = blockIdx.x * kCols + c;
-    long long ax = 0, ay = 0;
-    if (f < n2) {
-        for (int base = g; base < p2; base += kGroups * kPerLane) {
-            longlong2 v[kPerLane];
-#pragma unroll
-            for (int i = 0; i < kPerLane; ++i) {
-                const int pp = base + kGroups * i;
-                v[i] = pp < p2 ? ypart[(size_t)pp * n2 + f] : make_longlong2(0, 0);
-            }
-#pragma unroll
-            for (int i = 0; i < kPerLane; ++i) {
-                ax += v[i].x;
-                ay += v[i].y;
-            }
-        }
-    }
-    sacc[g][c] = make_longlong2(ax, ay);
-    __syncthreads();
-    if (threadIdx.x < kCols && f < n2) {
-        long long sx = 0, sy = 0;
-#pragma unroll 8
-        for (int w = 0; w < kGroups; ++w) {
-            sx += sacc[w][c].x;
-            sy += sacc[w][c].y;
-        }
-        y[f] = make_float2(fix_to_float(sx), fix_to_float(sy));
-    }
-    trace_stamp(trace, 1, 2);
 }
 
 size_t k12_smem_bytes(const PlanData &p, int b, int stages) {
@@ -531,7 +528,7 @@ size_t k12_smem_bytes(const PlanData &p, int b, int stages) {
 
 template <typename T, int B, int NR, int CPT>
 static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
-                                float t, int mode, float *acts, void *ws, cudaStream_t s) {
+                                float t, int mode, float *acts, float *y, void *ws, cudaStream_t s) {
     auto kern = k12_cats_mlp<T, B, NR, CPT>;
     const int stages = k12_stages(p, B);
     const size_t smem = k12_smem_bytes(p, B, stages);
@@ -542,7 +539,7 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
         static_cast<const T *>(x), static_cast<const T *>(Wg), static_cast<const T *>(Wu), static_cast<const T *>(Wd),
         p.d, p.m, stages, t, mode, reinterpret_cast<int32_t *>(w + p.off_idx),
         reinterpret_cast<uint8_t *>(w + p.off_tokmask), reinterpret_cast<float *>(w + p.off_vals),
-        reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<long long *>(w + p.off_ypart),
+        reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<unsigned long long *>(w + p.off_ypart), y,
         reinterpret_cast<unsigned int *>(w + p.off_sched),
         p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
     return cudaGetLastError();
@@ -550,13 +547,13 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
 
 template <typename T, int B, int NR>
 static cudaError_t launch_k12_r(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
-                                float t, int mode, float *acts, void *ws, cudaStream_t s) {
+                                float t, int mode, float *acts, float *y, void *ws, cudaStream_t s) {
     switch (k12_cpt(p, B)) {
-        case 1: return launch_k12_t<T, B, NR, 1>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
-        case 2: return launch_k12_t<T, B, NR, 2>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
-        case 3: return B == 1 ? launch_k12_t<T, B, NR, (B == 1 ? 3 : 2)>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s)
+        case 1: return launch_k12_t<T, B, NR, 1>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 2: return launch_k12_t<T, B, NR, 2>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 3: return B == 1 ? launch_k12_t<T, B, NR, (B == 1 ? 3 : 2)>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s)
                               : cudaErrorInvalidValue;
-        case 4: return B == 1 ? launch_k12_t<T, B, NR, (B == 1 ? 4 : 2)>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s)
+        case 4: return B == 1 ? launch_k12_t<T, B, NR, (B == 1 ? 4 : 2)>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s)
                               : cudaErrorInvalidValue;
         default: return cudaErrorInvalidValue;
     }
@@ -564,63 +561,34 @@ static cudaError_t launch_k12_r(const PlanData &p, const void *x, const void *Wg
 
 template <typename T, int B>
 static cudaError_t launch_k12_b(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
-                                float t, int mode, float *acts, void *ws, cudaStream_t s) {
+                                float t, int mode, float *acts, float *y, void *ws, cudaStream_t s) {
     switch (k12_rows_per_tile(p, B)) {
-        case 4: return launch_k12_r<T, B, 4>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
-        case 2: return launch_k12_r<T, B, 2>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 4: return launch_k12_r<T, B, 4>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 2: return launch_k12_r<T, B, 2>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
 template <typename T>
 static cudaError_t launch_k12_dt(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu,
-                                 const void *Wd, float t, int mode, float *acts, void *ws, cudaStream_t s) {
+                                 const void *Wd, float t, int mode, float *acts, float *y, void *ws, cudaStream_t s) {
     switch (b) {
-        case 1: return launch_k12_b<T, 1>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
-        case 2: return launch_k12_b<T, 2>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
-        case 3: return launch_k12_b<T, 3>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
-        case 4: return launch_k12_b<T, 4>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
-        case 5: return launch_k12_b<T, 5>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
-        case 6: return launch_k12_b<T, 6>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
-        case 7: return launch_k12_b<T, 7>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
-        case 8: return launch_k12_b<T, 8>(p, x, Wg, Wu, Wd, t, mode, acts, ws, s);
+        case 1: return launch_k12_b<T, 1>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 2: return launch_k12_b<T, 2>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 3: return launch_k12_b<T, 3>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 4: return launch_k12_b<T, 4>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 5: return launch_k12_b<T, 5>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 6: return launch_k12_b<T, 6>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 7: return launch_k12_b<T, 7>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 8: return launch_k12_b<T, 8>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t launch_k12(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd,
-                       float t, int mode, float *acts, void *ws, cudaStream_t s) {
-    if (p.dt == CATS_BF16) return launch_k12_dt<bf16_bits>(p, x, b, Wg, Wu, Wd, t, mode, acts, ws, s);
-    return launch_k12_dt<float>(p, x, b, Wg, Wu, Wd, t, mode, acts, ws, s);
-}
-
-static cudaError_t launch_ex(const void *func, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
-                             void **args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelExC(&cfg, func, args);
-}
-
-cudaError_t launch_k3(const PlanData &p, int b, void *ws, float *y, cudaStream_t s, bool pdl) {
-    char *w = static_cast<char *>(ws);
-    const longlong2 *ypart = reinterpret_cast<const longlong2 *>(w + p.off_ypart);
-    int p2 = k12_grid(p, b);
-    int n2 = b * p.d / 2;
-    float2 *y2 = reinterpret_cast<float2 *>(y);
-    unsigned int *sched = reinterpret_cast<unsigned int *>(w + p.off_sched);
-    unsigned long long *trace = p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr;
-    const int grid = (n2 + 7) / 8;
-    void *args[] = {&ypart, &p2, &n2, &y2, &sched, &trace};
-    return launch_ex(reinterpret_cast<const void *>(k3_fixed_reduce), dim3(grid), dim3(kK3Threads), 0, s, pdl,
-                     args);
+                       float t, int mode, float *acts, float *y, void *ws, cudaStream_t s) {
+    if (p.dt == CATS_BF16) return launch_k12_dt<bf16_bits>(p, x, b, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+    return launch_k12_dt<float>(p, x, b, Wg, Wu, Wd, t, mode, acts, y, ws, s);
 }
 
 }  // namespace cats
