@@ -120,7 +120,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         int q_head = 0, q_tail = 0;  // pending UD jobs
         int gates_inflight = 0;      // GATE jobs issued, not yet retired
         bool ended = false;
-        unsigned long long p_wait = 0, p_busy = 0, p_issue = 0;  // diagnostics (CATS_TRACE)
+        unsigned long long p_wait = 0, p_busy = 0, p_issue = 0, t_last_gate = 0;  // diagnostics (CATS_TRACE)
 
         // issue job `prod` into its stage; returns false if nothing can be issued yet
         auto issue_job = [&]() -> bool {
@@ -157,6 +157,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                         bulk_g2s(dst, Wg + (size_t)r0 * d, (uint32_t)nr * row_bytes, &full[s], policy);
                     }
                     ++gates_inflight;
+                    if (trace) t_last_gate = gtimer();
                 } else if (gates_inflight == 0) {  // no tiles left and no GATE job can create UD work
                     if (lane == 0) {
                         D.type = kJobEnd;
@@ -275,6 +276,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             trace_put(trace, 2, 1, p_busy);
             trace_put(trace, 2, 2, (unsigned long long)retire);
             trace_put(trace, 2, 6, p_issue);
+            trace_put(trace, 2, 7, t_last_gate);
         }
     } else {
         // ===================================== CONSUMER WARPS ====================================

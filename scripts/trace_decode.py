@@ -22,8 +22,11 @@ ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--k", type=float, default=0.5)
 ap.add_argument("--dense", action="store_true")
 ap.add_argument("--json")
+ap.add_argument("--m", type=int, default=0, help="override m (e.g. a TP shard)")
 a = ap.parse_args()
 d, m = cats_synth.MODELS[a.model]
+if a.m:
+    m = a.m
 dev = torch.device("cuda:0")
 W = [w.to(dev) for w in cats_synth.mlp_weights(d, m, torch.bfloat16)]
 copies = [W] + [[w.clone() for w in W] for _ in range(3)]
@@ -73,5 +76,12 @@ st = tr[2, :g, :7].astype(np.float64)
 print("K12 per-CTA stats (avg/min/max):")
 for i, nm in enumerate(["producer wait ns", "producer busy ns", "jobs retired", "consumer wait ns", "gate jobs", "ud jobs", "producer issue ns"]):
     print(f"   {nm:18s} {st[:, i].mean():10.1f} {st[:, i].min():10.1f} {st[:, i].max():10.1f}")
+lg = (tr[2, :g, 7] - t0) / 1e3
+jd = (tr[0, :g, 2] - t0) / 1e3
+ok = tr[2, :g, 7] > 0
+print("last GATE issue (us): p10/50/90/max", np.percentile(lg[ok], [10, 50, 90, 100]).round(2))
+print("jobs_done - last GATE issue (us): p10/50/90/max", np.percentile((jd - lg)[ok], [10, 50, 90, 100]).round(2))
+corr = np.corrcoef(st[:, 2], jd)[0, 1]
+print("corr(jobs retired, jobs_done time)", round(float(corr), 3))
 if a.json:
     json.dump(rep, open(a.json, "w"), indent=1)
