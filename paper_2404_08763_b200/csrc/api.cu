@@ -343,8 +343,21 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.off_ypart = off;   off = align_up(off + (size_t)max_batch * d * 8, 256);  // int64 y accumulator
         p.off_xstage = off;  off = align_up(off + (size_t)max_batch * d * esize, 256);
         p.off_ystage = off;  off = align_up(off + (size_t)max_batch * d * 4, 256);
+        // split path (b >= 2): x1 per compact position and the KB range partials
+        const char *sm = std::getenv("CATS_SPLIT_MIN_B");
+        p.split_min_b = sm ? std::max(2, std::atoi(sm)) : 2;
+        size_t part_bytes = 0, x1_bytes = 0;
+        for (int b = 2; b <= max_batch; ++b) {
+            if (!split_supported(p, b)) continue;
+            part_bytes = std::max(part_bytes, (size_t)split_ranges(p, b) * b * d * 4);
+            x1_bytes = std::max(x1_bytes, (size_t)k12_ntiles(p, b) * k12_rows_per_tile(p, b) * b * 4);
+        }
+        p.off_x1 = off;      off = align_up(off + x1_bytes, 256);
+        p.off_part = off;    off = align_up(off + part_bytes, 256);
         const char *tr = std::getenv("CATS_TRACE");
         p.trace = tr && tr[0] == '1';
+        const char *lt = std::getenv("CATS_LAZY_TAIL");
+        p.lazy_tail = lt ? std::max(0, std::atoi(lt)) : 1;
         p.off_trace = off;
         p.trace_bytes = p.trace ? (size_t)kTraceKernels * kTraceCtas * kTraceSlots * 8 : 0;
         off = align_up(off + p.trace_bytes, 256);
@@ -410,10 +423,19 @@ cats_status_t validate_common(const cats_mlp_plan_t *plan, const void *x, int b,
     return CATS_OK;
 }
 
+// b = 1 (or a shape the split path does not take): K12, one kernel. b >= split_min_b: KA + KB.
+cudaError_t launch_mlp(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd,
+                       float t, int mode, float *y, void *ws, cudaStream_t st, cudaEvent_t ev_mid) {
+    if (b >= p.split_min_b && split_supported(p, b)) return launch_split(p, x, b, Wg, Wu, Wd, t, mode, y, ws, st, ev_mid);
+    cudaError_t e = launch_k12(p, x, b, Wg, Wu, Wd, t, mode, nullptr, y, ws, st);
+    if (e == cudaSuccess && ev_mid) e = cudaEventRecord(ev_mid, st);
+    return e;
+}
+
 cats_status_t run_mlp(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd, float t,
                       int dense, float *y, void *ws, cudaStream_t st) {
     cudaError_t e = cudaSetDevice(p.device);
-    if (e == cudaSuccess) e = launch_k12(p, x, b, Wg, Wu, Wd, t, dense ? kModeDense : kModeCats, nullptr, y, ws, st);
+    if (e == cudaSuccess) e = launch_mlp(p, x, b, Wg, Wu, Wd, t, dense ? kModeDense : kModeCats, y, ws, st, nullptr);
     return cuda_status(e);
 }
 
@@ -442,9 +464,9 @@ extern "C" cats_status_t cats_mlp_decode_profiled(const cats_mlp_plan_t *plan, c
     for (int i = 0; i < 3; ++i) ev[i] = static_cast<cudaEvent_t>(events[i]);
     cudaError_t e = cudaSetDevice(p.device);
     if (e == cudaSuccess) e = cudaEventRecord(ev[0], st);
-    if (e == cudaSuccess) e = launch_k12(p, x, b, W_gate, W_up, W_down_nm, t, kModeCats, nullptr, y, ws, st);
-    if (e == cudaSuccess) e = cudaEventRecord(ev[1], st);
-    if (e == cudaSuccess) e = cudaEventRecord(ev[2], st);  // (single kernel: the reduction is inside K12)
+    // K12: ev[1] right after the kernel (= ev[2]); split path: ev[1] between KA and KB
+    if (e == cudaSuccess) e = launch_mlp(p, x, b, W_gate, W_up, W_down_nm, t, kModeCats, y, ws, st, ev[1]);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[2], st);
     return cuda_status(e);
 }
 

@@ -112,6 +112,14 @@ __device__ __forceinline__ void bulk_commit_and_wait_all() {
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait_primary() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+template <int NTHREADS>
+__device__ __forceinline__ void consumer_barrier() {  // named barrier 1: the consumer threads only
+    asm volatile("bar.sync 1, %0;" ::"n"(NTHREADS) : "memory");
+}
+
 // ---- diagnostics: per-CTA %globaltimer stamps into the workspace trace area (null = off) ----
 constexpr int kTraceCtas = 512, kTraceSlots = 8, kTraceKernels = 3;
 __device__ __forceinline__ void trace_stamp(unsigned long long *tr, int kernel, int slot) {

@@ -38,6 +38,9 @@ struct PlanData {
     // workspace layout (byte offsets)
     size_t off_sched, off_idx, off_tokmask, off_vals, off_cnt, off_ypart, off_xstage, off_ystage, ws_bytes;
     bool trace;         // CATS_TRACE=1 at plan creation: kernels stamp %globaltimer into the workspace
+    int lazy_tail;      // K12 stops reserving tile ids for the last lazy_tail * grid tiles (CATS_LAZY_TAIL)
+    int split_min_b;    // batches b >= split_min_b run the split path KA + KB (CATS_SPLIT_MIN_B)
+    size_t off_x1, off_part;  // split path: x1 per compact position [m][max_b]; KB partials [R][max_b][d]
     size_t off_trace, trace_bytes;
 };
 
@@ -62,6 +65,47 @@ inline int k12_stages(const PlanData &p, int b) {
     return (int)std::min<size_t>((k12_smem_budget_c(b) - extra) / stage, kMaxStages);
 }
 
+// ---- split path for b >= 2 (mlp_split.cu): KA = gate + up (dynamic tiles), KB = down (static balanced
+// ranges of the compact active list x column parts, fixed-order two-phase reduction) ----
+constexpr int kSplitAWarps = 16;                         // KA consumer warps (both groups)
+constexpr int kSplitAGroups = 2;                         // KA job streams per CTA (one producer warp each)
+constexpr int kSplitAThreads = (kSplitAWarps + kSplitAGroups) * 32;
+constexpr int kSplitBMaxThreads = 672;                   // KB: <= 20 consumer warps + 1 producer warp
+constexpr int kSplitFifo = 64;                           // KA active-neuron FIFO (power of two)
+
+template <int NR, int B>
+struct SplitDesc {   // one KA ring stage: GATE(tile) or UP(<= NR active neurons)
+    int type, tile, n;
+    int id[NR];      // UP: neuron ids
+    int pos[NR];     // UP: compact positions (tile * NR + rank)
+    float v[NR][B];  // UP: v = SiLU(u), 0 for tokens where |v| < t
+};
+template <int B>
+struct SplitFifoEntry {  // one active neuron waiting for its UP job
+    int id, pos;
+    float v[B];
+};
+
+inline int split_q(int b) { return b <= 4 ? 1 : 2; }  // KB column parts (bounds y registers per thread)
+inline int split_ept(const PlanData &p, int b) { return p.esize == 4 ? 4 : (b <= 4 ? 8 : 4); }  // KB columns/thread
+inline int split_part_cols(const PlanData &p, int b) { return p.d / split_q(b); }
+inline int split_kb_consumers(const PlanData &p, int b) {
+    const int c = (split_part_cols(p, b) + split_ept(p, b) - 1) / split_ept(p, b);
+    return (c + 31) / 32 * 32;
+}
+inline int split_ranges(const PlanData &p, int b) {  // R: static ranges of the active list
+    return std::max(1, std::min(p.num_sms / split_q(b), p.m / 8));
+}
+inline int split_kb_grid(const PlanData &p, int b) { return split_ranges(p, b) * split_q(b); }
+inline int split_ka_grid(const PlanData &p, int b) {
+    return std::max(1, std::min(p.num_sms, (k12_ntiles(p, b) + kSplitAGroups - 1) / kSplitAGroups));
+}
+size_t split_ka_smem(const PlanData &p, int b, int stages);
+size_t split_kb_smem(const PlanData &p, int b, int stages);
+int split_ka_stages(const PlanData &p, int b);
+int split_kb_stages(const PlanData &p, int b);
+bool split_supported(const PlanData &p, int b);
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel / size (thread-safe)
 cudaError_t ensure_smem_attr(const void *func, size_t smem);
 
@@ -69,6 +113,10 @@ cudaError_t ensure_smem_attr(const void *func, size_t smem);
 // K12 = the whole decode (gate ... down projection and the split-K reduction; y written by the last CTA)
 cudaError_t launch_k12(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd,
                        float t, int mode, float *acts, float *y, void *ws, cudaStream_t s);
+
+// split path (b >= 2): KA then KB, both PDL launches; ev (optional) = event recorded between them
+cudaError_t launch_split(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd,
+                         float t, int mode, float *y, void *ws, cudaStream_t s, cudaEvent_t ev_mid);
 
 cudaError_t launch_calib_hist(const void *acts, uint64_t n, cats_dtype_t dt, const cats_calib_window_t &w,
                               uint64_t *hist, uint64_t *counts, cudaStream_t s);

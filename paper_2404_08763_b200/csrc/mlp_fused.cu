@@ -43,13 +43,6 @@ namespace cats {
 enum : int { kJobEnd = 0, kJobGate = 1, kJobUD = 2 };
 
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-template <int NTHREADS>
-__device__ __forceinline__ void consumer_barrier() {  // named barrier 1: the consumer threads only
-    asm volatile("bar.sync 1, %0;" ::"n"(NTHREADS) : "memory");
-}
 
 template <int NU, int B>
 struct JobDesc {
@@ -60,13 +53,24 @@ struct JobDesc {
     float v[NU][B];  // UD: v = SiLU(u) per token, 0 where the token's |v| < t
 };
 
+constexpr unsigned int kNoTile = 0xffffffffu;
+
+// if (pred) t = atomicAdd(sched, 1) without a select on the result: the destination is written by a
+// predicated ATOM, so the warp only waits for it where t is next read.
+__device__ __forceinline__ void claim_tile_async(unsigned int &t, unsigned int *sched, bool pred) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p atom.global.add.u32 %0, [%1], 1;\n\t}"
+                 : "+r"(t)
+                 : "l"(sched), "r"((unsigned)pred)
+                 : "memory");
+}
+
 template <typename T, int B, int NR, int CPT>
 __global__ void __launch_bounds__(k12_threads_c(B), k12_ctas_per_sm_c(B))
 k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restrict__ Wu, const T *__restrict__ Wd,
              int d, int m, int stages, float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask,
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
              unsigned long long *__restrict__ yacc, float *__restrict__ y, unsigned int *__restrict__ sched,
-             unsigned long long *__restrict__ trace) {
+             int lazy_tail, unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
     constexpr int NW = k12_consumer_warps_c(B);
@@ -110,10 +114,14 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         const bool dense = mode == kModeDense;
         const bool gate_only = mode == kModeGateOnly;
         const uint64_t policy = l2_evict_first_policy();
-        // tile ids, software-pipelined two deep (lane 0): t_next is resolved, t_pend is an atomic in
-        // flight. A GATE issue uses t_next, then moves t_pend -> t_next (its round trip overlapped
-        // one full GATE interval) and starts a new atomic. No select ever reads the newest atomic.
-        unsigned int t_next = 0, t_pend = 0;
+        // Tile claims (lane 0). While many tiles remain, the next GATE tile is reserved one issue ahead
+        // (t_res: a predicated atomic whose round trip overlaps the jobs in between; nothing reads
+        // it until the next GATE issue). For the last `lazy_tail` tiles no CTA reserves: a tile is
+        // claimed when a stage is free to stream it, so no CTA sits on unstarted work while others
+        // drain (balanced tail), and small layers spread over all CTAs.
+        unsigned int t_res = kNoTile;  // raw counter value; tile id = dyn_base + counter
+        const int batch = max(1, min(stages, ntiles / (int)gridDim.x));  // static first tiles per CTA
+        const unsigned int dyn_base = gridDim.x * (unsigned)batch;        // first dynamically claimed tile
         int prod = 0;                // jobs issued; job j lives in stage j % stages
         int ps = 0;                  // = prod % stages
         int retire = 0;              // jobs retired (consumed and post-processed), in order
@@ -143,13 +151,15 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 }
                 ++q_head;
             } else {
-                const unsigned int tile = __shfl_sync(0xffffffffu, t_next, 0);
+                unsigned int tile = t_res;
+                if (lane == 0 && tile == kNoTile) tile = atomicAdd(&sched[0], 1u);  // claim now
+                tile = __shfl_sync(0xffffffffu, tile, 0) + dyn_base;
                 if (tile < (unsigned)ntiles) {  // GATE job: a new tile of W_gate rows
                     const int r0 = (int)tile * NR;
                     const int nr = min(NR, m - r0);
                     if (lane == 0) {
-                        t_next = t_pend;
-                        t_pend = atomicAdd(&sched[0], 1u);
+                        t_res = kNoTile;
+                        claim_tile_async(t_res, sched, tile + (unsigned)lazy_tail < (unsigned)ntiles);
                         D.type = kJobGate;
                         D.tile = (int)tile;
                         D.n = nr;
@@ -158,15 +168,16 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     }
                     ++gates_inflight;
                     if (trace) t_last_gate = gtimer();
-                } else if (gates_inflight == 0) {  // no tiles left and no GATE job can create UD work
+                } else {
+                    if (lane == 0) t_res = tile - dyn_base;  // past the end: keep it, no further claims
+                    if (gates_inflight != 0) return false;  // an in-flight GATE job may add UD work
+                    // no tiles left and nothing in flight can create UD work: end the ring
                     if (lane == 0) {
                         D.type = kJobEnd;
                         D.n = 0;
                         mbar_arrive_expect_tx(&full[s], 0u);
                     }
                     ended = true;
-                } else {
-                    return false;  // an in-flight GATE job will produce UD work: fill later
                 }
             }
             __syncwarp();
@@ -176,15 +187,13 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         };
 
         if (lane == 0) {
-            // prime the ring with a batch of consecutive GATE tiles (one atomic), at most the
-            // CTA's fair share so small layers still spread over all CTAs
-            const int batch = max(1, min(stages, ntiles / (int)gridDim.x));
-            const unsigned int base = atomicAdd(&sched[0], (unsigned)batch);
-            t_next = atomicAdd(&sched[0], 1u);
-            t_pend = atomicAdd(&sched[0], 1u);
+            // Prime the ring with this CTA's static first batch of GATE tiles (at most its fair share,
+            // so small layers spread over all CTAs). Weights are read-only, so the loads may start
+            // before the PDL predecessor has finished; everything it writes (tile counter, y
+            // accumulator, x, index lists) is touched only after griddepcontrol.wait below.
+            const unsigned int base = blockIdx.x * (unsigned)batch;
             for (int s = 0; s < batch; ++s) {
-                const unsigned int tile = base + s;
-                if (tile >= (unsigned)ntiles) break;
+                const unsigned int tile = base + s;  // grid * batch <= ntiles
                 const int r0 = (int)tile * NR;
                 const int nr = min(NR, m - r0);
                 desc[s].type = kJobGate;
@@ -196,11 +205,12 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 ++prod;
             }
         }
+        pdl_wait_primary();
+        if (lane == 0) claim_tile_async(t_res, sched, dyn_base + (unsigned)lazy_tail < (unsigned)ntiles);
         prod = __shfl_sync(0xffffffffu, prod, 0);
         ps = prod % stages;
         gates_inflight = prod;
-        while (!ended && prod < retire + stages && issue_job()) {
-        }
+        // the rest of the ring fills as jobs retire (UD work first)
         trace_stamp(trace, 0, 1);
 
         int rs = 0;                  // = retire % stages
@@ -280,6 +290,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         }
     } else {
         // ===================================== CONSUMER WARPS ====================================
+        pdl_wait_primary();     // x (and the accumulators) may come from the PDL predecessor
         float xr[B][CPT][VEC];  // x, own chunks, fp32
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
@@ -537,13 +548,26 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
     if (e != cudaSuccess) return e;
     char *w = static_cast<char *>(ws);
-    kern<<<k12_grid(p, B), k12_threads_c(B), smem, s>>>(
-        static_cast<const T *>(x), static_cast<const T *>(Wg), static_cast<const T *>(Wu), static_cast<const T *>(Wd),
-        p.d, p.m, stages, t, mode, reinterpret_cast<int32_t *>(w + p.off_idx),
+    // Programmatic dependent launch: the CTAs of this decode may become resident while the previous
+    // kernel on the stream drains, and start streaming their static W_gate tiles (see the kernel).
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)k12_grid(p, B));
+    cfg.blockDim = dim3((unsigned)k12_threads_c(B));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(
+        &cfg, kern, static_cast<const T *>(x), static_cast<const T *>(Wg), static_cast<const T *>(Wu),
+        static_cast<const T *>(Wd), p.d, p.m, stages, t, mode, reinterpret_cast<int32_t *>(w + p.off_idx),
         reinterpret_cast<uint8_t *>(w + p.off_tokmask), reinterpret_cast<float *>(w + p.off_vals),
         reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<unsigned long long *>(w + p.off_ypart), y,
-        reinterpret_cast<unsigned int *>(w + p.off_sched),
+        reinterpret_cast<unsigned int *>(w + p.off_sched), p.lazy_tail * k12_grid(p, B),
         p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -1,0 +1,791 @@
+// mlp_split.cu -- the CATS-MLP decode for batches b >= 2: two persistent kernels, KA and KB.
+//
+// Paper: Custom GPU Kernel "MLP using CATS":
+//     v <- SiLU(x W_gate); Mask <- |v| >= t; x1 <- (x W_up[Mask]) * v[Mask]; y <- x1 W_down[Mask]
+// with the batch semantics of DESIGN.md reading G6: a neuron's W_up / W_down rows are read once if it
+// is active for ANY of the b tokens (the union), and token i uses v_i = 0 where |v_i| < t.
+//
+// Why a second path. K12 keeps x and the exact fixed-point y partial of every token
+// in registers: 2*b*d values per CTA, which is the whole register file at b = 8. Here the two
+// register-heavy halves run in different kernels, each with its own work decomposition:
+//
+//  * KA (gate + up, dynamic): the K12 dataflow (persistent CTAs, tile counter, S-stage TMA bulk ring,
+//    one producer warp) with x staged once in shared memory. Jobs are GATE(tile of NR W_gate rows) and
+//    UP(<= NR active neurons' W_up rows, gathered across tiles from a FIFO). Every job is the same
+//    consumer work: NR x b dot products, bf16 x bf16 products accumulated in fp32 by FHFMA.BF16
+//    (fma.rn.f32.bf16 reads both bf16 halves straight from the packed registers: no unpack), one
+//    warp reduce-scatter (NR*b - 1 shuffles), a fixed-order sum over the 16 warps by the producer.
+//    The producer turns GATE results into u -> v = SiLU(u) -> keep = |v| >= t -> ballot compaction
+//    (idx / tokmask / vals / cnt, the same per-tile layout as K12) and UP results into
+//    x1 = (x W_up[j]) * v_j (Optimization 1), written per compact position.
+//    Each neuron's u and x1 are computed entirely inside one CTA in a fixed order: deterministic.
+//  * KB (down, static): the compact active list (tile segments, prefix-summed in every CTA) is cut
+//    into R equal ranges; CTA (r, q) streams the W_down rows of range r, column part q (d / Q
+//    columns, so y stays in <= 32 registers per thread), accumulates y_r = sum_j x1_j W_down[j] in
+//    fp32 in list order, writes the partial, and after a grid barrier every CTA sums a slice of the
+//    R partials in fixed order r = 0..R-1 into y: the deterministic two-phase split-K reduction of
+//    the north star. The equal ranges balance the data-dependent work exactly.
+//
+// KA -> KB -> next decode run as programmatic dependent launches: a kernel's CTAs become resident
+// while its predecessor drains and wait (griddepcontrol.wait) only before touching its outputs.
+#include "cats_device.cuh"
+#include "cats_internal.h"
+
+namespace cats {
+
+enum : int { kSJobEnd = 0, kSJobGate = 1, kSJobUp = 2 };
+
+// ------------------------------------------------------------------------------ arithmetic helpers
+// acc + sum_e w[e] * x[e] over one 16-byte chunk; products exact, fp32 accumulation in e order
+template <typename T>
+__device__ __forceinline__ float dot16(const uint4 &w, const uint4 &x, float acc);
+template <>
+__device__ __forceinline__ float dot16<bf16_bits>(const uint4 &w, const uint4 &x, float acc) {
+    asm("{\n\t.reg .b16 a0, a1, b0, b1;\n\t"
+        "mov.b32 {a0, a1}, %1;\n\tmov.b32 {b0, b1}, %5;\n\t"
+        "fma.rn.f32.bf16 %0, a0, b0, %0;\n\tfma.rn.f32.bf16 %0, a1, b1, %0;\n\t"
+        "mov.b32 {a0, a1}, %2;\n\tmov.b32 {b0, b1}, %6;\n\t"
+        "fma.rn.f32.bf16 %0, a0, b0, %0;\n\tfma.rn.f32.bf16 %0, a1, b1, %0;\n\t"
+        "mov.b32 {a0, a1}, %3;\n\tmov.b32 {b0, b1}, %7;\n\t"
+        "fma.rn.f32.bf16 %0, a0, b0, %0;\n\tfma.rn.f32.bf16 %0, a1, b1, %0;\n\t"
+        "mov.b32 {a0, a1}, %4;\n\tmov.b32 {b0, b1}, %8;\n\t"
+        "fma.rn.f32.bf16 %0, a0, b0, %0;\n\tfma.rn.f32.bf16 %0, a1, b1, %0;\n\t}"
+        : "+f"(acc)
+        : "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w), "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w));
+    return acc;
+}
+template <>
+__device__ __forceinline__ float dot16<float>(const uint4 &w, const uint4 &x, float acc) {
+    acc = fmaf(__uint_as_float(w.x), __uint_as_float(x.x), acc);
+    acc = fmaf(__uint_as_float(w.y), __uint_as_float(x.y), acc);
+    acc = fmaf(__uint_as_float(w.z), __uint_as_float(x.z), acc);
+    acc = fmaf(__uint_as_float(w.w), __uint_as_float(x.w), acc);
+    return acc;
+}
+
+// Sum a[P] over the 32 lanes of a warp; afterwards lane l holds the warp total of a[l % P].
+// Halving rounds (xor P/2 .. 1): a lane keeps the half selected by its lane bit and adds the
+// partner's copy of it (P - 1 shuffles in all), then xor rounds P .. 16 combine the lane groups.
+// A fixed tree: the same bits every run.
+template <int P>
+__device__ __forceinline__ float warp_reduce_scatter(float (&a)[P], int lane) {
+#pragma unroll
+    for (int h = P / 2; h >= 1; h >>= 1) {
+        const bool up = (lane & h) != 0;
+#pragma unroll
+        for (int j = 0; j < h; ++j) {
+            const float keep = up ? a[h + j] : a[j];
+            const float send = up ? a[j] : a[h + j];
+            a[j] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+        }
+    }
+    float v = a[0];
+#pragma unroll
+    for (int o = P; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+constexpr int pow2_ceil(int v) { return v <= 1 ? 1 : 2 * pow2_ceil((v + 1) / 2); }
+
+__device__ __forceinline__ void claim_async(unsigned int &t, unsigned int *ctr, bool pred) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p atom.global.add.u32 %0, [%1], 1;\n\t}"
+                 : "+r"(t)
+                 : "l"(ctr), "r"((unsigned)pred)
+                 : "memory");
+}
+constexpr unsigned int kNoTileS = 0xffffffffu;
+
+// ======================================================================================== KA
+template <typename T, int B, int NR>
+__global__ void __launch_bounds__(kSplitAThreads, 1)
+ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restrict__ Wu, int d, int m, int stages,
+           float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask, float *__restrict__ vals,
+           int32_t *__restrict__ cnt, float *__restrict__ x1out, unsigned int *__restrict__ sched, int lazy_tail,
+           unsigned long long *__restrict__ trace) {
+    constexpr int NW = kSplitAWarps;    // consumer warps (both groups)
+    constexpr int NC = NW * 32;
+    constexpr int NG = kSplitAGroups;    // independent job streams (producer + ring + consumers)
+    constexpr int NWG = NW / NG;         // consumer warps per group
+    constexpr int NCG = NWG * 32;
+    constexpr int NP = NR * B;          // (row, token) dot products per job
+    constexpr int PP = pow2_ceil(NP);   // padded to a power of two for the reduce-scatter
+    static_assert(PP <= 32, "one lane per (row, token) pair");
+    constexpr uint32_t TKM = (1u << B) - 1u;
+    using Desc = SplitDesc<NR, B>;
+    using Ent = SplitFifoEntry<B>;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = warp < NW ? warp / NWG : warp - NW;  // this warp's group
+    const int nch = d * (int)sizeof(T) / 16;
+    const uint32_t row_bytes = (uint32_t)d * (uint32_t)sizeof(T);
+    const uint32_t stage_bytes = (uint32_t)NR * row_bytes;
+    const int ntiles = (m + NR - 1) / NR;
+
+    // shared memory: x, then per group: ring, barriers, descriptors, FIFO, partial sums
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char *xs = smem;                                                             // [B][d] x
+    unsigned char *ring0 = xs + (size_t)B * row_bytes;                                    // [NG][stages][stage]
+    uint64_t *full0 = reinterpret_cast<uint64_t *>(ring0 + (size_t)NG * stages * stage_bytes);  // [NG][stages]
+    uint64_t *empty0 = full0 + NG * stages;                                               // [NG][stages]
+    Desc *desc0 = reinterpret_cast<Desc *>(empty0 + NG * stages);                         // [NG][stages]
+    Ent *fifo0 = reinterpret_cast<Ent *>(desc0 + NG * stages);                            // [NG][kSplitFifo]
+    float *red0 = reinterpret_cast<float *>(fifo0 + NG * kSplitFifo);                     // [NG][stages][NWG][PP]
+    unsigned char *ring = ring0 + (size_t)g * stages * stage_bytes;
+    uint64_t *full = full0 + g * stages;
+    uint64_t *empty = empty0 + g * stages;
+    Desc *desc = desc0 + g * stages;
+    Ent *fifo = fifo0 + g * kSplitFifo;
+    float *red = red0 + (size_t)g * stages * NWG * PP;
+
+    trace_stamp(trace, 0, 0);
+    pdl_launch_dependents();
+    if (tid == 0) {
+        for (int s = 0; s < NG * stages; ++s) {
+            mbar_init(&full0[s], 1);
+            mbar_init(&empty0[s], NWG);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp >= NW) {
+        // ===================================== PRODUCER WARPS ====================================
+        // one per group; the groups share the tile counter and x, nothing else
+        const bool dense = mode == kModeDense;
+        const uint64_t policy = l2_evict_first_policy();
+        unsigned int res0 = kNoTileS, res1 = kNoTileS;  // reserved tiles (raw counter values)
+        int rsel = 0;                                    // slot the next GATE issue uses
+        const int nstreams = (int)gridDim.x * NG;  // job streams in the grid
+        const int batch = max(1, min(stages, ntiles / nstreams));
+        const unsigned int dyn_base = (unsigned)nstreams * (unsigned)batch;
+        int prod = 0, ps = 0, retire = 0;
+        int q_head = 0, q_tail = 0;  // active-neuron FIFO (uniform across the warp)
+        int gates_inflight = 0;
+        bool ended = false;
+
+        auto issue_up = [&](int n) {  // UP job: W_up rows of the next n FIFO neurons
+            const int s = ps;
+            Desc &D = desc[s];
+            if (lane < n) {
+                const Ent &E = fifo[(q_head + lane) & (kSplitFifo - 1)];
+                D.id[lane] = E.id;
+                D.pos[lane] = E.pos;
+#pragma unroll
+                for (int tk = 0; tk < B; ++tk) D.v[lane][tk] = E.v[tk];
+            }
+            if (lane == 0) {
+                D.type = kSJobUp;
+                D.n = n;
+                mbar_arrive_expect_tx(&full[s], (uint32_t)n * row_bytes);
+            }
+            __syncwarp();
+            if (lane < n)
+                bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)lane * row_bytes, Wu + (size_t)D.id[lane] * d,
+                         row_bytes, &full[s], policy);
+            q_head += n;
+        };
+        auto issue_job = [&]() -> bool {
+            const int s = ps;
+            const int qn = q_tail - q_head;
+            if (qn >= NR) {
+                issue_up(NR);
+            } else {
+                // next tile: the reservation claimed two GATE issues ago (two slots used in turn,
+                // selected by branches so no instruction waits on the newest atomic); a slot that
+                // came back past the end is parked there and the other one is tried
+                unsigned int tile = kNoTileS;
+                if (lane == 0) {
+                    for (int tries = 0; tries < 2; ++tries) {
+                        unsigned int raw;
+                        if (rsel == 0) {
+                            raw = res0;
+                            if (raw == kNoTileS) raw = atomicAdd(&sched[0], 1u);
+                        } else {
+                            raw = res1;
+                            if (raw == kNoTileS) raw = atomicAdd(&sched[0], 1u);
+                        }
+                        if (raw + dyn_base < (unsigned)ntiles) {
+                            tile = raw + dyn_base;
+                            break;
+                        }
+                        if (rsel == 0) res0 = raw; else res1 = raw;
+                        rsel ^= 1;
+                    }
+                }
+                tile = __shfl_sync(0xffffffffu, tile, 0);
+                if (tile < (unsigned)ntiles) {
+                    const int r0 = (int)tile * NR;
+                    const int nr = min(NR, m - r0);
+                    if (lane == 0) {
+                        const bool more = tile + 1u + (unsigned)lazy_tail < (unsigned)ntiles;
+                        if (rsel == 0) {
+                            res0 = kNoTileS;
+                            claim_async(res0, sched, more);
+                        } else {
+                            res1 = kNoTileS;
+                            claim_async(res1, sched, more);
+                        }
+                        rsel ^= 1;
+                        desc[s].type = kSJobGate;
+                        desc[s].tile = (int)tile;
+                        desc[s].n = nr;
+                        mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
+                        bulk_g2s(ring + (size_t)s * stage_bytes, Wg + (size_t)r0 * d, (uint32_t)nr * row_bytes,
+                                 &full[s], policy);
+                    }
+                    ++gates_inflight;
+                } else {
+                    if (qn > 0) {
+                        issue_up(qn);  // drain a partial UP job
+                    } else if (gates_inflight != 0) {
+                        return false;  // an in-flight GATE job may still add neurons
+                    } else {
+                        if (lane == 0) {
+                            desc[s].type = kSJobEnd;
+                            desc[s].n = 0;
+                            mbar_arrive_expect_tx(&full[s], 0u);
+                        }
+                        ended = true;
+                    }
+                }
+            }
+            __syncwarp();
+            ++prod;
+            if (++ps == stages) ps = 0;
+            return true;
+        };
+
+        if (lane == 0) {  // static first batch (weights only: safe before the PDL wait)
+            const unsigned int base = (blockIdx.x * NG + g) * (unsigned)batch;
+            for (int s = 0; s < batch; ++s) {
+                if (base + s >= (unsigned)ntiles) break;  // tiny layers: fewer tiles than streams
+                ++prod;
+                const int r0 = (int)(base + s) * NR;
+                const int nr = min(NR, m - r0);
+                desc[s].type = kSJobGate;
+                desc[s].tile = (int)(base + s);
+                desc[s].n = nr;
+                mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
+                bulk_g2s(ring + (size_t)s * stage_bytes, Wg + (size_t)r0 * d, (uint32_t)nr * row_bytes, &full[s],
+                         policy);
+            }
+        }
+        prod = __shfl_sync(0xffffffffu, prod, 0);
+        ps = prod % stages;
+        gates_inflight = prod;
+        pdl_wait_primary();
+        if (lane == 0) {
+            claim_async(res0, sched, dyn_base + (unsigned)lazy_tail < (unsigned)ntiles);
+            claim_async(res1, sched, dyn_base + 1u + (unsigned)lazy_tail < (unsigned)ntiles);
+        }
+        if (prod == 0) {  // no static tile: claim (or end) right away
+            while (!ended && issue_job()) {
+            }
+        }
+
+        int rs = 0;
+        uint32_t rphase = 0;
+        const int r = lane / B, tk = lane % B;  // this lane's (row, token) pair
+        unsigned long long p_wait = 0;           // diagnostics (CATS_TRACE)
+        int n_gate = 0, n_up = 0;
+        // retire every job in order; after END (the last job issued, never released by the
+        // consumers) is queued, the UP jobs still in flight are retired before the loop exits
+        while (!ended || retire < prod - 1) {
+            const unsigned long long tw0 = trace ? gtimer() : 0ull;
+            mbar_wait(&empty[rs], rphase);
+            if (trace) p_wait += gtimer() - tw0;
+            const Desc &D = desc[rs];
+            if (trace) { if (D.type == kSJobGate) ++n_gate; else ++n_up; }
+            const int n = D.n;
+            const bool mine = lane < NP && r < n;
+            float u = 0.f;
+            if (mine) {
+                const float *rb = red + (size_t)rs * NWG * PP + lane;
+#pragma unroll
+                for (int w = 0; w < NWG; ++w) u += rb[w * PP];
+            }
+            if (D.type == kSJobGate) {
+                // u -> v = SiLU(u) (Eq. 2) -> keep = |v| >= t (Eq. 4, ties kept) -> compaction
+                const int tile = D.tile, r0 = tile * NR;
+                const float v = __fdividef(u, 1.0f + __expf(-u));
+                const bool keep = mine && (dense || fabsf(v) >= t);
+                const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+                uint32_t rowact = 0;
+#pragma unroll
+                for (int rr = 0; rr < NR; ++rr)
+                    if ((bal >> (rr * B)) & TKM) rowact |= 1u << rr;
+                const int nact = __popc(rowact);
+                if (lane < NP && ((rowact >> r) & 1u)) {
+                    const int rank = __popc(rowact & ((1u << r) - 1u));
+                    const int pos = r0 + rank;
+                    const float vk = keep ? v : 0.f;
+                    vals[(size_t)pos * B + tk] = vk;
+                    Ent &E = fifo[(q_tail + rank) & (kSplitFifo - 1)];
+                    E.v[tk] = vk;
+                    if (tk == 0) {
+                        idx[pos] = r0 + r;
+                        tokmask[pos] = (uint8_t)((bal >> (r * B)) & TKM);
+                        E.id = r0 + r;
+                        E.pos = pos;
+                    }
+                }
+                if (lane == 0) cnt[tile] = nact;
+                q_tail += nact;
+                --gates_inflight;
+            } else if (mine) {  // UP: x1 = (x W_up[j]) * v_j, per token
+                x1out[(size_t)D.pos[r] * B + tk] = u * D.v[r][tk];
+            }
+            __syncwarp();
+            ++retire;
+            if (++rs == stages) { rs = 0; rphase ^= 1u; }
+            while (!ended && prod < retire + stages && issue_job()) {
+            }
+        }
+        if (lane == 0) {
+            trace_put(trace, 2, 0, p_wait);
+            trace_put(trace, 2, 2, (unsigned long long)retire);
+            trace_put(trace, 2, 4, (unsigned long long)n_gate);
+            trace_put(trace, 2, 5, (unsigned long long)n_up);
+        }
+    } else {
+        // ===================================== CONSUMER WARPS ====================================
+        pdl_wait_primary();  // x may come from the predecessor
+        {
+            const uint4 *xg = reinterpret_cast<const uint4 *>(x);
+            uint4 *xd = reinterpret_cast<uint4 *>(xs);
+            for (int i = tid; i < B * nch; i += NC) xd[i] = xg[i];
+        }
+        consumer_barrier<NC>();
+        const uint32_t xbase = smem_u32(xs);
+        const int ctid = tid - g * NCG;  // consumer thread index within the group
+        const int cwarp = warp - g * NWG;
+        int s = 0;
+        uint32_t phase = 0;
+        unsigned long long c_wait = 0;
+        for (;;) {
+            const unsigned long long cw0 = trace ? gtimer() : 0ull;
+            mbar_wait(&full[s], phase);
+            if (trace) c_wait += gtimer() - cw0;
+            const int type = desc[s].type;
+            if (type == kSJobEnd) break;
+            const uint32_t sbase = smem_u32(ring + (size_t)s * stage_bytes);
+            float acc[PP];
+#pragma unroll
+            for (int p = 0; p < PP; ++p) acc[p] = 0.f;
+            for (int ch = ctid; ch < nch; ch += NCG) {
+                uint4 xv[B];
+#pragma unroll
+                for (int tk = 0; tk < B; ++tk) xv[tk] = lds128(xbase + (uint32_t)tk * row_bytes + (uint32_t)ch * 16u);
+                // rows r >= n of a short job hold stale shared memory: their sums are computed
+                // anyway (no branches) and ignored by the producer
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {
+                    const uint4 w = lds128(sbase + (uint32_t)r * row_bytes + (uint32_t)ch * 16u);
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) acc[r * B + tk] = dot16<T>(w, xv[tk], acc[r * B + tk]);
+                }
+            }
+            const float v = warp_reduce_scatter<PP>(acc, lane);
+            if (lane < PP) red[((size_t)s * NWG + cwarp) * PP + lane] = v;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == stages) { s = 0; phase ^= 1u; }
+        }
+        if (tid == 0) trace_put(trace, 2, 3, c_wait);
+    }
+    trace_stamp(trace, 0, 2);
+    __syncthreads();
+    if (tid == 0 && atomicAdd(&sched[1], 1u) == gridDim.x - 1) {  // last CTA: reset the tile scheduler
+        sched[0] = 0u;
+        sched[1] = 0u;
+        sched[2] = 0u;  // KB's grid-barrier counter
+    }
+    trace_stamp(trace, 0, 3);
+}
+
+// ======================================================================================== KB
+template <typename T, int B, int EPT>
+__global__ void __launch_bounds__(kSplitBMaxThreads, 1)
+kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, int stages, int rows_per_stage,
+        int maxr, const int32_t *__restrict__ idx, const int32_t *__restrict__ cnt, const float *__restrict__ x1in,
+        float *__restrict__ part, float *__restrict__ y, unsigned int *__restrict__ sched,
+        unsigned long long *__restrict__ trace) {
+    constexpr int EB = EPT * (int)sizeof(T);  // bytes of a thread's columns in one row (8 or 16)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nth = blockDim.x, NCW = nth / 32 - 1, NCt = NCW * 32;  // consumer warps / threads
+    const int rr = blockIdx.x / Q, q = blockIdx.x % Q;
+    const int part_cols = d / Q;
+    const uint32_t seg_bytes = (uint32_t)part_cols * (uint32_t)sizeof(T);
+    const uint32_t stage_bytes = (uint32_t)rows_per_stage * seg_bytes;
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char *ring = smem;                                                               // [stages][stage]
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * stage_bytes);       // [stages]
+    uint64_t *empty = full + stages;                                                          // [stages]
+    int *pre = reinterpret_cast<int *>(empty + stages);                                       // [ntiles + 1]
+    int *wsum = pre + ntiles + 1;                                                             // [32]
+    int *lj = wsum + 32;                                                                      // [maxr]
+    float *lx = reinterpret_cast<float *>(lj + maxr);                                         // [maxr][B]
+
+    trace_stamp(trace, 1, 0);
+    pdl_launch_dependents();
+    if (tid == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        fence_mbar_init();
+    }
+    pdl_wait_primary();  // everything below reads KA's outputs
+    trace_stamp(trace, 1, 5);
+
+    // ---- exclusive prefix of the per-tile active counts (every CTA, identical) ----
+    if (tid == 0) pre[0] = 0;
+    for (int base = 0; base < ntiles; base += 4 * nth) {  // 4 loads in flight per thread
+        int c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = base + u * nth + tid;
+            c[u] = i < ntiles ? __ldcg(cnt + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = base + u * nth + tid;
+            if (i < ntiles) pre[i + 1] = c[u];
+        }
+    }
+    __syncthreads();
+    {
+        const int per = (ntiles + nth - 1) / nth;
+        const int a = min(ntiles, tid * per), e = min(ntiles, a + per);
+        int sum = 0;
+        for (int i = a; i < e; ++i) sum += pre[i + 1];
+        int incl = sum;  // inclusive scan of the thread sums within the warp
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const int nwarps = nth / 32;
+            int w = lane < nwarps ? wsum[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += v;
+            }
+            if (lane < nwarps) wsum[lane] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        int run = (warp > 0 ? wsum[warp - 1] : 0) + incl - sum;  // exclusive start of this thread
+        for (int i = a; i < e; ++i) {
+            run += pre[i + 1];
+            pre[i + 1] = run;
+        }
+    }
+    __syncthreads();
+    trace_stamp(trace, 1, 6);
+    const long long U = pre[ntiles];
+    const int lo = (int)(U * rr / R), hi = (int)(U * (rr + 1) / R), len = hi - lo;
+
+    // ---- this range's neurons and x1 values: compact rank g -> (tile, k) by binary search ----
+    for (int i = tid; i < len; i += nth) {
+        const int g = lo + i;
+        int a = 0, b = ntiles;  // largest tau with pre[tau] <= g
+        while (b - a > 1) {
+            const int mid = (a + b) >> 1;
+            if (pre[mid] <= g) a = mid; else b = mid;
+        }
+        const int pos = a * nr_tile + (g - pre[a]);
+        lj[i] = __ldcg(idx + pos);
+#pragma unroll
+        for (int tk = 0; tk < B; ++tk) lx[i * B + tk] = __ldcg(x1in + (size_t)pos * B + tk);
+    }
+    __syncthreads();
+    trace_stamp(trace, 1, 1);
+    const int njobs = (len + rows_per_stage - 1) / rows_per_stage;
+
+    if (warp == NCW) {
+        // ---- producer: W_down row segments [j][q*part_cols, (q+1)*part_cols) into the ring ----
+        const uint64_t policy = l2_evict_first_policy();
+        for (int jn = 0; jn < njobs; ++jn) {
+            const int s = jn % stages;
+            if (jn >= stages) mbar_wait(&empty[s], (uint32_t)((jn / stages) - 1) & 1u);
+            const int r0 = jn * rows_per_stage, nrow = min(rows_per_stage, len - r0);
+            if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)nrow * seg_bytes);
+            __syncwarp();
+            if (lane < nrow)
+                bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)lane * seg_bytes,
+                         Wd + (size_t)lj[r0 + lane] * d + (size_t)q * part_cols, seg_bytes, &full[s], policy);
+        }
+    } else {
+        // ---- consumers: y[tk][c] += x1[j][tk] * W_down[j][c] over the range, list order, fp32 ----
+        const int c0 = tid * EPT;  // first column of this thread within the part
+        const bool own = c0 < part_cols;
+        float acc[B][EPT];
+#pragma unroll
+        for (int tk = 0; tk < B; ++tk)
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) acc[tk][e] = 0.f;
+        for (int jn = 0; jn < njobs; ++jn) {
+            const int s = jn % stages;
+            mbar_wait(&full[s], (uint32_t)(jn / stages) & 1u);
+            const int r0 = jn * rows_per_stage, nrow = min(rows_per_stage, len - r0);
+            if (own) {
+                const uint32_t sb = smem_u32(ring + (size_t)s * stage_bytes) + (uint32_t)c0 * sizeof(T);
+                for (int i = 0; i < nrow; ++i) {
+                    float wf[EPT];
+                    if constexpr (EB == 16) {
+                        unpack16(lds128(sb + (uint32_t)i * seg_bytes), wf);
+                    } else {  // 8 bytes = 4 bf16
+                        uint32_t w0, w1;
+                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "r"(sb + (uint32_t)i * seg_bytes));
+                        wf[0] = __uint_as_float(w0 << 16);
+                        wf[1] = __uint_as_float(w0 & 0xffff0000u);
+                        wf[2] = __uint_as_float(w1 << 16);
+                        wf[3] = __uint_as_float(w1 & 0xffff0000u);
+                    }
+                    const float *xr = lx + (size_t)(r0 + i) * B;
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) {
+                        const float a = xr[tk];
+#pragma unroll
+                        for (int e = 0; e < EPT; ++e) acc[tk][e] = fmaf(a, wf[e], acc[tk][e]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        if (own) {  // partial of range rr, columns of part q
+#pragma unroll
+            for (int tk = 0; tk < B; ++tk) {
+                float *dst = part + ((size_t)rr * B + tk) * d + (size_t)q * part_cols + c0;
+#pragma unroll
+                for (int e = 0; e < EPT; e += 4)
+                    *reinterpret_cast<float4 *>(dst + e) = make_float4(acc[tk][e], acc[tk][e + 1], acc[tk][e + 2], acc[tk][e + 3]);
+            }
+        }
+    }
+    trace_stamp(trace, 1, 2);
+
+    // ---- grid barrier (all R*Q CTAs are resident: one per SM, launched together) ----
+    __syncthreads();
+    if (tid == 0) {
+        // arrival counter sched[2] (zeroed by KA's last CTA, which completes before KB passes
+        // griddepcontrol.wait): the barrier opens when every CTA of this grid has arrived
+        __threadfence();
+        atomicAdd(&sched[2], 1u);
+        unsigned int seen;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(sched + 2) : "memory");
+        } while (seen < gridDim.x);
+    }
+    __syncthreads();
+    trace_stamp(trace, 1, 3);
+
+    // ---- fixed-order reduction: y[e] = sum_{r=0..R-1} part[r][e], this CTA's slice of B*d ----
+    {
+        const int total4 = B * d / 4;
+        const int G = gridDim.x, gidx = blockIdx.x;
+        const int g0 = (int)((long long)total4 * gidx / G), g1 = (int)((long long)total4 * (gidx + 1) / G);
+        const int ng = g1 - g0;
+        // r-slices per float4 group: enough that each thread has <= 8 partials (one batch of loads)
+        const int ns = ng > 0 ? max(1, min(min(R, nth / ng), max((R + 7) / 8, 4))) : 1;
+        const float4 *p4 = reinterpret_cast<const float4 *>(part);
+        if (ns == 1) {  // (few CTAs) each thread sums whole columns
+            for (int i = tid; i < ng; i += nth) {
+                float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int r = 0; r < R; r += 8) {
+                    float4 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        v[u] = r + u < R ? __ldcg(p4 + (size_t)(r + u) * total4 + g0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        a.x += v[u].x; a.y += v[u].y; a.z += v[u].z; a.w += v[u].w;
+                    }
+                }
+                reinterpret_cast<float4 *>(y)[g0 + i] = a;
+            }
+        } else {  // ng * ns <= nth: slice sums into the (idle) ring, then a fixed-order sum of slices
+            float4 *red4 = reinterpret_cast<float4 *>(ring);
+            if (tid < ng * ns) {
+                const int grp = tid % ng, sl = tid / ng;
+                float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int r = sl; r < R; r += 8 * ns) {  // 8 loads in flight, summed in r order
+                    float4 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        v[u] = r + u * ns < R ? __ldcg(p4 + (size_t)(r + u * ns) * total4 + g0 + grp)
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        a.x += v[u].x; a.y += v[u].y; a.z += v[u].z; a.w += v[u].w;
+                    }
+                }
+                red4[sl * ng + grp] = a;
+            }
+            __syncthreads();
+            if (tid < ng) {
+                float4 a = red4[tid];
+                for (int sl = 1; sl < ns; ++sl) {
+                    const float4 v = red4[sl * ng + tid];
+                    a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+                }
+                reinterpret_cast<float4 *>(y)[g0 + tid] = a;
+            }
+        }
+    }
+    trace_stamp(trace, 1, 4);
+}
+
+// ================================================================================== host side
+// KA shared memory: x [b][d], then per group (kSplitAGroups): the ring, 2 mbarriers, a descriptor and
+// the warp partial sums per stage, and the FIFO. `stages` counts stages per group.
+static size_t split_ka_per_stage(const PlanData &p, int b) {
+    const int nr = k12_rows_per_tile(p, b);
+    const size_t desc = (3 + 2 * (size_t)nr + (size_t)nr * b) * 4;  // sizeof(SplitDesc<nr, b>)
+    return (size_t)nr * p.d * p.esize + 16 + desc + (size_t)(kSplitAWarps / kSplitAGroups) * pow2_ceil(nr * b) * 4;
+}
+size_t split_ka_smem(const PlanData &p, int b, int stages) {
+    const size_t ent = (2 + (size_t)b) * 4;  // sizeof(SplitFifoEntry<b>)
+    return (size_t)b * p.d * p.esize + kSplitAGroups * ((size_t)stages * split_ka_per_stage(p, b) + kSplitFifo * ent);
+}
+int split_ka_stages(const PlanData &p, int b) {
+    const size_t fixed = split_ka_smem(p, b, 0);
+    if (fixed >= kSmemBudget) return 0;
+    return (int)std::min<size_t>((kSmemBudget - fixed) / (kSplitAGroups * split_ka_per_stage(p, b)), kMaxStages);
+}
+static int split_kb_rows_per_stage(const PlanData &p, int b) {
+    const size_t seg = (size_t)split_part_cols(p, b) * p.esize;
+    return (int)std::max<size_t>(1, std::min<size_t>(32, (32 * 1024) / seg));
+}
+static int split_kb_maxr(const PlanData &p, int b) {
+    const int R = split_ranges(p, b);
+    return (p.m + R - 1) / R + 1;
+}
+size_t split_kb_smem(const PlanData &p, int b, int stages) {
+    const size_t seg = (size_t)split_part_cols(p, b) * p.esize;
+    const size_t stage = (size_t)split_kb_rows_per_stage(p, b) * seg;
+    const int ntiles = k12_ntiles(p, b);
+    const int maxr = split_kb_maxr(p, b);
+    return (size_t)stages * stage + (size_t)stages * 16 + (size_t)(ntiles + 1 + 32) * 4 + (size_t)maxr * 4 +
+           (size_t)maxr * b * 4;
+}
+int split_kb_stages(const PlanData &p, int b) {
+    const size_t seg = (size_t)split_part_cols(p, b) * p.esize;
+    const size_t stage = (size_t)split_kb_rows_per_stage(p, b) * seg;
+    const size_t fixed = split_kb_smem(p, b, 0);
+    if (fixed >= kSmemBudget) return 0;
+    int st = (int)std::min<size_t>((kSmemBudget - fixed) / (stage + 16), kMaxStages);
+    // the reduction scratch (one float4 per thread) lives in the ring
+    while (st > 0 && (size_t)st * stage < (size_t)kSplitBMaxThreads * 16) ++st;
+    return st;
+}
+bool split_supported(const PlanData &p, int b) {
+    if (b < 2 || b > 8) return false;
+    if (p.d % (split_q(b) * split_ept(p, b)) != 0) return false;
+    if (((size_t)split_part_cols(p, b) * p.esize) % 16 != 0) return false;
+    if (split_kb_consumers(p, b) + 32 > kSplitBMaxThreads) return false;
+    const int sa = split_ka_stages(p, b), sb = split_kb_stages(p, b);
+    if (sa < 2 || split_ka_smem(p, b, sa) > kSmemBudget) return false;  // >= 2 stages per group
+    if (sb < 2 || split_kb_smem(p, b, sb) > kSmemBudget) return false;
+    return true;
+}
+
+static cudaLaunchConfig_t pdl_config(cudaLaunchAttribute *attr, int grid, int threads, size_t smem,
+                                     cudaStream_t s) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cfg;
+}
+
+template <typename T, int B, int NR>
+static cudaError_t launch_ka(const PlanData &p, const void *x, const void *Wg, const void *Wu, float t, int mode,
+                             void *ws, cudaStream_t s) {
+    static_assert(sizeof(SplitDesc<NR, B>) == (3 + 2 * NR + NR * B) * 4, "split_ka_smem layout");
+    static_assert(sizeof(SplitFifoEntry<B>) == (2 + B) * 4, "split_ka_smem layout");
+    auto kern = ka_gate_up<T, B, NR>;
+    const int stages = split_ka_stages(p, B);
+    const size_t smem = split_ka_smem(p, B, stages);
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
+    if (e != cudaSuccess) return e;
+    char *w = static_cast<char *>(ws);
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = pdl_config(attr, split_ka_grid(p, B), kSplitAThreads, smem, s);
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<const T *>(x), static_cast<const T *>(Wg),
+                              static_cast<const T *>(Wu), p.d, p.m, stages, t, mode,
+                              reinterpret_cast<int32_t *>(w + p.off_idx), reinterpret_cast<uint8_t *>(w + p.off_tokmask),
+                              reinterpret_cast<float *>(w + p.off_vals), reinterpret_cast<int32_t *>(w + p.off_cnt),
+                              reinterpret_cast<float *>(w + p.off_x1), reinterpret_cast<unsigned int *>(w + p.off_sched),
+                              p.lazy_tail * split_ka_grid(p, B),
+                              p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
+}
+
+template <typename T, int B, int EPT>
+static cudaError_t launch_kb(const PlanData &p, const void *Wd, float *y, void *ws, cudaStream_t s) {
+    auto kern = kb_down<T, B, EPT>;
+    const int stages = split_kb_stages(p, B);
+    const size_t smem = split_kb_smem(p, B, stages);
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
+    if (e != cudaSuccess) return e;
+    char *w = static_cast<char *>(ws);
+    cudaLaunchAttribute attr[1];
+    const int threads = split_kb_consumers(p, B) + 32;
+    cudaLaunchConfig_t cfg = pdl_config(attr, split_kb_grid(p, B), threads, smem, s);
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<const T *>(Wd), p.d, k12_ntiles(p, B), k12_rows_per_tile(p, B),
+                              split_q(B), split_ranges(p, B), stages, split_kb_rows_per_stage(p, B),
+                              split_kb_maxr(p, B), reinterpret_cast<const int32_t *>(w + p.off_idx),
+                              reinterpret_cast<const int32_t *>(w + p.off_cnt),
+                              reinterpret_cast<const float *>(w + p.off_x1), reinterpret_cast<float *>(w + p.off_part), y,
+                              reinterpret_cast<unsigned int *>(w + p.off_sched),
+                              p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
+}
+
+template <typename T, int B>
+static cudaError_t launch_split_b(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
+                                  float t, int mode, float *y, void *ws, cudaStream_t s, cudaEvent_t ev_mid) {
+    cudaError_t e = k12_rows_per_tile(p, B) == 4 ? launch_ka<T, B, 4>(p, x, Wg, Wu, t, mode, ws, s)
+                                                 : launch_ka<T, B, 2>(p, x, Wg, Wu, t, mode, ws, s);
+    if (e != cudaSuccess) return e;
+    if (ev_mid) {
+        e = cudaEventRecord(ev_mid, s);
+        if (e != cudaSuccess) return e;
+    }
+    constexpr int EPT = sizeof(T) == 4 ? 4 : (B <= 4 ? 8 : 4);  // = split_ept()
+    return launch_kb<T, B, EPT>(p, Wd, y, ws, s);
+}
+
+template <typename T>
+static cudaError_t launch_split_dt(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu,
+                                   const void *Wd, float t, int mode, float *y, void *ws, cudaStream_t s,
+                                   cudaEvent_t ev) {
+    switch (b) {
+        case 2: return launch_split_b<T, 2>(p, x, Wg, Wu, Wd, t, mode, y, ws, s, ev);
+        case 3: return launch_split_b<T, 3>(p, x, Wg, Wu, Wd, t, mode, y, ws, s, ev);
+        case 4: return launch_split_b<T, 4>(p, x, Wg, Wu, Wd, t, mode, y, ws, s, ev);
+        case 5: return launch_split_b<T, 5>(p, x, Wg, Wu, Wd, t, mode, y, ws, s, ev);
+        case 6: return launch_split_b<T, 6>(p, x, Wg, Wu, Wd, t, mode, y, ws, s, ev);
+        case 7: return launch_split_b<T, 7>(p, x, Wg, Wu, Wd, t, mode, y, ws, s, ev);
+        case 8: return launch_split_b<T, 8>(p, x, Wg, Wu, Wd, t, mode, y, ws, s, ev);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_split(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd,
+                         float t, int mode, float *y, void *ws, cudaStream_t s, cudaEvent_t ev_mid) {
+    if (p.dt == CATS_BF16) return launch_split_dt<bf16_bits>(p, x, b, Wg, Wu, Wd, t, mode, y, ws, s, ev_mid);
+    return launch_split_dt<float>(p, x, b, Wg, Wu, Wd, t, mode, y, ws, s, ev_mid);
+}
+
+}  // namespace cats

@@ -57,31 +57,37 @@ ws[off.value:off.value + nbytes.value].zero_()
 step(20)
 torch.cuda.synchronize()
 tr = ws[off.value:off.value + nbytes.value].cpu().numpy().view(np.uint64).reshape(3, 512, 8).astype(np.int64)
-info = plan.info
-grids = [info["grid"], 0]
-t0 = tr[0, :grids[0], 0].min()
 rep = {}
-names = {0: ["start", "primed", "jobs_done", "exit"], 1: ["start", "k12_visible", "exit"]}
-for k in range(1):
-    g = min(grids[k], 512)
-    print(f"K{k + 1} ({g} CTAs), us relative to first K1 CTA start:")
+t0 = None
+names = {0: ["start", "primed", "jobs_done", "exit"], 1: ["start", "list_ready", "jobs_done", "barrier", "exit", "pdl_waited", "prefix_done"]}
+titles = {0: "K12 / KA", 1: "KB"}
+for k in range(2):
+    g = int((tr[k, :, 0] > 0).sum())  # CTAs that stamped
+    if g == 0:
+        continue
+    if t0 is None:
+        t0 = tr[k, :g, 0].min()
+    print(f"{titles[k]} ({g} CTAs), us relative to the first CTA start:")
     for sidx, nm in enumerate(names[k]):
         v = (tr[k, :g, sidx] - t0) / 1e3
         v = v[tr[k, :g, sidx] > 0]
         if len(v):
             print(f"   {nm:12s} min {v.min():8.2f}  avg {v.mean():8.2f}  max {v.max():8.2f}")
-            rep[f"K{k + 1}.{nm}"] = [float(v.min()), float(v.mean()), float(v.max())]
-g = grids[0]
+            rep[f"K{k}.{nm}"] = [float(v.min()), float(v.mean()), float(v.max())]
+g = int((tr[0, :, 0] > 0).sum())
 st = tr[2, :g, :7].astype(np.float64)
-print("K12 per-CTA stats (avg/min/max):")
-for i, nm in enumerate(["producer wait ns", "producer busy ns", "jobs retired", "consumer wait ns", "gate jobs", "ud jobs", "producer issue ns"]):
-    print(f"   {nm:18s} {st[:, i].mean():10.1f} {st[:, i].min():10.1f} {st[:, i].max():10.1f}")
-lg = (tr[2, :g, 7] - t0) / 1e3
-jd = (tr[0, :g, 2] - t0) / 1e3
-ok = tr[2, :g, 7] > 0
-print("last GATE issue (us): p10/50/90/max", np.percentile(lg[ok], [10, 50, 90, 100]).round(2))
-print("jobs_done - last GATE issue (us): p10/50/90/max", np.percentile((jd - lg)[ok], [10, 50, 90, 100]).round(2))
-corr = np.corrcoef(st[:, 2], jd)[0, 1]
-print("corr(jobs retired, jobs_done time)", round(float(corr), 3))
+if st[:, 2].max() > 0:  # K12 producer / consumer statistics
+    print("K12 per-CTA stats (avg/min/max):")
+    for i, nm in enumerate(["producer wait ns", "producer busy ns", "jobs retired", "consumer wait ns", "gate jobs",
+                            "ud jobs", "producer issue ns"]):
+        print(f"   {nm:18s} {st[:, i].mean():10.1f} {st[:, i].min():10.1f} {st[:, i].max():10.1f}")
+    lg = (tr[2, :g, 7] - t0) / 1e3
+    jd = (tr[0, :g, 2] - t0) / 1e3
+    ok = tr[2, :g, 7] > 0
+    if ok.any():
+        print("last GATE issue (us): p10/50/90/max", np.percentile(lg[ok], [10, 50, 90, 100]).round(2))
+        print("jobs_done - last GATE issue (us): p10/50/90/max",
+              np.percentile((jd - lg)[ok], [10, 50, 90, 100]).round(2))
+    print("corr(jobs retired, jobs_done time)", round(float(np.corrcoef(st[:, 2], jd)[0, 1]), 3))
 if a.json:
     json.dump(rep, open(a.json, "w"), indent=1)

@@ -274,3 +274,20 @@ def test_calibration_full_size_config4():
         assert info["passes"] <= 2
     del acts
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("d,m,b,k", [(4096, 11008, 2, 0.5), (4096, 11008, 8, 0.9), (5120, 3456, 5, 0.7),
+                                     (264, 1000, 3, 0.5)])
+def test_split_path_matches_fused_path(d, m, b, k, monkeypatch):
+    """b >= 2 runs the split path (KA gate+up, KB down); forcing K12 on the same inputs must give the
+    same y within the parity tolerance (the two differ only in fp32 summation order)."""
+    Wg, Wu, Wd = (_dev(a) for a in cats_synth.mlp_weights(d, m, torch.bfloat16, layer=b))
+    x = _dev(cats_synth.tokens(b, d, torch.bfloat16, seed=21))
+    plan_s = cats.MlpPlan(d, m, max_batch=b)
+    monkeypatch.setenv("CATS_SPLIT_MIN_B", "9")
+    plan_f = cats.MlpPlan(d, m, max_batch=b)
+    t = 0.1 if k < 0.9 else 0.3
+    ys = cats.cats_mlp_decode(plan_s, x, Wg, Wu, Wd, t, ws=plan_s.workspace())
+    yf = cats.cats_mlp_decode(plan_f, x, Wg, Wu, Wd, t, ws=plan_f.workspace())
+    err = (ys.double() - yf.double()).norm() / yf.double().norm().clamp_min(1e-30)
+    assert float(err) <= Y_TOL
