@@ -353,6 +353,7 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
             x1_bytes = std::max(x1_bytes, (size_t)k12_ntiles(p, b) * k12_rows_per_tile(p, b) * b * 4);
         }
         p.off_x1 = off;      off = align_up(off + x1_bytes, 256);
+        p.off_tmask = off;   off = align_up(off + (size_t)((m + 1) / 2) * 4, 256);
         p.off_part = off;    off = align_up(off + part_bytes, 256);
         const char *tr = std::getenv("CATS_TRACE");
         p.trace = tr && tr[0] == '1';
@@ -406,6 +407,9 @@ extern "C" cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, vo
                                               static_cast<cudaStream_t>(s));
     if (e == cudaSuccess)
         e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_ypart, 0, (size_t)plan->p.max_batch * plan->p.d * 8,
+                            static_cast<cudaStream_t>(s));
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_tmask, 0, (size_t)((plan->p.m + 1) / 2) * 4,
                             static_cast<cudaStream_t>(s));
     return cuda_status(e);
 }

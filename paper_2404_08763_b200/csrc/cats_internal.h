@@ -41,6 +41,7 @@ struct PlanData {
     int lazy_tail;      // K12 stops reserving tile ids for the last lazy_tail * grid tiles (CATS_LAZY_TAIL)
     int split_min_b;    // batches b >= split_min_b run the split path KA + KB (CATS_SPLIT_MIN_B)
     size_t off_x1, off_part;  // split path: x1 per compact position [m][max_b]; KB partials [R][max_b][d]
+    size_t off_tmask;         // split path: per-tile active-row mask words (KA -> KB), zero between calls
     size_t off_trace, trace_bytes;
 };
 
@@ -86,8 +87,8 @@ struct SplitFifoEntry {  // one active neuron waiting for its UP job
     float v[B];
 };
 
-inline int split_q(int b) { return b <= 4 ? 1 : 2; }  // KB column parts (bounds y registers per thread)
-inline int split_ept(const PlanData &p, int b) { return p.esize == 4 ? 4 : (b <= 4 ? 8 : 4); }  // KB columns/thread
+inline int split_q(int) { return 2; }  // KB column parts (halves the partials; bounds y registers per thread)
+inline int split_ept(const PlanData &, int) { return 4; }  // KB columns per thread (16 B fp32, 8 B bf16)
 inline int split_part_cols(const PlanData &p, int b) { return p.d / split_q(b); }
 inline int split_kb_consumers(const PlanData &p, int b) {
     const int c = (split_part_cols(p, b) + split_ept(p, b) - 1) / split_ept(p, b);

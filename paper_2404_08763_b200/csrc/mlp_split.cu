@@ -100,8 +100,8 @@ template <typename T, int B, int NR>
 __global__ void __launch_bounds__(kSplitAThreads, 1)
 ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restrict__ Wu, int d, int m, int stages,
            float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask, float *__restrict__ vals,
-           int32_t *__restrict__ cnt, float *__restrict__ x1out, unsigned int *__restrict__ sched, int lazy_tail,
-           unsigned long long *__restrict__ trace) {
+           int32_t *__restrict__ cnt, unsigned int *__restrict__ tmask, float *__restrict__ x1out,
+           unsigned int *__restrict__ sched, int lazy_tail, unsigned long long *__restrict__ trace) {
     constexpr int NW = kSplitAWarps;    // consumer warps (both groups)
     constexpr int NC = NW * 32;
     constexpr int NG = kSplitAGroups;    // independent job streams (producer + ring + consumers)
@@ -329,7 +329,13 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
                         E.pos = pos;
                     }
                 }
-                if (lane == 0) cnt[tile] = nact;
+                if (lane == 0) {
+                    cnt[tile] = nact;
+                    // one self-contained word per tile (valid bit + active rows): KB starts from these
+                    // while KA is still running its UP jobs
+                    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(tmask + tile), "r"(0x80000000u | rowact)
+                                 : "memory");
+                }
                 q_tail += nact;
                 --gates_inflight;
             } else if (mine) {  // UP: x1 = (x W_up[j]) * v_j, per token
@@ -407,9 +413,8 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
 template <typename T, int B, int EPT>
 __global__ void __launch_bounds__(kSplitBMaxThreads, 1)
 kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, int stages, int rows_per_stage,
-        int maxr, const int32_t *__restrict__ idx, const int32_t *__restrict__ cnt, const float *__restrict__ x1in,
-        float *__restrict__ part, float *__restrict__ y, unsigned int *__restrict__ sched,
-        unsigned long long *__restrict__ trace) {
+        int maxr, unsigned int *__restrict__ tmask, const float *__restrict__ x1in, float *__restrict__ part,
+        float *__restrict__ y, unsigned int *__restrict__ sched, unsigned long long *__restrict__ trace) {
     constexpr int EB = EPT * (int)sizeof(T);  // bytes of a thread's columns in one row (8 or 16)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nth = blockDim.x, NCW = nth / 32 - 1, NCt = NCW * 32;  // consumer warps / threads
@@ -425,7 +430,9 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     int *pre = reinterpret_cast<int *>(empty + stages);                                       // [ntiles + 1]
     int *wsum = pre + ntiles + 1;                                                             // [32]
     int *lj = wsum + 32;                                                                      // [maxr]
-    float *lx = reinterpret_cast<float *>(lj + maxr);                                         // [maxr][B]
+    int *lpos = lj + maxr;                                                                    // [maxr]
+    float *lx = reinterpret_cast<float *>(lpos + maxr);                                       // [maxr][B]
+    uint8_t *rowm = reinterpret_cast<uint8_t *>(lx + (size_t)maxr * B);                       // [ntiles]
 
     trace_stamp(trace, 1, 0);
     pdl_launch_dependents();
@@ -436,24 +443,31 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
         }
         fence_mbar_init();
     }
-    pdl_wait_primary();  // everything below reads KA's outputs
-    trace_stamp(trace, 1, 5);
-
-    // ---- exclusive prefix of the per-tile active counts (every CTA, identical) ----
+    // ---- per-tile active-row masks, published by KA's GATE retire (valid bit 31). KB does NOT wait
+    //      for KA to finish here: the list and the first W_down loads overlap KA's UP tail. ----
     if (tid == 0) pre[0] = 0;
     for (int base = 0; base < ntiles; base += 4 * nth) {  // 4 loads in flight per thread
-        int c[4];
+        unsigned int c[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int i = base + u * nth + tid;
-            c[u] = i < ntiles ? __ldcg(cnt + i) : 0;
+            c[u] = 0x80000000u;
+            if (i < ntiles) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c[u]) : "l"(tmask + i) : "memory");
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int i = base + u * nth + tid;
-            if (i < ntiles) pre[i + 1] = c[u];
+            if (i < ntiles) {
+                while (!(c[u] & 0x80000000u)) {  // that tile's GATE job has not retired yet
+                    __nanosleep(128);
+                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c[u]) : "l"(tmask + i) : "memory");
+                }
+                rowm[i] = (uint8_t)(c[u] & 0xffu);
+                pre[i + 1] = __popc(c[u] & 0xffu);
+            }
         }
     }
+    trace_stamp(trace, 1, 5);
     __syncthreads();
     {
         const int per = (ntiles + nth - 1) / nth;
@@ -490,7 +504,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     const long long U = pre[ntiles];
     const int lo = (int)(U * rr / R), hi = (int)(U * (rr + 1) / R), len = hi - lo;
 
-    // ---- this range's neurons and x1 values: compact rank g -> (tile, k) by binary search ----
+    // ---- this range's neurons: compact rank g -> (tile, k) by binary search; neuron = k-th set row ----
     for (int i = tid; i < len; i += nth) {
         const int g = lo + i;
         int a = 0, b = ntiles;  // largest tau with pre[tau] <= g
@@ -498,10 +512,11 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
             const int mid = (a + b) >> 1;
             if (pre[mid] <= g) a = mid; else b = mid;
         }
-        const int pos = a * nr_tile + (g - pre[a]);
-        lj[i] = __ldcg(idx + pos);
-#pragma unroll
-        for (int tk = 0; tk < B; ++tk) lx[i * B + tk] = __ldcg(x1in + (size_t)pos * B + tk);
+        const int k = g - pre[a];
+        unsigned int msk = rowm[a];
+        for (int j = 0; j < k; ++j) msk &= msk - 1u;  // drop the k lowest set rows
+        lj[i] = a * nr_tile + (__ffs(msk) - 1);
+        lpos[i] = a * nr_tile + k;
     }
     __syncthreads();
     trace_stamp(trace, 1, 1);
@@ -522,6 +537,9 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
         }
     } else {
         // ---- consumers: y[tk][c] += x1[j][tk] * W_down[j][c] over the range, list order, fp32 ----
+        pdl_wait_primary();  // x1 comes from KA's UP jobs: KA must have completed
+        for (int i = tid; i < len * B; i += NCt) lx[i] = __ldcg(x1in + (size_t)lpos[i / B] * B + (i % B));
+        asm volatile("bar.sync 1, %0;" ::"r"(NCt) : "memory");  // consumers only
         const int c0 = tid * EPT;  // first column of this thread within the part
         const bool own = c0 < part_cols;
         float acc[B][EPT];
@@ -585,6 +603,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     }
     __syncthreads();
     trace_stamp(trace, 1, 3);
+    for (int i = blockIdx.x * nth + tid; i < ntiles; i += gridDim.x * nth) tmask[i] = 0u;  // for the next call
 
     // ---- fixed-order reduction: y[e] = sum_{r=0..R-1} part[r][e], this CTA's slice of B*d ----
     {
@@ -672,8 +691,8 @@ size_t split_kb_smem(const PlanData &p, int b, int stages) {
     const size_t stage = (size_t)split_kb_rows_per_stage(p, b) * seg;
     const int ntiles = k12_ntiles(p, b);
     const int maxr = split_kb_maxr(p, b);
-    return (size_t)stages * stage + (size_t)stages * 16 + (size_t)(ntiles + 1 + 32) * 4 + (size_t)maxr * 4 +
-           (size_t)maxr * b * 4;
+    return (size_t)stages * stage + (size_t)stages * 16 + (size_t)(ntiles + 1 + 32) * 4 + (size_t)maxr * 8 +
+           (size_t)maxr * b * 4 + (size_t)ntiles;
 }
 int split_kb_stages(const PlanData &p, int b) {
     const size_t seg = (size_t)split_part_cols(p, b) * p.esize;
@@ -727,7 +746,8 @@ static cudaError_t launch_ka(const PlanData &p, const void *x, const void *Wg, c
                               static_cast<const T *>(Wu), p.d, p.m, stages, t, mode,
                               reinterpret_cast<int32_t *>(w + p.off_idx), reinterpret_cast<uint8_t *>(w + p.off_tokmask),
                               reinterpret_cast<float *>(w + p.off_vals), reinterpret_cast<int32_t *>(w + p.off_cnt),
-                              reinterpret_cast<float *>(w + p.off_x1), reinterpret_cast<unsigned int *>(w + p.off_sched),
+                              reinterpret_cast<unsigned int *>(w + p.off_tmask), reinterpret_cast<float *>(w + p.off_x1),
+                              reinterpret_cast<unsigned int *>(w + p.off_sched),
                               p.lazy_tail * split_ka_grid(p, B),
                               p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
 }
@@ -745,8 +765,7 @@ static cudaError_t launch_kb(const PlanData &p, const void *Wd, float *y, void *
     cudaLaunchConfig_t cfg = pdl_config(attr, split_kb_grid(p, B), threads, smem, s);
     return cudaLaunchKernelEx(&cfg, kern, static_cast<const T *>(Wd), p.d, k12_ntiles(p, B), k12_rows_per_tile(p, B),
                               split_q(B), split_ranges(p, B), stages, split_kb_rows_per_stage(p, B),
-                              split_kb_maxr(p, B), reinterpret_cast<const int32_t *>(w + p.off_idx),
-                              reinterpret_cast<const int32_t *>(w + p.off_cnt),
+                              split_kb_maxr(p, B), reinterpret_cast<unsigned int *>(w + p.off_tmask),
                               reinterpret_cast<const float *>(w + p.off_x1), reinterpret_cast<float *>(w + p.off_part), y,
                               reinterpret_cast<unsigned int *>(w + p.off_sched),
                               p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
@@ -762,7 +781,7 @@ static cudaError_t launch_split_b(const PlanData &p, const void *x, const void *
         e = cudaEventRecord(ev_mid, s);
         if (e != cudaSuccess) return e;
     }
-    constexpr int EPT = sizeof(T) == 4 ? 4 : (B <= 4 ? 8 : 4);  // = split_ept()
+    constexpr int EPT = 4;  // = split_ept()
     return launch_kb<T, B, EPT>(p, Wd, y, ws, s);
 }
 
