@@ -291,19 +291,14 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     } else {
         // ===================================== CONSUMER WARPS ====================================
         pdl_wait_primary();     // x (and the accumulators) may come from the PDL predecessor
-        float xr[B][CPT][VEC];  // x, own chunks, fp32
+        uint4 xr[B][CPT];  // x, own chunks, packed (bf16 pairs or fp32), 0 past the row end
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             const int ch = tid + k * NC;
 #pragma unroll
-            for (int tk = 0; tk < B; ++tk) {
-                if (ch < nch) {
-                    unpack16(*reinterpret_cast<const uint4 *>(x + (size_t)tk * d + (size_t)ch * VEC), xr[tk][k]);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < VEC; ++e) xr[tk][k][e] = 0.f;
-                }
-            }
+            for (int tk = 0; tk < B; ++tk)
+                xr[tk][k] = ch < nch ? *reinterpret_cast<const uint4 *>(x + (size_t)tk * d + (size_t)ch * VEC)
+                                     : make_uint4(0u, 0u, 0u, 0u);
         }
         int yhi[B][CPT][VEC], ylo[B][CPT][VEC];  // exact fixed-point partial of y (units 2^-30), own chunks
 #pragma unroll
@@ -346,14 +341,9 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
 #pragma unroll
                     for (int tk = 0; tk < B; ++tk) part[r][tk] = 0.f;
 #pragma unroll
-                    for (int k = 0; k < CPT; ++k) {
-                        float wf[VEC];
-                        unpack16(wr[r][k], wf);
+                    for (int k = 0; k < CPT; ++k)
 #pragma unroll
-                        for (int tk = 0; tk < B; ++tk)
-#pragma unroll
-                            for (int e = 0; e < VEC; ++e) part[r][tk] = fmaf(xr[tk][k][e], wf[e], part[r][tk]);
-                    }
+                        for (int tk = 0; tk < B; ++tk) part[r][tk] = dot16<T>(wr[r][k], xr[tk][k], part[r][tk]);
                 }
 #pragma unroll
                 for (int r = 0; r < NR; ++r)
@@ -390,14 +380,9 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
 #pragma unroll
                     for (int tk = 0; tk < B; ++tk) part[i][tk] = 0.f;
 #pragma unroll
-                    for (int k = 0; k < CPT; ++k) {
-                        float wf[VEC];
-                        unpack16(wu[i][k], wf);
+                    for (int k = 0; k < CPT; ++k)
 #pragma unroll
-                        for (int tk = 0; tk < B; ++tk)
-#pragma unroll
-                            for (int e = 0; e < VEC; ++e) part[i][tk] = fmaf(xr[tk][k][e], wf[e], part[i][tk]);
-                    }
+                        for (int tk = 0; tk < B; ++tk) part[i][tk] = dot16<T>(wu[i][k], xr[tk][k], part[i][tk]);
                 }
 #pragma unroll
                 for (int i = 0; i < NU; ++i)

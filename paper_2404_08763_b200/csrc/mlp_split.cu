@@ -36,33 +36,6 @@ namespace cats {
 enum : int { kSJobEnd = 0, kSJobGate = 1, kSJobUp = 2 };
 
 // ------------------------------------------------------------------------------ arithmetic helpers
-// acc + sum_e w[e] * x[e] over one 16-byte chunk; products exact, fp32 accumulation in e order
-template <typename T>
-__device__ __forceinline__ float dot16(const uint4 &w, const uint4 &x, float acc);
-template <>
-__device__ __forceinline__ float dot16<bf16_bits>(const uint4 &w, const uint4 &x, float acc) {
-    asm("{\n\t.reg .b16 a0, a1, b0, b1;\n\t"
-        "mov.b32 {a0, a1}, %1;\n\tmov.b32 {b0, b1}, %5;\n\t"
-        "fma.rn.f32.bf16 %0, a0, b0, %0;\n\tfma.rn.f32.bf16 %0, a1, b1, %0;\n\t"
-        "mov.b32 {a0, a1}, %2;\n\tmov.b32 {b0, b1}, %6;\n\t"
-        "fma.rn.f32.bf16 %0, a0, b0, %0;\n\tfma.rn.f32.bf16 %0, a1, b1, %0;\n\t"
-        "mov.b32 {a0, a1}, %3;\n\tmov.b32 {b0, b1}, %7;\n\t"
-        "fma.rn.f32.bf16 %0, a0, b0, %0;\n\tfma.rn.f32.bf16 %0, a1, b1, %0;\n\t"
-        "mov.b32 {a0, a1}, %4;\n\tmov.b32 {b0, b1}, %8;\n\t"
-        "fma.rn.f32.bf16 %0, a0, b0, %0;\n\tfma.rn.f32.bf16 %0, a1, b1, %0;\n\t}"
-        : "+f"(acc)
-        : "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w), "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w));
-    return acc;
-}
-template <>
-__device__ __forceinline__ float dot16<float>(const uint4 &w, const uint4 &x, float acc) {
-    acc = fmaf(__uint_as_float(w.x), __uint_as_float(x.x), acc);
-    acc = fmaf(__uint_as_float(w.y), __uint_as_float(x.y), acc);
-    acc = fmaf(__uint_as_float(w.z), __uint_as_float(x.z), acc);
-    acc = fmaf(__uint_as_float(w.w), __uint_as_float(x.w), acc);
-    return acc;
-}
-
 // Sum a[P] over the 32 lanes of a warp; afterwards lane l holds the warp total of a[l % P].
 // Halving rounds (xor P/2 .. 1): a lane keeps the half selected by its lane bit and adds the
 // partner's copy of it (P - 1 shuffles in all), then xor rounds P .. 16 combine the lane groups.
