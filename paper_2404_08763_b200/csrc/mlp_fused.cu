@@ -492,15 +492,30 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             }
         }
         consumer_barrier<NC>();
+        trace_stamp(trace, 0, 4);  // partial reduced into yacc
         if (tid == 0) s_last = (atomicAdd(&sched[1], 1u) == gridDim.x - 1) ? 1u : 0u;
         consumer_barrier<NC>();
         if (s_last) {
             __threadfence();
             if (mode != kModeGateOnly) {
-                for (int c = tid; c < B * d / 2; c += NC) {
-                    const longlong2 v = __ldcg(reinterpret_cast<const longlong2 *>(yacc) + c);
-                    reinterpret_cast<float2 *>(y)[c] = make_float2(fix_to_float(v.x), fix_to_float(v.y));
-                    reinterpret_cast<longlong2 *>(yacc)[c] = make_longlong2(0, 0);
+                // 8 independent L2 loads in flight per thread (the accumulator was just written by
+                // the bulk-reduce engine of every SM; a serial loop would pay one L2 trip per step)
+                const int n2 = B * d / 2;
+                for (int c0 = 0; c0 < n2; c0 += 8 * NC) {
+                    longlong2 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int c = c0 + u * NC + tid;
+                        v[u] = c < n2 ? __ldcg(reinterpret_cast<const longlong2 *>(yacc) + c) : make_longlong2(0, 0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int c = c0 + u * NC + tid;
+                        if (c < n2) {
+                            reinterpret_cast<float2 *>(y)[c] = make_float2(fix_to_float(v[u].x), fix_to_float(v[u].y));
+                            reinterpret_cast<longlong2 *>(yacc)[c] = make_longlong2(0, 0);
+                        }
+                    }
                 }
             }
             if (tid == 0) {

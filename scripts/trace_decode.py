@@ -59,7 +59,7 @@ torch.cuda.synchronize()
 tr = ws[off.value:off.value + nbytes.value].cpu().numpy().view(np.uint64).reshape(3, 512, 8).astype(np.int64)
 rep = {}
 t0 = None
-names = {0: ["start", "primed", "jobs_done", "exit"], 1: ["start", "list_ready", "jobs_done", "barrier", "exit", "pdl_waited", "prefix_done"]}
+names = {0: ["start", "primed", "jobs_done", "exit", "reduced"], 1: ["start", "list_ready", "jobs_done", "barrier", "exit", "pdl_waited", "prefix_done"]}
 titles = {0: "K12 / KA", 1: "KB"}
 for k in range(2):
     g = int((tr[k, :, 0] > 0).sum())  # CTAs that stamped
