@@ -229,10 +229,18 @@ cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const void *ws, 
                                    uint8_t *tokmask_host, uint32_t *nnz_union, uint32_t *nnz_per_token,
                                    cats_stream_t s);
 
+/* Which kernels a cats_mlp_decode / cats_mlp_dense call with batch b launches on this plan
+ * (DESIGN.md §6): *kernels = 1 for the fused single-kernel path K12 (b = 1, or shapes the split path
+ * does not take), 2 for the split path KA (gate + up) then KB (down + the two-phase reduction).
+ * Errors: CATS_E_NULL, CATS_E_BATCH (b outside [1, max_batch]). Host-only. */
+cats_status_t cats_mlp_kernels_per_call(const cats_mlp_plan_t *plan, int b, int *kernels);
+
 /* Diagnostics. When the environment variable CATS_TRACE=1 is set at plan creation, the kernels
  * record %globaltimer stamps (ns) per CTA into a trace area of the workspace:
  * uint64 trace[3][512 CTAs][8 slots] at byte `offset` (bytes = 0 when tracing is off).
- * [0] K12 slots: 0 start, 1 ring primed, 2 jobs done, 3 exit (after the split-K reduction);
+ * [0] K12 / KA slots: 0 start, 1 ring primed, 2 jobs done, 3 exit, 4 K12 partial reduced;
+ * [1] KB slots: 0 start, 1 list ready, 2 jobs done, 3 barrier passed, 4 exit, 5 masks read,
+ *     6 prefix done;
  * [2] per-CTA producer/consumer statistics (see scripts/trace_decode.py). */
 cats_status_t cats_mlp_trace_info(const cats_mlp_plan_t *plan, size_t *offset, size_t *bytes);
 

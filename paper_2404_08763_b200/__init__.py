@@ -19,7 +19,7 @@ __all__ = [
     "CatsError", "MlpPlan", "cats_calib_rank", "cats_calibrate_workspace_bytes", "cats_calibrate_threshold",
     "cats_calib_window_init", "cats_calib_hist", "cats_calib_step", "cats_mlp_decode", "cats_mlp_dense",
     "cats_mlp_decode_profiled",
-    "cats_mlp_decode_host", "cats_mlp_gate_act", "cats_mlp_last_active", "library_path",
+    "cats_mlp_decode_host", "cats_mlp_gate_act", "cats_mlp_last_active", "cats_mlp_kernels_per_call", "library_path",
 ]
 
 
@@ -246,6 +246,13 @@ def cats_mlp_gate_act(plan: MlpPlan, x, W_gate, acts=None, ws=None, stream=None)
                                      _stream(stream, x.device))
     _check(rc, "cats_mlp_gate_act")
     return acts
+
+
+def cats_mlp_kernels_per_call(plan: MlpPlan, b: int) -> int:
+    """1 = the fused kernel K12, 2 = the split path KA + KB (b >= 2), for a decode of batch b."""
+    n = ctypes.c_int()
+    _check(plan._lib.cats_mlp_kernels_per_call(plan.handle, int(b), ctypes.byref(n)), "cats_mlp_kernels_per_call")
+    return n.value
 
 
 def cats_mlp_last_active(plan: MlpPlan, ws: torch.Tensor, b: int, stream=None):

@@ -60,6 +60,7 @@ _SIGS = {
     "cats_mlp_gate_act": (I, [P, P, I, P, P, P, SZ, P]),
     "cats_mlp_last_active": (I, [P, P, I, P, P, P, P, P]),
     "cats_mlp_trace_info": (I, [P, P, P]),
+    "cats_mlp_kernels_per_call": (I, [P, I, P]),
 }
 
 

@@ -555,6 +555,13 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
     })
 }
 
+extern "C" cats_status_t cats_mlp_kernels_per_call(const cats_mlp_plan_t *plan, int b, int *kernels) {
+    if (!plan || !kernels) return CATS_E_NULL;
+    if (b < 1 || b > plan->p.max_batch) return CATS_E_BATCH;
+    *kernels = (b >= plan->p.split_min_b && split_supported(plan->p, b)) ? 2 : 1;
+    return CATS_OK;
+}
+
 extern "C" cats_status_t cats_mlp_trace_info(const cats_mlp_plan_t *plan, size_t *offset, size_t *bytes) {
     if (!plan || !offset || !bytes) return CATS_E_NULL;
     *offset = plan->p.off_trace;

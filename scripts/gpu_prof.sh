@@ -7,7 +7,7 @@ CMD="python scripts/prof_decode.py --steps 8 --dense ${PROF_ARGS}"
 timeout 300 $CMD > gpurun_out/prof_plain.log 2>&1 || { echo "plain run failed"; cat gpurun_out/prof_plain.log; exit 1; }
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
    --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/ncu_list.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k12_|k3_" -s 20 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k12_" -s 10 -c 2 \
    -o gpurun_out/${TAG}_prof -f $CMD > gpurun_out/ncu_full.log 2>&1
 # read-bandwidth ceilings with torch (context): sum (read-only) and copy of 4 GiB
 timeout 120 python - > gpurun_out/membw.log 2>&1 <<'PY'

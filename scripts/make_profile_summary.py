@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--rep")
     ap.add_argument("--launches")
     ap.add_argument("--bench")
+    ap.add_argument("--extra", nargs="*", default=[],
+                    help="label::path.ncu-rep of further full-set captures (e.g. the b>=2 split path)")
     a = ap.parse_args()
     rep = a.rep or os.path.join(ROOT, "gpurun_out", f"{a.tag}_prof.ncu-rep")
     lau = a.launches or os.path.join(ROOT, "gpurun_out", f"{a.tag}_launches.csv")
@@ -82,6 +84,25 @@ def main():
                 traffic["K12"] = statistics.median(x["dram__bytes_read.sum"] + x["dram__bytes_write.sum"] for x in dec)
                 lines.append(f"K12 CATS-decode launches: {len(dec)}, median DRAM traffic {traffic['K12'] / 1e6:.2f} MB "
                              f"per launch, median time {statistics.median(x['gpu__time_duration.sum'] for x in dec) / 1e3:.2f} us")
+        lines.append("")
+    for item in a.extra:
+        label, path = item.split("::", 1)
+        if not os.path.exists(path):
+            continue
+        data = ncu_summary.raw(path)
+        lines += [f"## Full-set capture: {label}", "",
+                  "| kernel | duration | DRAM read | DRAM write | regs | dyn smem | grid x block | top stalls |",
+                  "|---|---|---|---|---|---|---|---|"]
+        for d in data:
+            lines.append(f"| `{d['kernel']}` | {d.get('dur')} {d.get('dur_unit')} | {d.get('dram_rd')} "
+                         f"{d.get('dram_rd_unit')} | {d.get('dram_wr')} {d.get('dram_wr_unit')} | {d.get('regs')} | "
+                         f"{d.get('dyn_smem')} {d.get('dyn_smem_unit')} | {d.get('grid')} x {d.get('block')} | "
+                         f"{', '.join(f'{n} {v}' for v, n in d['stalls'][:4])} |")
+            name = "KA" if "ka_gate_up" in d["kernel"] else "KB" if "kb_down" in d["kernel"] else None
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            if name and "b=2" in label and isinstance(d.get("dram_rd"), float):
+                traffic[f"{name}_b2"] = d["dram_rd"] * scale.get(d.get("dram_rd_unit"), 1) + \
+                    d["dram_wr"] * scale.get(d.get("dram_wr_unit"), 1)
         lines.append("")
     if a.bench and os.path.exists(a.bench):
         for ln in open(a.bench):

@@ -212,3 +212,17 @@ def test_host_select_nonfinite():
     with pytest.raises(cats.CatsError) as e:
         emulated_calibrate(acts, 0.5)
     assert e.value.name == "CATS_E_NONFINITE"
+
+
+def test_kernels_per_call_path_choice():
+    """b = 1 runs the fused K12 (one kernel); b >= 2 the split path KA + KB where it fits shared memory."""
+    p = cats.MlpPlan(4096, 11008, max_batch=8, dtype=torch.bfloat16, num_sms=148)
+    assert cats.cats_mlp_kernels_per_call(p, 1) == 1
+    assert [cats.cats_mlp_kernels_per_call(p, b) for b in range(2, 9)] == [2] * 7
+    toy = cats.MlpPlan(64, 176, max_batch=3, dtype=torch.float32, num_sms=148)
+    assert cats.cats_mlp_kernels_per_call(toy, 3) == 2
+    wide = cats.MlpPlan(8192, 512, max_batch=8, dtype=torch.bfloat16, num_sms=148)
+    assert cats.cats_mlp_kernels_per_call(wide, 8) == 1  # x alone would take 128 KB of KA's shared memory
+    with pytest.raises(cats.CatsError) as e:
+        cats.cats_mlp_kernels_per_call(p, 9)
+    assert e.value.name == "CATS_E_BATCH"
