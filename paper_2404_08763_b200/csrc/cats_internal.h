@@ -87,20 +87,30 @@ struct SplitFifoEntry {  // one active neuron waiting for its UP job
     float v[B];
 };
 
-inline int split_q(int) { return 2; }  // KB column parts (halves the partials; bounds y registers per thread)
-inline int split_ept(const PlanData &, int) { return 4; }  // KB columns per thread (16 B fp32, 8 B bf16)
-inline int split_part_cols(const PlanData &p, int b) { return p.d / split_q(b); }
+// KB on tensor cores (bf16, d a multiple of 1024: 4 column parts of 16-column tiles over 16 warps)
+constexpr int kSplitMmaMinB = 4;  // batches from which KA / KB use warp-level bf16 MMA (measured crossover)
+inline bool split_kb_mma(const PlanData &p, int b) {  // instantiated for 1, 4, 5 tiles per warp
+    return b >= kSplitMmaMinB && p.esize == 2 && (p.d == 1024 || p.d == 4096 || p.d == 5120);
+}
+inline int split_q(const PlanData &p, int b) { return split_kb_mma(p, b) ? 4 : 2; }  // KB column parts
+inline int split_ept(const PlanData &, int) { return 4; }  // KB (FFMA path) columns per thread
+inline int split_part_cols(const PlanData &p, int b) { return p.d / split_q(p, b); }
+inline int split_kb_mt(const PlanData &p, int b) {  // 16-column MMA tiles per KB warp (0 = FFMA path)
+    return split_kb_mma(p, b) ? split_part_cols(p, b) / (16 * 16) : 0;
+}
 inline int split_kb_consumers(const PlanData &p, int b) {
+    if (split_kb_mma(p, b)) return 16 * 32;
     const int c = (split_part_cols(p, b) + split_ept(p, b) - 1) / split_ept(p, b);
     return (c + 31) / 32 * 32;
 }
 inline int split_ranges(const PlanData &p, int b) {  // R: static ranges of the active list
-    return std::max(1, std::min(p.num_sms / split_q(b), p.m / 8));
+    return std::max(1, std::min(p.num_sms / split_q(p, b), p.m / 8));
 }
-inline int split_kb_grid(const PlanData &p, int b) { return split_ranges(p, b) * split_q(b); }
+inline int split_kb_grid(const PlanData &p, int b) { return split_ranges(p, b) * split_q(p, b); }
 inline int split_ka_grid(const PlanData &p, int b) {
     return std::max(1, std::min(p.num_sms, (k12_ntiles(p, b) + kSplitAGroups - 1) / kSplitAGroups));
 }
+int split_ka_ks(const PlanData &p, int b);
 size_t split_ka_smem(const PlanData &p, int b, int stages);
 size_t split_kb_smem(const PlanData &p, int b, int stages);
 int split_ka_stages(const PlanData &p, int b);

@@ -28,6 +28,8 @@
 //
 // KA -> KB -> next decode run as programmatic dependent launches: a kernel's CTAs become resident
 // while its predecessor drains and wait (griddepcontrol.wait) only before touching its outputs.
+#include <cuda_bf16.h>
+
 #include "cats_device.cuh"
 #include "cats_internal.h"
 
@@ -60,6 +62,27 @@ __device__ __forceinline__ float warp_reduce_scatter(float (&a)[P], int lane) {
 
 constexpr int pow2_ceil(int v) { return v <= 1 ? 1 : 2 * pow2_ceil((v + 1) / 2); }
 
+// warp-level bf16 MMA, fp32 accumulate (D += A B), m16n8k16, A row-major, B column-major
+__device__ __forceinline__ void mma_bf16_16816(float (&dd)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+                 "{%8, %9}, {%0, %1, %2, %3};"
+                 : "+f"(dd[0]), "+f"(dd[1]), "+f"(dd[2]), "+f"(dd[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t saddr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(saddr)
+                 : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t saddr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(saddr)
+                 : "memory");
+}
+
 __device__ __forceinline__ void claim_async(unsigned int &t, unsigned int *ctr, bool pred) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p atom.global.add.u32 %0, [%1], 1;\n\t}"
                  : "+r"(t)
@@ -69,7 +92,7 @@ __device__ __forceinline__ void claim_async(unsigned int &t, unsigned int *ctr, 
 constexpr unsigned int kNoTileS = 0xffffffffu;
 
 // ======================================================================================== KA
-template <typename T, int B, int NR>
+template <typename T, int B, int NR, int KS>
 __global__ void __launch_bounds__(kSplitAThreads, 1)
 ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restrict__ Wu, int d, int m, int stages,
            float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask, float *__restrict__ vals,
@@ -91,13 +114,16 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
     const int g = warp < NW ? warp / NWG : warp - NW;  // this warp's group
     const int nch = d * (int)sizeof(T) / 16;
     const uint32_t row_bytes = (uint32_t)d * (uint32_t)sizeof(T);
-    const uint32_t stage_bytes = (uint32_t)NR * row_bytes;
+    // stage rows are padded by 16 B: the NR rows of a stage start in different shared-memory bank
+    // groups (conflict-free ldmatrix) and the zeroed pad absorbs a half 16-wide k-step at the row end
+    const uint32_t rs_bytes = row_bytes + 16u;
+    const uint32_t stage_bytes = (uint32_t)NR * rs_bytes;
     const int ntiles = (m + NR - 1) / NR;
 
     // shared memory: x, then per group: ring, barriers, descriptors, FIFO, partial sums
     extern __shared__ __align__(128) unsigned char smem[];
-    unsigned char *xs = smem;                                                             // [B][d] x
-    unsigned char *ring0 = xs + (size_t)B * row_bytes;                                    // [NG][stages][stage]
+    unsigned char *xs = smem;  // x: [B][d] (dot-product path) or [B][d + 8] (tensor-core path, padded rows)
+    unsigned char *ring0 = xs + (size_t)B * (KS > 0 ? row_bytes + 16u : row_bytes);       // [NG][stages][stage]
     uint64_t *full0 = reinterpret_cast<uint64_t *>(ring0 + (size_t)NG * stages * stage_bytes);  // [NG][stages]
     uint64_t *empty0 = full0 + NG * stages;                                               // [NG][stages]
     Desc *desc0 = reinterpret_cast<Desc *>(empty0 + NG * stages);                         // [NG][stages]
@@ -119,6 +145,8 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
         }
         fence_mbar_init();
     }
+    for (int i = tid; i < NG * stages * NR; i += blockDim.x)  // row pads (never written by copies)
+        *reinterpret_cast<uint4 *>(ring0 + (size_t)i * rs_bytes + row_bytes) = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
 
     if (warp >= NW) {
@@ -153,7 +181,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
             }
             __syncwarp();
             if (lane < n)
-                bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)lane * row_bytes, Wu + (size_t)D.id[lane] * d,
+                bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)lane * rs_bytes, Wu + (size_t)D.id[lane] * d,
                          row_bytes, &full[s], policy);
             q_head += n;
         };
@@ -203,9 +231,11 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
                         desc[s].tile = (int)tile;
                         desc[s].n = nr;
                         mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
-                        bulk_g2s(ring + (size_t)s * stage_bytes, Wg + (size_t)r0 * d, (uint32_t)nr * row_bytes,
-                                 &full[s], policy);
                     }
+                    __syncwarp();
+                    if (lane < nr)  // one copy per (padded) row
+                        bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)lane * rs_bytes,
+                                 Wg + (size_t)(r0 + lane) * d, row_bytes, &full[s], policy);
                     ++gates_inflight;
                 } else {
                     if (qn > 0) {
@@ -239,8 +269,9 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
                 desc[s].tile = (int)(base + s);
                 desc[s].n = nr;
                 mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
-                bulk_g2s(ring + (size_t)s * stage_bytes, Wg + (size_t)r0 * d, (uint32_t)nr * row_bytes, &full[s],
-                         policy);
+                for (int r = 0; r < nr; ++r)
+                    bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)r * rs_bytes, Wg + (size_t)(r0 + r) * d,
+                             row_bytes, &full[s], policy);
             }
         }
         prod = __shfl_sync(0xffffffffu, prod, 0);
@@ -329,6 +360,58 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
     } else {
         // ===================================== CONSUMER WARPS ====================================
         pdl_wait_primary();  // x may come from the predecessor
+        const int ctid = tid - g * NCG;  // consumer thread index within the group
+        const int cwarp = warp - g * NWG;
+        int s = 0;
+        uint32_t phase = 0;
+        unsigned long long c_wait = 0;
+        if constexpr (KS > 0) {
+            // ---- tensor-core dot products (bf16): D[16 x 8] += A[16 x 16] B[16 x 8] per 16-wide k-step,
+            //      A = x (rows = tokens; rows >= b repeat token 0 and are ignored), B = W^T (columns =
+            //      the job's NR rows; the other 8 - NR columns repeat them and are ignored). Warp w of the
+            //      group owns k-steps [w*spw, (w+1)*spw). Both operands come from shared memory with
+            //      ldmatrix (x rows and stage rows padded by 16 B: conflict-free). ----
+            {
+                const uint4 *xg = reinterpret_cast<const uint4 *>(x);
+                const uint32_t xrs = row_bytes + 16u;
+                for (int i = tid; i < B * nch; i += NC)
+                    *reinterpret_cast<uint4 *>(xs + (size_t)(i / nch) * xrs + (size_t)(i % nch) * 16) = xg[i];
+                if (tid < B) *reinterpret_cast<uint4 *>(xs + (size_t)tid * xrs + row_bytes) = make_uint4(0u, 0u, 0u, 0u);
+            }
+            consumer_barrier<NC>();
+            const int g4 = lane >> 2, t4 = lane & 3;
+            const int nsteps = (d + 15) / 16;
+            const int spw = (nsteps + NWG - 1) / NWG;
+            const int j0 = cwarp * spw, j1 = min(nsteps, j0 + spw);
+            // ldmatrix.x4 row addresses: lane i -> matrix i/8 (k offset 8*(i/8)), row i%8
+            const uint32_t koff = (uint32_t)(lane >> 3) * 16u + (uint32_t)j0 * 32u;
+            const uint32_t arow = smem_u32(xs) + (uint32_t)((lane & 7) < B ? (lane & 7) : 0) * (row_bytes + 16u) + koff;
+            const uint32_t brow = (uint32_t)((lane & 7) % NR) * rs_bytes + koff;
+            for (;;) {
+                const unsigned long long cw0 = trace ? gtimer() : 0ull;
+                mbar_wait(&full[s], phase);
+                if (trace) c_wait += gtimer() - cw0;
+                if (desc[s].type == kSJobEnd) break;
+                const uint32_t sb = smem_u32(ring + (size_t)s * stage_bytes) + brow;
+                float dacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+                for (int j = j0; j < j1; j += 2) {
+                    const uint32_t o = (uint32_t)(j - j0) * 32u;
+                    uint32_t a0, a2, a4, a6, b0, b1, b2, b3;
+                    ldsm_x4(arow + o, a0, a2, a4, a6);  // steps j (a0, a2) and j + 1 (a4, a6)
+                    ldsm_x4(sb + o, b0, b1, b2, b3);    // steps j (b0, b1) and j + 1 (b2, b3)
+                    mma_bf16_16816(dacc, a0, a0, a2, a2, b0, b1);  // rows 8..15 of A: ignored copies
+                    if (j + 1 < j1) mma_bf16_16816(dacc, a4, a4, a6, a6, b2, b3);
+                }
+                // lane (g4, t4) holds D[token g4][row 2 t4] and D[g4][2 t4 + 1]
+                float *rb = red + ((size_t)s * NWG + cwarp) * PP;
+                if (g4 < B && 2 * t4 < NR) rb[(2 * t4) * B + g4] = dacc[0];
+                if (g4 < B && 2 * t4 + 1 < NR) rb[(2 * t4 + 1) * B + g4] = dacc[1];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                if (++s == stages) { s = 0; phase ^= 1u; }
+            }
+        } else {
         {
             const uint4 *xg = reinterpret_cast<const uint4 *>(x);
             uint4 *xd = reinterpret_cast<uint4 *>(xs);
@@ -336,11 +419,6 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
         }
         consumer_barrier<NC>();
         const uint32_t xbase = smem_u32(xs);
-        const int ctid = tid - g * NCG;  // consumer thread index within the group
-        const int cwarp = warp - g * NWG;
-        int s = 0;
-        uint32_t phase = 0;
-        unsigned long long c_wait = 0;
         for (;;) {
             const unsigned long long cw0 = trace ? gtimer() : 0ull;
             mbar_wait(&full[s], phase);
@@ -359,7 +437,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
                 // anyway (no branches) and ignored by the producer
 #pragma unroll
                 for (int r = 0; r < NR; ++r) {
-                    const uint4 w = lds128(sbase + (uint32_t)r * row_bytes + (uint32_t)ch * 16u);
+                    const uint4 w = lds128(sbase + (uint32_t)r * rs_bytes + (uint32_t)ch * 16u);
 #pragma unroll
                     for (int tk = 0; tk < B; ++tk) acc[r * B + tk] = dot16<T>(w, xv[tk], acc[r * B + tk]);
                 }
@@ -369,6 +447,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
             if (++s == stages) { s = 0; phase ^= 1u; }
+        }
         }
         if (tid == 0) trace_put(trace, 2, 3, c_wait);
     }
@@ -383,7 +462,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
 }
 
 // ======================================================================================== KB
-template <typename T, int B, int EPT>
+template <typename T, int B, int EPT, int MT>
 __global__ void __launch_bounds__(kSplitBMaxThreads, 1)
 kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, int stages, int rows_per_stage,
         int maxr, unsigned int *__restrict__ tmask, const float *__restrict__ x1in, float *__restrict__ part,
@@ -394,7 +473,8 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     const int rr = blockIdx.x / Q, q = blockIdx.x % Q;
     const int part_cols = d / Q;
     const uint32_t seg_bytes = (uint32_t)part_cols * (uint32_t)sizeof(T);
-    const uint32_t stage_bytes = (uint32_t)rows_per_stage * seg_bytes;
+    const uint32_t sst = seg_bytes + 16u;  // stage row stride (padded: conflict-free ldmatrix)
+    const uint32_t stage_bytes = (uint32_t)rows_per_stage * sst;
 
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char *ring = smem;                                                               // [stages][stage]
@@ -505,7 +585,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
             if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)nrow * seg_bytes);
             __syncwarp();
             if (lane < nrow)
-                bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)lane * seg_bytes,
+                bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)lane * sst,
                          Wd + (size_t)lj[r0 + lane] * d + (size_t)q * part_cols, seg_bytes, &full[s], policy);
         }
     } else {
@@ -513,6 +593,64 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
         pdl_wait_primary();  // x1 comes from KA's UP jobs: KA must have completed
         for (int i = tid; i < len * B; i += NCt) lx[i] = __ldcg(x1in + (size_t)lpos[i / B] * B + (i % B));
         asm volatile("bar.sync 1, %0;" ::"r"(NCt) : "memory");  // consumers only
+        if constexpr (MT > 0) {
+            // ---- tensor cores (bf16): D[16 cols x 8 tokens] += A[16 cols x 16 neurons] B[16 neurons x 8]
+            //      A = W_down^T from the stage (ldmatrix .trans), B = x1 split exactly enough into
+            //      bf16 hi + lo (two MMAs; |x1 - hi - lo| <= 2^-16 |x1|). Warp w owns MT 16-column
+            //      tiles; 16 neurons (one stage) per k-step, in list order: deterministic. ----
+            const int g4 = lane >> 2, t4 = lane & 3;
+            const int col0 = warp * MT * 16;  // within the part
+            float dacc[MT][4];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) dacc[mt][e] = 0.f;
+            const int mat = lane >> 3, r8 = lane & 7;
+            for (int jn = 0; jn < njobs; ++jn) {
+                const int s = jn % stages;
+                mbar_wait(&full[s], (uint32_t)(jn / stages) & 1u);
+                const int r0 = jn * rows_per_stage, nrow = min(rows_per_stage, len - r0);
+                // B fragments: x1 of neurons 2 t4, 2 t4 + 1 (b0) and 2 t4 + 8, + 9 (b1), token g4
+                uint32_t bh[2], bl[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    float v[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int rr2 = 2 * t4 + 8 * h + e;
+                        v[e] = (g4 < B && rr2 < nrow) ? lx[(size_t)(r0 + rr2) * B + g4] : 0.f;
+                    }
+                    const __nv_bfloat162 hi = __floats2bfloat162_rn(v[0], v[1]);
+                    const float2 hf = __bfloat1622float2(hi);
+                    const __nv_bfloat162 lo = __floats2bfloat162_rn(v[0] - hf.x, v[1] - hf.y);
+                    bh[h] = *reinterpret_cast<const uint32_t *>(&hi);
+                    bl[h] = *reinterpret_cast<const uint32_t *>(&lo);
+                }
+                // A: lane -> neuron row r8 + 8 (mat / 2) (rows past nrow repeat row 0: finite, x1 = 0),
+                //    columns + 8 (mat % 2)
+                const int arow = r8 + 8 * (mat >> 1);
+                const uint32_t abase = smem_u32(ring + (size_t)s * stage_bytes) + (uint32_t)(arow < nrow ? arow : 0) * sst +
+                                       (uint32_t)(col0 + 8 * (mat & 1)) * 2u;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4_trans(abase + (uint32_t)mt * 32u, a0, a1, a2, a3);
+                    mma_bf16_16816(dacc[mt], a0, a1, a2, a3, bh[0], bh[1]);
+                    mma_bf16_16816(dacc[mt], a0, a1, a2, a3, bl[0], bl[1]);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
+            // lane (g4, t4): D[col g4 (+8)][token 2 t4 (+1)]
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int c = col0 + mt * 16 + g4 + 8 * (e >> 1), tk = 2 * t4 + (e & 1);
+                    if (tk < B) part[((size_t)rr * B + tk) * d + (size_t)q * part_cols + c] = dacc[mt][e];
+                }
+            }
+        } else {
         const int c0 = tid * EPT;  // first column of this thread within the part
         const bool own = c0 < part_cols;
         float acc[B][EPT];
@@ -529,10 +667,10 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
                 for (int i = 0; i < nrow; ++i) {
                     float wf[EPT];
                     if constexpr (EB == 16) {
-                        unpack16(lds128(sb + (uint32_t)i * seg_bytes), wf);
+                        unpack16(lds128(sb + (uint32_t)i * sst), wf);
                     } else {  // 8 bytes = 4 bf16
                         uint32_t w0, w1;
-                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "r"(sb + (uint32_t)i * seg_bytes));
+                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "r"(sb + (uint32_t)i * sst));
                         wf[0] = __uint_as_float(w0 << 16);
                         wf[1] = __uint_as_float(w0 & 0xffff0000u);
                         wf[2] = __uint_as_float(w1 << 16);
@@ -558,6 +696,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
                 for (int e = 0; e < EPT; e += 4)
                     *reinterpret_cast<float4 *>(dst + e) = make_float4(acc[tk][e], acc[tk][e + 1], acc[tk][e + 2], acc[tk][e + 3]);
             }
+        }
         }
     }
     trace_stamp(trace, 1, 2);
@@ -635,16 +774,23 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
 }
 
 // ================================================================================== host side
-// KA shared memory: x [b][d], then per group (kSplitAGroups): the ring, 2 mbarriers, a descriptor and
-// the warp partial sums per stage, and the FIFO. `stages` counts stages per group.
+// KA dot-product engine: 1 = warp-level bf16 MMA (bf16 weights, b >= kSplitMmaMinB), 0 = FHFMA.BF16 / FFMA.
+// Measured (Llama2-7B): the MMA path wins from b = 4 (b = 8: KA 58 -> 38 us); at b = 2 its ldmatrix
+// traffic (x re-read per job, half the B columns duplicated) makes it slower than FHFMA.
+int split_ka_ks(const PlanData &p, int b) { return (p.esize == 2 && b >= kSplitMmaMinB) ? 1 : 0; }
+// KA shared memory: x [b][d] (FHFMA path only), then per group (kSplitAGroups): the ring of padded
+// rows, 2 mbarriers, a descriptor and the warp partial sums per stage, and the FIFO. `stages` counts
+// stages per group.
 static size_t split_ka_per_stage(const PlanData &p, int b) {
     const int nr = k12_rows_per_tile(p, b);
     const size_t desc = (3 + 2 * (size_t)nr + (size_t)nr * b) * 4;  // sizeof(SplitDesc<nr, b>)
-    return (size_t)nr * p.d * p.esize + 16 + desc + (size_t)(kSplitAWarps / kSplitAGroups) * pow2_ceil(nr * b) * 4;
+    return (size_t)nr * ((size_t)p.d * p.esize + 16) + 16 + desc +
+           (size_t)(kSplitAWarps / kSplitAGroups) * pow2_ceil(nr * b) * 4;
 }
 size_t split_ka_smem(const PlanData &p, int b, int stages) {
     const size_t ent = (2 + (size_t)b) * 4;  // sizeof(SplitFifoEntry<b>)
-    return (size_t)b * p.d * p.esize + kSplitAGroups * ((size_t)stages * split_ka_per_stage(p, b) + kSplitFifo * ent);
+    const size_t xs = (size_t)b * ((size_t)p.d * p.esize + (split_ka_ks(p, b) > 0 ? 16 : 0));
+    return xs + kSplitAGroups * ((size_t)stages * split_ka_per_stage(p, b) + kSplitFifo * ent);
 }
 int split_ka_stages(const PlanData &p, int b) {
     const size_t fixed = split_ka_smem(p, b, 0);
@@ -652,6 +798,7 @@ int split_ka_stages(const PlanData &p, int b) {
     return (int)std::min<size_t>((kSmemBudget - fixed) / (kSplitAGroups * split_ka_per_stage(p, b)), kMaxStages);
 }
 static int split_kb_rows_per_stage(const PlanData &p, int b) {
+    if (split_kb_mma(p, b)) return 16;  // one 16-neuron MMA k-step per stage
     const size_t seg = (size_t)split_part_cols(p, b) * p.esize;
     return (int)std::max<size_t>(1, std::min<size_t>(32, (32 * 1024) / seg));
 }
@@ -660,7 +807,7 @@ static int split_kb_maxr(const PlanData &p, int b) {
     return (p.m + R - 1) / R + 1;
 }
 size_t split_kb_smem(const PlanData &p, int b, int stages) {
-    const size_t seg = (size_t)split_part_cols(p, b) * p.esize;
+    const size_t seg = (size_t)split_part_cols(p, b) * p.esize + 16;  // padded rows
     const size_t stage = (size_t)split_kb_rows_per_stage(p, b) * seg;
     const int ntiles = k12_ntiles(p, b);
     const int maxr = split_kb_maxr(p, b);
@@ -668,7 +815,7 @@ size_t split_kb_smem(const PlanData &p, int b, int stages) {
            (size_t)maxr * b * 4 + (size_t)ntiles;
 }
 int split_kb_stages(const PlanData &p, int b) {
-    const size_t seg = (size_t)split_part_cols(p, b) * p.esize;
+    const size_t seg = (size_t)split_part_cols(p, b) * p.esize + 16;  // padded rows
     const size_t stage = (size_t)split_kb_rows_per_stage(p, b) * seg;
     const size_t fixed = split_kb_smem(p, b, 0);
     if (fixed >= kSmemBudget) return 0;
@@ -679,7 +826,7 @@ int split_kb_stages(const PlanData &p, int b) {
 }
 bool split_supported(const PlanData &p, int b) {
     if (b < 2 || b > 8) return false;
-    if (p.d % (split_q(b) * split_ept(p, b)) != 0) return false;
+    if (p.d % (split_q(p, b) * split_ept(p, b)) != 0) return false;
     if (((size_t)split_part_cols(p, b) * p.esize) % 16 != 0) return false;
     if (split_kb_consumers(p, b) + 32 > kSplitBMaxThreads) return false;
     const int sa = split_ka_stages(p, b), sb = split_kb_stages(p, b);
@@ -702,12 +849,12 @@ static cudaLaunchConfig_t pdl_config(cudaLaunchAttribute *attr, int grid, int th
     return cfg;
 }
 
-template <typename T, int B, int NR>
+template <typename T, int B, int NR, int KS>
 static cudaError_t launch_ka(const PlanData &p, const void *x, const void *Wg, const void *Wu, float t, int mode,
                              void *ws, cudaStream_t s) {
     static_assert(sizeof(SplitDesc<NR, B>) == (3 + 2 * NR + NR * B) * 4, "split_ka_smem layout");
     static_assert(sizeof(SplitFifoEntry<B>) == (2 + B) * 4, "split_ka_smem layout");
-    auto kern = ka_gate_up<T, B, NR>;
+    auto kern = ka_gate_up<T, B, NR, KS>;
     const int stages = split_ka_stages(p, B);
     const size_t smem = split_ka_smem(p, B, stages);
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
@@ -725,9 +872,9 @@ static cudaError_t launch_ka(const PlanData &p, const void *x, const void *Wg, c
                               p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
 }
 
-template <typename T, int B, int EPT>
+template <typename T, int B, int EPT, int MT>
 static cudaError_t launch_kb(const PlanData &p, const void *Wd, float *y, void *ws, cudaStream_t s) {
-    auto kern = kb_down<T, B, EPT>;
+    auto kern = kb_down<T, B, EPT, MT>;
     const int stages = split_kb_stages(p, B);
     const size_t smem = split_kb_smem(p, B, stages);
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
@@ -737,7 +884,7 @@ static cudaError_t launch_kb(const PlanData &p, const void *Wd, float *y, void *
     const int threads = split_kb_consumers(p, B) + 32;
     cudaLaunchConfig_t cfg = pdl_config(attr, split_kb_grid(p, B), threads, smem, s);
     return cudaLaunchKernelEx(&cfg, kern, static_cast<const T *>(Wd), p.d, k12_ntiles(p, B), k12_rows_per_tile(p, B),
-                              split_q(B), split_ranges(p, B), stages, split_kb_rows_per_stage(p, B),
+                              split_q(p, B), split_ranges(p, B), stages, split_kb_rows_per_stage(p, B),
                               split_kb_maxr(p, B), reinterpret_cast<unsigned int *>(w + p.off_tmask),
                               reinterpret_cast<const float *>(w + p.off_x1), reinterpret_cast<float *>(w + p.off_part), y,
                               reinterpret_cast<unsigned int *>(w + p.off_sched),
@@ -747,15 +894,30 @@ static cudaError_t launch_kb(const PlanData &p, const void *Wd, float *y, void *
 template <typename T, int B>
 static cudaError_t launch_split_b(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
                                   float t, int mode, float *y, void *ws, cudaStream_t s, cudaEvent_t ev_mid) {
-    cudaError_t e = k12_rows_per_tile(p, B) == 4 ? launch_ka<T, B, 4>(p, x, Wg, Wu, t, mode, ws, s)
-                                                 : launch_ka<T, B, 2>(p, x, Wg, Wu, t, mode, ws, s);
+    cudaError_t e;
+    const int ks = split_ka_ks(p, B);
+    if constexpr (sizeof(T) == 2 && B >= kSplitMmaMinB) {
+        (void)ks;
+        e = k12_rows_per_tile(p, B) == 4 ? launch_ka<T, B, 4, 1>(p, x, Wg, Wu, t, mode, ws, s)
+                                         : launch_ka<T, B, 2, 1>(p, x, Wg, Wu, t, mode, ws, s);
+    } else {
+        e = k12_rows_per_tile(p, B) == 4 ? launch_ka<T, B, 4, 0>(p, x, Wg, Wu, t, mode, ws, s)
+                                         : launch_ka<T, B, 2, 0>(p, x, Wg, Wu, t, mode, ws, s);
+    }
     if (e != cudaSuccess) return e;
     if (ev_mid) {
         e = cudaEventRecord(ev_mid, s);
         if (e != cudaSuccess) return e;
     }
     constexpr int EPT = 4;  // = split_ept()
-    return launch_kb<T, B, EPT>(p, Wd, y, ws, s);
+    if constexpr (sizeof(T) == 2 && B >= kSplitMmaMinB) {
+        const int mt = split_kb_mt(p, B);
+        if (mt == 1) return launch_kb<T, B, EPT, 1>(p, Wd, y, ws, s);
+        if (mt == 4) return launch_kb<T, B, EPT, 4>(p, Wd, y, ws, s);
+        if (mt == 5) return launch_kb<T, B, EPT, 5>(p, Wd, y, ws, s);
+        if (mt != 0) return cudaErrorInvalidValue;
+    }
+    return launch_kb<T, B, EPT, 0>(p, Wd, y, ws, s);
 }
 
 template <typename T>

@@ -65,15 +65,26 @@ def emit(**kw):
     print(json.dumps(kw), flush=True)
 
 
+_STACKS = {}
+
+
+def weights(d, m, layers, copies, heavy, dtype):
+    """Device weight list (cached across b / k: generating a 32-layer stack on the host is slow)."""
+    key = (d, m, layers, copies, heavy, dtype)
+    if key not in _STACKS:
+        _STACKS.clear()
+        torch.cuda.empty_cache()
+        Ws = [[w.to(dev) for w in cats_synth.mlp_weights(d, m, dtype, layer=l, heavy=heavy)] for l in range(layers)]
+        if copies > 1:  # rotated copies of a single layer (defeat L2)
+            Ws = Ws + [[w.clone() for w in Ws[0]] for _ in range(copies - 1)]
+        _STACKS[key] = Ws
+    return _STACKS[key]
+
+
 def run_layers(name, d, m, layers, copies, b, k, heavy, dtype=torch.bfloat16, dense_too=False):
     plan = cats.MlpPlan(d, m, max_batch=8, dtype=dtype)
     ws = plan.workspace()
-    Ws = []
-    for l in range(layers):
-        W = [w.to(dev) for w in cats_synth.mlp_weights(d, m, dtype, layer=l, heavy=heavy)]
-        Ws.append(W)
-    if copies > 1:  # rotated copies of a single layer (defeat L2)
-        Ws = Ws + [[w.clone() for w in Ws[0]] for _ in range(copies - 1)]
+    Ws = weights(d, m, layers, copies, heavy, dtype)
     ts = [calibrate(plan, ws, W[0], d, k, dtype, seed=100 + l, heavy=heavy) if k > 0 else 0.0
           for l, W in enumerate(Ws[:layers])]
     ts = ts + [ts[0]] * (len(Ws) - len(ts))
@@ -95,7 +106,8 @@ def run_layers(name, d, m, layers, copies, b, k, heavy, dtype=torch.bfloat16, de
     eff = eff * esz // 2
     rec = dict(config=name, d=d, m=m, b=b, k=k, heavy=heavy, layers=n, us_per_token_layer=round(us / b, 3),
                us_per_step=round(us, 3), union_active=U, union_frac=round(U / m, 4),
-               per_token_sparsity=round(1 - float(per.mean()) / m, 4), eff_GBps=round(eff / (us * 1e-6) / 1e9, 1))
+               per_token_sparsity=round(1 - float(per.mean()) / m, 4), eff_GBps=round(eff / (us * 1e-6) / 1e9, 1),
+               kernels_per_call=cats.cats_mlp_kernels_per_call(plan, b))
     if dense_too:
         def fd():
             for W in Ws:
@@ -104,8 +116,6 @@ def run_layers(name, d, m, layers, copies, b, k, heavy, dtype=torch.bfloat16, de
         rec.update(dense_us_per_step=round(ud, 3), speedup_vs_dense=round(ud / us, 4),
                    dense_GBps=round(3 * 2 * d * m * esz // 2 / (ud * 1e-6) / 1e9, 1))
     emit(**rec)
-    del Ws
-    torch.cuda.empty_cache()
 
 
 run_layers("C0-toy", 64, 176, 1, 1, 1, 0.5, False, dtype=torch.float32, dense_too=True)
