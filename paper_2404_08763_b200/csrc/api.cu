@@ -355,6 +355,8 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.off_x1 = off;      off = align_up(off + x1_bytes, 256);
         p.off_tmask = off;   off = align_up(off + (size_t)((m + 1) / 2) * 4, 256);
         p.off_part = off;    off = align_up(off + part_bytes, 256);
+        const char *ks = std::getenv("CATS_K12_STAGES");
+        p.k12_max_stages = ks ? std::max(2, std::atoi(ks)) : 0;
         const char *tr = std::getenv("CATS_TRACE");
         p.trace = tr && tr[0] == '1';
         const char *lt = std::getenv("CATS_LAZY_TAIL");

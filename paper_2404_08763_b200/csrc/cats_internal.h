@@ -40,6 +40,7 @@ struct PlanData {
     bool trace;         // CATS_TRACE=1 at plan creation: kernels stamp %globaltimer into the workspace
     int lazy_tail;      // K12 stops reserving tile ids for the last lazy_tail * grid tiles (CATS_LAZY_TAIL)
     int split_min_b;    // batches b >= split_min_b run the split path KA + KB (CATS_SPLIT_MIN_B)
+    int k12_max_stages; // 0 = as many K12 stages as fit (CATS_K12_STAGES caps it, for experiments)
     size_t off_x1, off_part;  // split path: x1 per compact position [m][max_b]; KB partials [R][max_b][d]
     size_t off_tmask;         // split path: per-tile active-row mask words (KA -> KB), zero between calls
     size_t off_trace, trace_bytes;

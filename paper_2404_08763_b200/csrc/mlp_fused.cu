@@ -543,7 +543,7 @@ template <typename T, int B, int NR, int CPT>
 static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
                                 float t, int mode, float *acts, float *y, void *ws, cudaStream_t s) {
     auto kern = k12_cats_mlp<T, B, NR, CPT>;
-    const int stages = k12_stages(p, B);
+    const int stages = p.k12_max_stages > 0 ? std::min(p.k12_max_stages, k12_stages(p, B)) : k12_stages(p, B);
     const size_t smem = k12_smem_bytes(p, B, stages);
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
     if (e != cudaSuccess) return e;
