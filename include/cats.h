@@ -128,7 +128,8 @@ typedef struct {
 #define CATS_CALIB_BELOW 0     /* finite keys < lo */
 #define CATS_CALIB_INWIN 1     /* keys in [lo, hi] */
 #define CATS_CALIB_ABOVE 2     /* finite keys > hi */
-#define CATS_CALIB_NONFINITE 3 /* NaN / Inf */
+#define CATS_CALIB_NONFINITE 3 /* NaN / Inf: nonzero iff any was seen (the bf16 pass flags once per
+                                  thread instead of counting every value; ABOVE is exact only when 0) */
 #define CATS_CALIB_NCOUNTS 4
 
 /* Initial window for n values: the whole finite key range, coarse bins; strided sampling when n

@@ -55,22 +55,24 @@ calib_hist_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint32_t 
     uint32_t below = 0, nonfin = 0, inwin = 0, seen = 0;
     uint32_t cur_bin = 0xffffffffu, cur_cnt = 0;  // run-length cache against same-bin contention
     const uint32_t span = hi - lo;
+    auto classify_in = [&](uint32_t key) {  // key known to lie in [lo, hi]
+        ++inwin;
+        const uint32_t bin = (key - lo) >> shift;
+        if (bin == cur_bin) {
+            ++cur_cnt;
+        } else {
+            if (cur_cnt) atomicAdd(&sh[cur_bin], cur_cnt);
+            cur_bin = bin;
+            cur_cnt = 1;
+        }
+    };
     auto classify = [&](uint32_t key) {
         below += key < lo ? 1u : 0u;
         nonfin += key >= KT::kInf ? 1u : 0u;
         const uint32_t rel = key - lo;  // unsigned: wraps for key < lo
-        if (rel <= span) {
-            ++inwin;
-            const uint32_t bin = rel >> shift;
-            if (bin == cur_bin) {
-                ++cur_cnt;
-            } else {
-                if (cur_cnt) atomicAdd(&sh[cur_bin], cur_cnt);
-                cur_bin = bin;
-                cur_cnt = 1;
-            }
-        }
+        if (rel <= span) classify_in(key);
     };
+    uint32_t seen_main = 0;
 
     const uint64_t nvec = n / E;
     const uint64_t nwork = stride ? (nvec + stride - 1) / stride : nvec;
@@ -79,16 +81,53 @@ calib_hist_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint32_t 
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t step = stride ? stride : 1;
     // main loop: kCalUnroll independent 16-byte loads in flight per thread
+    uint32_t nge2 = 0, kmax2 = 0;  // bf16 word path: keys >= lo, running max of the key pairs
     for (; i + (kCalUnroll - 1) * gstride < nwork; i += kCalUnroll * gstride) {
         uint4 r[kCalUnroll];
+        if (step == 1) {  // full pass: no 64-bit multiply per load
 #pragma unroll
-        for (int u = 0; u < kCalUnroll; ++u) r[u] = ldg_stream(v4 + (i + u * gstride) * step);
+            for (int u = 0; u < kCalUnroll; ++u) r[u] = ldg_stream(v4 + i + u * gstride);
+        } else {
 #pragma unroll
-        for (int u = 0; u < kCalUnroll; ++u)
+            for (int u = 0; u < kCalUnroll; ++u) r[u] = ldg_stream(v4 + (i + u * gstride) * step);
+        }
+        if constexpr (sizeof(K) == 2) {
+            // two keys per 32-bit word, SIMD within the register: per 16-bit half,
+            // (0x8000 + key) - lo has bit 15 set iff key >= lo, (0x8000 + hi) - key iff key <= hi
+            // (no borrow crosses halves: both differences stay >= 1). ~6 instructions per key.
+            const uint32_t lo2 = lo * 0x10001u;
+            const uint32_t hi2x = (min(hi, KT::kMask) * 0x10001u) | 0x80008000u;
 #pragma unroll
-            for (int e = 0; e < E; ++e) classify(KT::key(r[u], e));
-        seen += kCalUnroll * E;
+            for (int u = 0; u < kCalUnroll; ++u) {
+                const uint32_t wv[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t gl = ((wv[q] | 0x80008000u) - lo2) & 0x80008000u;
+                    nge2 += __popc(gl);
+                    const uint32_t k2 = wv[q] & 0x7fff7fffu;
+                    kmax2 = __vmaxu2(kmax2, k2);
+                    const uint32_t iw = (hi2x - k2) & gl;
+                    if (iw) {  // in-window keys: the minority once the sample pass aimed the window
+                        if (iw & 0x8000u) classify_in(k2 & 0xffffu);
+                        if (iw & 0x80000000u) classify_in(k2 >> 16);
+                    }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < kCalUnroll; ++u)
+#pragma unroll
+                for (int e = 0; e < E; ++e) classify(KT::key(r[u], e));
+        }
+        seen_main += kCalUnroll * E;
     }
+    if constexpr (sizeof(K) == 2) {
+        below += seen_main - nge2;
+        // non-finite keys (always > hi) are flagged once per thread: CATS_CALIB_NONFINITE is then
+        // nonzero iff any NaN/Inf was seen (the calibration is rejected; cats.h)
+        nonfin += ((kmax2 & 0xffffu) >= KT::kInf || (kmax2 >> 16) >= KT::kInf) ? 1u : 0u;
+    }
+    seen += seen_main;
     for (; i < nwork; i += gstride) {
         const uint4 r = ldg_stream(v4 + i * step);
 #pragma unroll
