@@ -355,12 +355,16 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.off_x1 = off;      off = align_up(off + x1_bytes, 256);
         p.off_tmask = off;   off = align_up(off + (size_t)((m + 1) / 2) * 4, 256);
         p.off_part = off;    off = align_up(off + part_bytes, 256);
+        const char *mtl = std::getenv("CATS_K12_MIN_TILES");
+        p.k12_min_tiles = mtl ? std::max(1, std::atoi(mtl)) : 2;
+        const char *eg = std::getenv("CATS_K12_EAGER");
+        p.k12_eager = eg ? std::atoi(eg) : 0;
         const char *ks = std::getenv("CATS_K12_STAGES");
         p.k12_max_stages = ks ? std::max(2, std::atoi(ks)) : 0;
         const char *tr = std::getenv("CATS_TRACE");
         p.trace = tr && tr[0] == '1';
         const char *lt = std::getenv("CATS_LAZY_TAIL");
-        p.lazy_tail = lt ? std::max(0, std::atoi(lt)) : 1;
+        p.lazy_tail = lt ? std::max(0, std::atoi(lt)) : 8;
         p.off_trace = off;
         p.trace_bytes = p.trace ? (size_t)kTraceKernels * kTraceCtas * kTraceSlots * 8 : 0;
         off = align_up(off + p.trace_bytes, 256);

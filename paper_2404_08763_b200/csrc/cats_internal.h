@@ -41,6 +41,8 @@ struct PlanData {
     int lazy_tail;      // K12 stops reserving tile ids for the last lazy_tail * grid tiles (CATS_LAZY_TAIL)
     int split_min_b;    // batches b >= split_min_b run the split path KA + KB (CATS_SPLIT_MIN_B)
     int k12_max_stages; // 0 = as many K12 stages as fit (CATS_K12_STAGES caps it, for experiments)
+    int k12_min_tiles;  // K12 grid <= ntiles / k12_min_tiles (CATS_K12_MIN_TILES)
+    int k12_eager;      // K12 fills every stage with claimed tiles at start (CATS_K12_EAGER)
     size_t off_x1, off_part;  // split path: x1 per compact position [m][max_b]; KB partials [R][max_b][d]
     size_t off_tmask;         // split path: per-tile active-row mask words (KA -> KB), zero between calls
     size_t off_trace, trace_bytes;
@@ -56,8 +58,9 @@ inline int k12_cpt(const PlanData &p, int b) {
     const int nc = k12_consumer_warps_c(b) * 32;
     return (p.nchunks + nc - 1) / nc;
 }
-inline int k12_grid(const PlanData &p, int b) {
-    return std::min(p.num_sms * k12_ctas_per_sm_c(b), k12_ntiles(p, b));
+inline int k12_grid(const PlanData &p, int b) {  // >= k12_min_tiles tiles per CTA on small layers
+    const int mt = std::max(1, p.k12_min_tiles);
+    return std::max(1, std::min(p.num_sms * k12_ctas_per_sm_c(b), (k12_ntiles(p, b) + mt - 1) / mt));
 }
 size_t k12_smem_bytes(const PlanData &p, int b, int stages);
 inline int k12_stages(const PlanData &p, int b) {

@@ -70,7 +70,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
              int d, int m, int stages, float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask,
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
              unsigned long long *__restrict__ yacc, float *__restrict__ y, unsigned int *__restrict__ sched,
-             int lazy_tail, unsigned long long *__restrict__ trace) {
+             int lazy_tail, int eager, unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
     constexpr int NW = k12_consumer_warps_c(B);
@@ -210,7 +210,12 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         prod = __shfl_sync(0xffffffffu, prod, 0);
         ps = prod % stages;
         gates_inflight = prod;
-        // the rest of the ring fills as jobs retire (UD work first)
+        // the rest of the ring fills as jobs retire (UD work first); with `eager` (small layers) the
+        // free stages are filled with claimed tiles right away
+        if (eager) {
+            while (!ended && prod < stages && issue_job()) {
+            }
+        }
         trace_stamp(trace, 0, 1);
 
         int rs = 0;                  // = retire % stages
@@ -565,7 +570,7 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
         static_cast<const T *>(Wd), p.d, p.m, stages, t, mode, reinterpret_cast<int32_t *>(w + p.off_idx),
         reinterpret_cast<uint8_t *>(w + p.off_tokmask), reinterpret_cast<float *>(w + p.off_vals),
         reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<unsigned long long *>(w + p.off_ypart), y,
-        reinterpret_cast<unsigned int *>(w + p.off_sched), p.lazy_tail * k12_grid(p, B),
+        reinterpret_cast<unsigned int *>(w + p.off_sched), p.lazy_tail * k12_grid(p, B), p.k12_eager,
         p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();

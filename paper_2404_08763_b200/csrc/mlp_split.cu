@@ -499,16 +499,16 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     // ---- per-tile active-row masks, published by KA's GATE retire (valid bit 31). KB does NOT wait
     //      for KA to finish here: the list and the first W_down loads overlap KA's UP tail. ----
     if (tid == 0) pre[0] = 0;
-    for (int base = 0; base < ntiles; base += 4 * nth) {  // 4 loads in flight per thread
-        unsigned int c[4];
+    for (int base = 0; base < ntiles; base += 8 * nth) {  // 8 loads in flight per thread
+        unsigned int c[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const int i = base + u * nth + tid;
             c[u] = 0x80000000u;
             if (i < ntiles) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c[u]) : "l"(tmask + i) : "memory");
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const int i = base + u * nth + tid;
             if (i < ntiles) {
                 while (!(c[u] & 0x80000000u)) {  // that tile's GATE job has not retired yet

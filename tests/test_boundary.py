@@ -61,7 +61,7 @@ def test_plan_without_gpu():
     assert 2 * (i["smem"] + 1024) <= 228 * 1024      # two K12 CTAs per SM
     assert i["workspace_bytes"] >= 4096 * 8          # int64 y accumulator
     toy = cats.MlpPlan(64, 176, max_batch=1, dtype=torch.float32, num_sms=148)
-    assert toy.info["grid"] == 176 // 4              # no more CTAs than tiles
+    assert toy.info["grid"] == 176 // 4 // 2         # small layers: >= 2 tiles per CTA
     small = cats.MlpPlan(64, 5, max_batch=8, dtype=torch.float32, num_sms=148)
     assert small.info["grid"] == 2
     for b in range(1, 9):                            # every batch size fits the shared-memory budget
