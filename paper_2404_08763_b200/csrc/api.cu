@@ -325,11 +325,13 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.esize = esize;
         p.vec = 16 / esize;
         p.nchunks = d * esize / 16;
+        const char *nrf = std::getenv("CATS_K12_NR");
+        p.nr_force = nrf ? std::atoi(nrf) : 0;
         // K12: persistent CTAs pulling NR-row tiles from a global counter
         p.g1 = 0;
         for (int b = 1; b <= max_batch; ++b) {
             if (k12_cpt(p, b) > (b == 1 ? kMaxCPT : 2)) return CATS_E_UNSUPPORTED;
-            if (k12_stages(p, b) < 3 || k12_smem_bytes(p, b, k12_stages(p, b)) > k12_smem_budget_c(b))
+            if (k12_stages(p, b) < 2 || k12_smem_bytes(p, b, k12_stages(p, b)) > k12_smem_budget_c(b))
                 return CATS_E_UNSUPPORTED;
             p.g1 = std::max(p.g1, k12_grid(p, b));
         }

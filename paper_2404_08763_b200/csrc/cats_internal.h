@@ -43,6 +43,7 @@ struct PlanData {
     int k12_max_stages; // 0 = as many K12 stages as fit (CATS_K12_STAGES caps it, for experiments)
     int k12_min_tiles;  // K12 grid <= ntiles / k12_min_tiles (CATS_K12_MIN_TILES)
     int k12_eager;      // K12 fills every stage with claimed tiles at start (CATS_K12_EAGER)
+    int nr_force;       // 0 = automatic tile height; 2 / 4 forces it (CATS_K12_NR)
     size_t off_x1, off_part;  // split path: x1 per compact position [m][max_b]; KB partials [R][max_b][d]
     size_t off_tmask;         // split path: per-tile active-row mask words (KA -> KB), zero between calls
     size_t off_trace, trace_bytes;
@@ -50,8 +51,11 @@ struct PlanData {
 
 // K12 tile height NR (W_gate rows per GATE job; a UD job carries NR/2 neurons = the same bytes).
 inline int k12_rows_per_tile(const PlanData &p, int b) {
+    if (p.nr_force == 2 || p.nr_force == 4) return p.nr_force;  // CATS_K12_NR (experiments)
+    // 4-row tiles whenever two 4-row stages fit (measured at d = 5120, b = 1: 4 rows x 2 stages beats
+    // 2 rows x 5 stages, 55.6 vs 60.6 us; per-job costs are per row pair)
     const size_t row = (size_t)p.d * p.esize;
-    return 4 * row * 3 <= k12_smem_budget_c(b) - 8 * 1024 ? 4 : 2;
+    return 4 * row * 2 <= k12_smem_budget_c(b) - 8 * 1024 ? 4 : 2;
 }
 inline int k12_ntiles(const PlanData &p, int b) { return (p.m + k12_rows_per_tile(p, b) - 1) / k12_rows_per_tile(p, b); }
 inline int k12_cpt(const PlanData &p, int b) {
