@@ -51,10 +51,13 @@ struct PlanData {
 
 // K12 tile height NR (W_gate rows per GATE job; a UD job carries NR/2 neurons = the same bytes).
 inline int k12_rows_per_tile(const PlanData &p, int b) {
-    if (p.nr_force == 2 || p.nr_force == 4) return p.nr_force;  // CATS_K12_NR (experiments)
+    if (p.nr_force == 2 || p.nr_force == 4 || (p.nr_force == 6 && b == 1)) return p.nr_force;  // CATS_K12_NR
     // 4-row tiles whenever two 4-row stages fit (measured at d = 5120, b = 1: 4 rows x 2 stages beats
     // 2 rows x 5 stages, 55.6 vs 60.6 us; per-job costs are per row pair)
     const size_t row = (size_t)p.d * p.esize;
+    // b = 1 on large layers: 6-row tiles (two 48 KB stages at d = 4096; fewer, larger jobs: Mistral-7B
+    // 42.6 -> 41.9 us); small layers keep 4 rows (more tiles to balance)
+    if (b == 1 && p.m >= 8192 && 6 * row * 2 <= k12_smem_budget_c(b) - 8 * 1024) return 6;
     return 4 * row * 2 <= k12_smem_budget_c(b) - 8 * 1024 ? 4 : 2;
 }
 inline int k12_ntiles(const PlanData &p, int b) { return (p.m + k12_rows_per_tile(p, b) - 1) / k12_rows_per_tile(p, b); }

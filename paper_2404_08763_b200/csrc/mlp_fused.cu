@@ -596,6 +596,9 @@ static cudaError_t launch_k12_b(const PlanData &p, const void *x, const void *Wg
     switch (k12_rows_per_tile(p, B)) {
         case 4: return launch_k12_r<T, B, 4>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
         case 2: return launch_k12_r<T, B, 2>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 6:
+            if constexpr (B == 1) return launch_k12_r<T, B, 6>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+            return cudaErrorInvalidValue;
         default: return cudaErrorInvalidValue;
     }
 }

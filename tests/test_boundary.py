@@ -57,7 +57,7 @@ def test_rank_rule_exact():
 def test_plan_without_gpu():
     p = cats.MlpPlan(4096, 14336, max_batch=1, dtype=torch.bfloat16, num_sms=148)
     i = p.info
-    assert i["grid"] == 2 * 148 and i["stages"] >= 3 and i["rows_per_tile"] == 4
+    assert i["grid"] == 2 * 148 and i["stages"] >= 2 and i["rows_per_tile"] == 6
     assert 2 * (i["smem"] + 1024) <= 228 * 1024      # two K12 CTAs per SM
     assert i["workspace_bytes"] >= 4096 * 8          # int64 y accumulator
     toy = cats.MlpPlan(64, 176, max_batch=1, dtype=torch.float32, num_sms=148)
