@@ -506,9 +506,18 @@ extern "C" cats_status_t cats_mlp_decode_host(const cats_mlp_plan_t *plan, const
     cudaError_t e = cudaSetDevice(p.device);
     if (e == cudaSuccess) e = cudaMemcpyAsync(xd, x_host, (size_t)b * p.d * p.esize, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_status(e);
-    cats_status_t rc = run_mlp(p, xd, b, W_gate, W_up, W_down_nm, t, 0, yd, ws, st);
+    // pinned (mapped) y_host: the kernel writes y straight into host memory (one small PCIe write
+    // from the converting CTAs) instead of a separate device-to-host copy
+    cudaPointerAttributes pa{};
+    float *y_direct = nullptr;
+    if (cudaPointerGetAttributes(&pa, y_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer &&
+        aligned16(pa.devicePointer))
+        y_direct = static_cast<float *>(pa.devicePointer);
+    else
+        (void)cudaGetLastError();  // clear a pageable-pointer query error
+    cats_status_t rc = run_mlp(p, xd, b, W_gate, W_up, W_down_nm, t, 0, y_direct ? y_direct : yd, ws, st);
     if (rc != CATS_OK) return rc;
-    e = cudaMemcpyAsync(y_host, yd, (size_t)b * p.d * 4, cudaMemcpyDeviceToHost, st);
+    if (!y_direct) e = cudaMemcpyAsync(y_host, yd, (size_t)b * p.d * 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     return cuda_status(e);
 }
