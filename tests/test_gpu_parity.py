@@ -158,8 +158,14 @@ def test_decode_host_equals_device_path():
     plan = cats.MlpPlan(d, m, max_batch=b)
     ws = plan.workspace()
     y_dev = cats.cats_mlp_decode(plan, _dev(x), Wg, Wu, Wd, 0.1, ws=ws).cpu()
-    y_host = cats.cats_mlp_decode_host(plan, x.pin_memory(), Wg, Wu, Wd, 0.1, ws=ws)
+    y_host = cats.cats_mlp_decode_host(plan, x.pin_memory(), Wg, Wu, Wd, 0.1, ws=ws)  # kernel writes host y
     assert torch.equal(y_dev, y_host)
+    y_pageable = torch.empty((b, d), dtype=torch.float32)                         # device-to-host copy path
+    cats.cats_mlp_decode_host(plan, x, Wg, Wu, Wd, 0.1, y_host=y_pageable, ws=ws)
+    assert torch.equal(y_dev, y_pageable)
+    x1 = x[:1].clone()                                                            # b = 1 (K12), pinned
+    y1 = cats.cats_mlp_decode_host(plan, x1.pin_memory(), Wg, Wu, Wd, 0.1, ws=ws)
+    assert torch.equal(cats.cats_mlp_decode(plan, _dev(x1), Wg, Wu, Wd, 0.1, ws=ws).cpu(), y1)
 
 
 def test_tensor_parallel_emulated_on_one_gpu():
