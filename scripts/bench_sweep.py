@@ -81,7 +81,7 @@ def weights(d, m, layers, copies, heavy, dtype):
     return _STACKS[key]
 
 
-def run_layers(name, d, m, layers, copies, b, k, heavy, dtype=torch.bfloat16, dense_too=False):
+def run_layers(name, d, m, layers, copies, b, k, heavy, dtype=torch.bfloat16, dense_too=False, optimal=True):
     plan = cats.MlpPlan(d, m, max_batch=8, dtype=dtype)
     ws = plan.workspace()
     Ws = weights(d, m, layers, copies, heavy, dtype)
@@ -115,6 +115,19 @@ def run_layers(name, d, m, layers, copies, b, k, heavy, dtype=torch.bfloat16, de
         ud = graph_time(fd, a.reps) / n
         rec.update(dense_us_per_step=round(ud, 3), speedup_vs_dense=round(ud / us, 4),
                    dense_GBps=round(3 * 2 * d * m * esz // 2 / (ud * 1e-6) / 1e9, 1))
+    if optimal and b == 1 and k > 0:
+        # the paper's "Optimal" (Fig. 3): a dense MLP with only the (1 - k) m neurons CATS keeps --
+        # what a perfect predictor of the active set could at best achieve with the same kernel
+        mo = max(8, int(round(m * (1 - k))))
+        po = cats.MlpPlan(d, mo, max_batch=8, dtype=dtype)
+        wso = po.workspace()
+        Wo = [[w[:mo] for w in W] for W in Ws]
+
+        def fo():
+            for W in Wo:
+                cats.cats_mlp_dense(po, x, W[0], W[1], W[2], y=y, ws=wso)
+        uo = graph_time(fo, a.reps) / n
+        rec.update(optimal_us_per_step=round(uo, 3), cats_over_optimal=round(us / uo, 4))
     emit(**rec)
 
 
