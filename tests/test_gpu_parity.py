@@ -79,6 +79,7 @@ def run_parity(d, m, b, dtype, k, seed=0, heavy=False, num_sms=0, check_y=True):
     (512, 3001, 5, torch.bfloat16, 0.7),
     (1024, 4096, 8, torch.bfloat16, 0.5),
     (8192, 512, 1, torch.bfloat16, 0.5),     # widest supported row (4 chunks per K2 thread)
+    (8192, 700, 3, torch.bfloat16, 0.7),     # b >= 2 where the split path does not fit: K12 fallback
     (128, 7, 4, torch.bfloat16, 0.5),        # m < number of SMs
     (8, 1, 1, torch.float32, 0.0),           # a single neuron, one 32-byte row
 ])
