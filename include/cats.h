@@ -163,10 +163,11 @@ typedef struct {
     int d, m, max_batch;
     cats_dtype_t w_dtype;
     int device, num_sms;
-    int grid, threads;            /* K12 fused dataflow kernel: persistent CTAs (one per SM) */
+    /* K12 (the fused kernel) at b = max_batch: */
+    int grid, threads;            /* persistent CTAs (two per SM at b = 1, one at b >= 2) */
     int rows_per_tile;            /* W_gate rows per GATE job; a UD job carries rows_per_tile/2 neurons */
     int stages;                   /* shared-memory ring depth (one job per stage) */
-    size_t smem;                  /* K12 dynamic shared memory bytes (at max_batch) */
+    size_t smem;                  /* dynamic shared memory bytes per CTA */
     size_t workspace_bytes;
 } cats_mlp_plan_info_t;
 
@@ -181,17 +182,24 @@ cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_dtype_t w_d
 void cats_mlp_plan_destroy(cats_mlp_plan_t *plan);
 cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_mlp_plan_info_t *info);
 cats_status_t cats_mlp_workspace_bytes(const cats_mlp_plan_t *plan, size_t *bytes);
-/* Initialise a freshly allocated workspace once (zeroes K1's tile-scheduler counters, which every
- * K1 launch leaves zeroed again on exit). Required before the first call that uses `ws`.
- * Asynchronous on s. Errors: CATS_E_NULL, CATS_E_WORKSPACE, CATS_E_ALIGN, CATS_E_CUDA. */
+/* Initialise a freshly allocated workspace once (zeroes the scheduler counters, the int64 y
+ * accumulator and the per-tile mask words, which every launch leaves zeroed again on exit).
+ * Required before the first call that uses `ws`. Asynchronous on s.
+ * Errors: CATS_E_NULL, CATS_E_WORKSPACE, CATS_E_ALIGN, CATS_E_CUDA. */
 cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, void *ws, size_t ws_bytes, cats_stream_t s);
 
 /* y[b][d] = CATS_t gated MLP of x[b][d] over this plan's m neurons (under tensor parallelism y
  * is the rank's partial; the caller all-reduces). t >= 0; t = 0 gives dense semantics.
- * ONE kernel launch on s (K12): a persistent dataflow kernel doing the gate GEMV, SiLU, threshold,
- * compaction, sparse up x v, down projection and the split-K reduction (TMA bulk-reduce of exact
- * fixed-point partials; the last CTA writes y). Deterministic: bit-identical y for identical
- * inputs, whatever the dynamic tile schedule.
+ * b = 1: ONE kernel launch on s (K12), a persistent dataflow kernel doing the gate GEMV, SiLU,
+ * threshold, compaction, sparse up x v, down projection and the split-K reduction (TMA bulk-reduce
+ * of exact fixed-point partials; the last CTA writes y).
+ * b >= 2: TWO launches (KA: gate + up with compaction; KB: down projection over balanced ranges of
+ * the active list + a fixed-order two-phase reduction); b >= 4 uses warp-level bf16 MMA for the
+ * dot products. cats_mlp_kernels_per_call() tells which. All launches use programmatic dependent
+ * launch (a successor's CTAs start streaming weights while the predecessor drains).
+ * KB keeps all of its CTAs (<= the plan's SM count) co-resident for a grid barrier: do not run the
+ * decode concurrently with a kernel that occupies SMs indefinitely.
+ * Deterministic: bit-identical y for identical inputs, whatever the dynamic tile schedule.
  * Errors: CATS_E_NULL, CATS_E_ALIGN, CATS_E_BATCH, CATS_E_THRESHOLD, CATS_E_WORKSPACE,
  *         CATS_E_CUDA. */
 cats_status_t cats_mlp_decode(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
