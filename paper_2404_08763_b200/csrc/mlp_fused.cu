@@ -462,6 +462,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         // yacc to fp32 once, writes y, and re-zeroes yacc and the tile scheduler for the next call.
         __shared__ unsigned int s_last;
         if (mode != kModeGateOnly) {
+            consumer_barrier<NC>();  // every consumer warp is past its last job: the ring is idle
             unsigned long long *sbuf = reinterpret_cast<unsigned long long *>(ring);
             const int tpc = min(B, (int)(((size_t)stages * stage_bytes) / ((size_t)d * 8)));  // tokens per chunk
             for (int t0 = 0; t0 < B; t0 += tpc) {

@@ -137,7 +137,9 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
     float *red = red0 + (size_t)g * stages * NWG * PP;
 
     trace_stamp(trace, 0, 0);
-    pdl_launch_dependents();
+    // (griddepcontrol.launch_dependents comes after each thread's griddepcontrol.wait: KB may only
+    //  start once this grid's predecessor -- the previous decode -- has completed, because KB reads
+    //  the per-tile masks and counters that decode re-armed)
     if (tid == 0) {
         for (int s = 0; s < NG * stages; ++s) {
             mbar_init(&full0[s], 1);
@@ -278,6 +280,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
         ps = prod % stages;
         gates_inflight = prod;
         pdl_wait_primary();
+        pdl_launch_dependents();
         if (lane == 0) {
             claim_async(res0, sched, dyn_base + (unsigned)lazy_tail < (unsigned)ntiles);
             claim_async(res1, sched, dyn_base + 1u + (unsigned)lazy_tail < (unsigned)ntiles);
@@ -360,6 +363,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
     } else {
         // ===================================== CONSUMER WARPS ====================================
         pdl_wait_primary();  // x may come from the predecessor
+        pdl_launch_dependents();
         const int ctid = tid - g * NCG;  // consumer thread index within the group
         const int cwarp = warp - g * NWG;
         int s = 0;

@@ -59,7 +59,7 @@ torch.cuda.synchronize()
 tr = ws[off.value:off.value + nbytes.value].cpu().numpy().view(np.uint64).reshape(3, 512, 8).astype(np.int64)
 rep = {}
 t0 = None
-names = {0: ["start", "primed", "jobs_done", "exit", "reduced"], 1: ["start", "list_ready", "jobs_done", "barrier", "exit", "pdl_waited", "prefix_done"]}
+names = {0: ["start", "primed", "jobs_done", "exit", "reduced"], 1: ["start", "list_ready", "jobs_done", "barrier", "exit", "masks_read", "prefix_done"]}
 titles = {0: "K12 / KA", 1: "KB"}
 for k in range(2):
     g = int((tr[k, :, 0] > 0).sum())  # CTAs that stamped
@@ -75,6 +75,14 @@ for k in range(2):
             print(f"   {nm:12s} min {v.min():8.2f}  avg {v.mean():8.2f}  max {v.max():8.2f}")
             rep[f"K{k}.{nm}"] = [float(v.min()), float(v.mean()), float(v.max())]
 g = int((tr[0, :, 0] > 0).sum())
+gb = int((tr[1, :, 0] > 0).sum())
+if gb and tr[2, :gb, 5].max() > 0 and tr[2, :gb, 4].max() == 0:  # KB-only statistics written
+    sb = tr[2, :gb, :].astype(np.float64)
+    print("KB per-CTA: producer empty-wait ns avg/max", sb[:, 0].mean().round(0), sb[:, 0].max(),
+          "| consumer full-wait ns avg/max", sb[:, 3].mean().round(0), sb[:, 3].max(),
+          "| chunks avg/min/max", sb[:, 5].mean().round(1), sb[:, 5].min(), sb[:, 5].max(),
+          "| claim-wait ns", sb[:, 1].mean().round(0), "| x1-issue ns", sb[:, 2].mean().round(0),
+          "| search ns", sb[:, 4].mean().round(0), "| search+bulk ns", sb[:, 6].mean().round(0))
 st = tr[2, :g, :7].astype(np.float64)
 if st[:, 2].max() > 0:  # K12 producer / consumer statistics
     print("K12 per-CTA stats (avg/min/max):")
