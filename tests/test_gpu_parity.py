@@ -298,3 +298,19 @@ def test_split_path_matches_fused_path(d, m, b, k, monkeypatch):
     yf = cats.cats_mlp_decode(plan_f, x, Wg, Wu, Wd, t, ws=plan_f.workspace())
     err = (ys.double() - yf.double()).norm() / yf.double().norm().clamp_min(1e-30)
     assert float(err) <= Y_TOL
+
+
+def test_mixed_batches_share_one_workspace():
+    """K12 (b = 1) and the split path (b >= 2) re-arm their counters, accumulators and tile masks for
+    each other: alternating batch sizes on one workspace gives the same bits as fresh workspaces."""
+    d, m = 4096, 11008
+    Wg, Wu, Wd = (_dev(a) for a in cats_synth.mlp_weights(d, m, torch.bfloat16, layer=3))
+    plan = cats.MlpPlan(d, m, max_batch=8)
+    ws = plan.workspace()
+    for i, b in enumerate([1, 8, 2, 1, 5, 4, 1, 3]):
+        x = _dev(cats_synth.tokens(b, d, torch.bfloat16, seed=40 + i))
+        y_shared = cats.cats_mlp_decode(plan, x, Wg, Wu, Wd, 0.12, ws=ws).clone()
+        y_fresh = cats.cats_mlp_decode(plan, x, Wg, Wu, Wd, 0.12, ws=plan.workspace())
+        assert torch.equal(y_shared, y_fresh), b
+        y_dense = cats.cats_mlp_dense(plan, x, Wg, Wu, Wd, ws=ws)
+        assert torch.isfinite(y_dense).all()
