@@ -183,7 +183,7 @@ def run_reference(args):
 def workload_config(args, d, m):
     return {"workload": f"{args.model} MLP layer decode (d={d}, m={m}) bf16 b={args.batch} "
                         f"k={args.sparsity} TP={args.gpus}",
-            "model_shape": {"d": d, "m": m}, "batch": args.batch, "sparsity": args.sparsity,
+            "layer_shape": {"d": d, "m": m}, "batch": args.batch, "sparsity": args.sparsity,
             "tp": args.gpus, "storage": "bf16", "accumulate": "f32",
             "l2": f"inputs larger than L2: {args.copies} rotated weight copies per rank",
             "timing": "CUDA events on the launching stream, max over ranks; steps replayed from a CUDA graph "
