@@ -359,6 +359,8 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.off_part = off;    off = align_up(off + part_bytes, 256);
         const char *mtl = std::getenv("CATS_K12_MIN_TILES");
         p.k12_min_tiles = mtl ? std::max(1, std::atoi(mtl)) : 2;
+        const char *pf = std::getenv("CATS_K12_L2PF");
+        p.k12_l2pf = pf ? std::max(0, std::atoi(pf)) : 0;  // measured: prefetching only slows the drain
         const char *eg = std::getenv("CATS_K12_EAGER");
         p.k12_eager = eg ? std::atoi(eg) : 0;
         const char *ks = std::getenv("CATS_K12_STAGES");

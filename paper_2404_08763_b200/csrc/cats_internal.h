@@ -43,6 +43,7 @@ struct PlanData {
     int k12_max_stages; // 0 = as many K12 stages as fit (CATS_K12_STAGES caps it, for experiments)
     int k12_min_tiles;  // K12 grid <= ntiles / k12_min_tiles (CATS_K12_MIN_TILES)
     int k12_eager;      // K12 fills every stage with claimed tiles at start (CATS_K12_EAGER)
+    int k12_l2pf;       // K12 static tiles per CTA prefetched into L2 at start (CATS_K12_L2PF)
     int nr_force;       // 0 = automatic tile height; 2 / 4 forces it (CATS_K12_NR)
     size_t off_x1, off_part;  // split path: x1 per compact position [m][max_b]; KB partials [R][max_b][d]
     size_t off_tmask;         // split path: per-tile active-row mask words (KA -> KB), zero between calls

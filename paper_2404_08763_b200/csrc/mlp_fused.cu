@@ -70,7 +70,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
              int d, int m, int stages, float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask,
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
              unsigned long long *__restrict__ yacc, float *__restrict__ y, unsigned int *__restrict__ sched,
-             int lazy_tail, int eager, unsigned long long *__restrict__ trace) {
+             int lazy_tail, int eager, int l2pf, unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
     constexpr int NW = k12_consumer_warps_c(B);
@@ -120,8 +120,13 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         // claimed when a stage is free to stream it, so no CTA sits on unstarted work while others
         // drain (balanced tail), and small layers spread over all CTAs.
         unsigned int t_res = kNoTile;  // raw counter value; tile id = dyn_base + counter
-        const int batch = max(1, min(stages, ntiles / (int)gridDim.x));  // static first tiles per CTA
+        // static first tiles per CTA: `stages` of them go straight into the ring, up to l2pf more are
+        // prefetched into L2 (cp.async.bulk.prefetch) -- both before griddepcontrol.wait, so they use
+        // the HBM time while the previous kernel drains -- and taken in order before any claim
+        const int batch = max(1, min(stages + l2pf, ntiles / (int)gridDim.x));
         const unsigned int dyn_base = gridDim.x * (unsigned)batch;        // first dynamically claimed tile
+        const unsigned int sbase = blockIdx.x * (unsigned)batch;          // this CTA's static tiles
+        int snext = min(batch, stages);                                    // next static tile to issue
         int prod = 0;                // jobs issued; job j lives in stage j % stages
         int ps = 0;                  // = prod % stages
         int retire = 0;              // jobs retired (consumed and post-processed), in order
@@ -151,15 +156,25 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 }
                 ++q_head;
             } else {
-                unsigned int tile = t_res;
-                if (lane == 0 && tile == kNoTile) tile = atomicAdd(&sched[0], 1u);  // claim now
-                tile = __shfl_sync(0xffffffffu, tile, 0) + dyn_base;
+                unsigned int tile;
+                const bool from_static = snext < batch;
+                if (from_static) {  // a static tile (L2-prefetched at start)
+                    tile = sbase + (unsigned)snext;
+                } else {
+                    tile = t_res;
+                    if (lane == 0 && tile == kNoTile) tile = atomicAdd(&sched[0], 1u);  // claim now
+                    tile = __shfl_sync(0xffffffffu, tile, 0) + dyn_base;
+                }
                 if (tile < (unsigned)ntiles) {  // GATE job: a new tile of W_gate rows
                     const int r0 = (int)tile * NR;
                     const int nr = min(NR, m - r0);
-                    if (lane == 0) {
+                    if (from_static) {
+                        ++snext;
+                    } else if (lane == 0) {
                         t_res = kNoTile;
                         claim_tile_async(t_res, sched, tile + (unsigned)lazy_tail < (unsigned)ntiles);
+                    }
+                    if (lane == 0) {
                         D.type = kJobGate;
                         D.tile = (int)tile;
                         D.n = nr;
@@ -191,9 +206,14 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             // so small layers spread over all CTAs). Weights are read-only, so the loads may start
             // before the PDL predecessor has finished; everything it writes (tile counter, y
             // accumulator, x, index lists) is touched only after griddepcontrol.wait below.
-            const unsigned int base = blockIdx.x * (unsigned)batch;
-            for (int s = 0; s < batch; ++s) {
-                const unsigned int tile = base + s;  // grid * batch <= ntiles
+            for (int s = batch > stages ? stages : batch; s < batch; ++s) {  // the rest of the static tiles -> L2
+                const int r0 = (int)(sbase + s) * NR;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Wg + (size_t)r0 * d),
+                             "r"((uint32_t)min(NR, m - r0) * row_bytes)
+                             : "memory");
+            }
+            for (int s = 0; s < min(batch, stages); ++s) {
+                const unsigned int tile = sbase + s;  // grid * batch <= ntiles
                 const int r0 = (int)tile * NR;
                 const int nr = min(NR, m - r0);
                 desc[s].type = kJobGate;
@@ -571,7 +591,7 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
         static_cast<const T *>(Wd), p.d, p.m, stages, t, mode, reinterpret_cast<int32_t *>(w + p.off_idx),
         reinterpret_cast<uint8_t *>(w + p.off_tokmask), reinterpret_cast<float *>(w + p.off_vals),
         reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<unsigned long long *>(w + p.off_ypart), y,
-        reinterpret_cast<unsigned int *>(w + p.off_sched), p.lazy_tail * k12_grid(p, B), p.k12_eager,
+        reinterpret_cast<unsigned int *>(w + p.off_sched), p.lazy_tail * k12_grid(p, B), p.k12_eager, p.k12_l2pf,
         p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
