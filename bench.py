@@ -242,20 +242,31 @@ def main():
     # sync-free, so they capture as-is); replayed K/G times in the timed region
     G = 8
     graph = torch.cuda.CUDAGraph()
-    cap = torch.cuda.Stream(dev)
-    cap.wait_stream(stream)
-    with torch.cuda.stream(cap):
-        for i in range(G):  # warm the capture stream
-            step(i, st=cap)
-    stream.wait_stream(cap)
-    torch.cuda.synchronize(dev)
-    with torch.cuda.graph(graph, stream=cap):
-        for i in range(G):
-            step(i, st=cap)
-    torch.cuda.synchronize(dev)
+    graph_ok = True
+    try:
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            for i in range(G):  # warm the capture stream
+                step(i, st=cap)
+        stream.wait_stream(cap)
+        torch.cuda.synchronize(dev)
+        with torch.cuda.graph(graph, stream=cap):
+            for i in range(G):
+                step(i, st=cap)
+        torch.cuda.synchronize(dev)
+    except Exception as exc:  # e.g. a collective that cannot be captured: time eager launches instead
+        graph_ok = False
+        print(f"[bench] CUDA graph capture failed ({type(exc).__name__}: {exc}); timing eager steps",
+              file=sys.stderr, flush=True)
+        torch.cuda.synchronize(dev)
+    if world > 1:  # every rank must take the same timing path
+        ok_t = torch.tensor([1 if graph_ok else 0], device=dev)
+        dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+        graph_ok = bool(ok_t.item())
 
     def make_graph_step(k_total):
-        full = k_total // G * G
+        full = k_total // G * G if graph_ok else 0
 
         def graph_step(i):  # exactly k_total steps: k_total // G replays + k_total % G eager steps
             if i < full:
@@ -395,7 +406,7 @@ def main():
             "detail": {
                 "t": t, "nnz_union_per_rank": nnz_local, "nnz_union_total": U, "m_per_rank": ms,
                 "realized_sparsity": round(1 - U / m, 4),
-                "eager_us_per_step": round(ms_eager * 1e3, 3), "graph_steps_per_replay": G,
+                "eager_us_per_step": round(ms_eager * 1e3, 3), "graph_steps_per_replay": G if graph_ok else 0,
                 "isolated_launch_us": {"K12" if not split else "KA": round(k_first, 3),
                                        **({"KB": round(k_second, 3)} if split else {})},
                 "effective_bytes_per_step": step_bytes,
