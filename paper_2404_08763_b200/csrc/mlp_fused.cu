@@ -7,31 +7,36 @@
 // Alg. 1 line 4 "idcs <- indices where Mask = 1" done per tile with a warp ballot (no
 // atomic appends).
 //
-// B200 design (DESIGN.md §6):
-//  * Work unit = a tile of NR consecutive neurons. Persistent CTAs (one per SM) pull tiles from a
-//    global counter, so SMs with more bandwidth take more tiles: no static-partition tail, and no
-//    grid-wide barrier between the gate GEMV and the sparse up/down projection.
+// B200 design (DESIGN.md §5.3):
+//  * Work unit = a tile of NR consecutive neurons (6 / 4 / 2, k12_rows_per_tile). Persistent CTAs
+//    (two per SM at b = 1, one at b >= 2) take their first tiles statically -- issued before
+//    griddepcontrol.wait, so they stream while the previous kernel drains -- and the rest from a
+//    global counter (one tile reserved ahead, none in the last 8 x grid tiles): SMs with more
+//    bandwidth take more tiles, and there is no grid-wide barrier between the gate GEMV and the
+//    sparse up/down projection.
 //  * Each CTA runs a ring of S shared-memory stages fed by the TMA bulk-copy engine
-//    (cp.async.bulk + mbarrier transaction counts). A stage holds one JOB:
-//        GATE(tile): the tile's NR rows of W_gate (neuron-major, contiguous);
-//        UD(<= NU active neurons of one tile): their W_up and W_down rows (contiguous 2d-byte rows).
-//  * Warp specialisation: 16 consumer warps do the arithmetic; one producer warp retires jobs in
-//    order (full/empty mbarrier pair per stage), turns a GATE job's partial dot products into
+//    (cp.async.bulk + mbarrier transaction counts, L2 evict-first). A stage holds one JOB:
+//        GATE(tile): the tile's NR rows of W_gate (neuron-major, contiguous: one copy);
+//        UD(<= NU = NR/2 active neurons of one tile): their W_up and W_down rows (one copy per row).
+//  * Warp specialisation: 8 (b = 1) or 16 consumer warps do the arithmetic; one producer warp retires
+//    jobs in order (full/empty mbarrier pair per stage), turns a GATE job's partial dot products into
 //    u -> v = SiLU(u) -> keep = |v| >= t -> ballot compaction, queues the tile's active neurons as
 //    UD jobs, and refills freed stages (UD jobs first, else a new GATE tile). UD rows are requested
 //    S-1 jobs before they are consumed, so the mask -> load dependency is hidden and only active
 //    neurons' W_up / W_down rows are ever read (the paper's memory saving).
-//  * Consumer thread t owns 16-byte column chunks {t, t+512, ...} of d: x stays in registers (fp32);
-//    dot products are per-thread partials, a fixed xor butterfly per warp, then a fixed-order sum
-//    over the 16 warps. GATE jobs need no consumer barrier; UD jobs one named barrier.
+//  * Consumer thread t owns 16-byte column chunks {t, t + NC, ...} of d; x stays in registers,
+//    packed; dot products use FHFMA.BF16 (bf16 x bf16 -> fp32 straight from the packed registers),
+//    a fixed xor butterfly per warp, then a fixed-order sum over the warps. GATE jobs need no
+//    consumer barrier; UD jobs one named barrier.
 //  * Determinism under dynamic scheduling: a UD job's contribution y_job[c] = sum_i x1_i Wd[i][c]
 //    (<= NU neurons of ONE tile, ascending, fp32, fixed order) is converted once to an exact
 //    fixed-point integer round(y_job * 2^30) (split into two int32 halves, cats_device.cuh
 //    fix_acc) and added to the thread's integer accumulator. Integer
 //    addition is associative, so y does not depend on which CTA took which tile or in which order:
 //    bit-reproducible. (Replaces the paper's fp16 tl.atomic_add into Y.)
-//  * Split-K reduction: each CTA bulk-reduces (TMA cp.reduce.async.bulk .add.u64) its integer
-//    partial into one global accumulator; the last CTA converts it to fp32 once and writes y.
+//  * Split-K reduction: each CTA stages its integer partial in the (idle) ring and bulk-reduces it
+//    (TMA cp.reduce.async.bulk .add.u64) into one global accumulator; the last CTA converts it to
+//    fp32 once, writes y, re-zeroes the accumulator and re-arms the tile counter.
 //
 // Workspace outputs for introspection: tile tau's cnt[tau] active neurons are written ascending at
 // positions [tau*NR, tau*NR + cnt[tau]) of idx / tokmask / vals (v in fp32, 0 where |v| < t).
