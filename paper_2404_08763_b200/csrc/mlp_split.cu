@@ -5,26 +5,29 @@
 // with the batch semantics of DESIGN.md reading G6: a neuron's W_up / W_down rows are read once if it
 // is active for ANY of the b tokens (the union), and token i uses v_i = 0 where |v_i| < t.
 //
-// Why a second path (DESIGN.md §6.3). K12 keeps x and the exact fixed-point y partial of every token
+// Why a second path (DESIGN.md §5.2). K12 keeps x and the exact fixed-point y partial of every token
 // in registers: 2*b*d values per CTA, which is the whole register file at b = 8. Here the two
 // register-heavy halves run in different kernels, each with its own work decomposition:
 //
-//  * KA (gate + up, dynamic): the K12 dataflow (persistent CTAs, tile counter, S-stage TMA bulk ring,
-//    one producer warp) with x staged once in shared memory. Jobs are GATE(tile of NR W_gate rows) and
-//    UP(<= NR active neurons' W_up rows, gathered across tiles from a FIFO). Every job is the same
-//    consumer work: NR x b dot products, bf16 x bf16 products accumulated in fp32 by FHFMA.BF16
-//    (fma.rn.f32.bf16 reads both bf16 halves straight from the packed registers: no unpack), one
-//    warp reduce-scatter (NR*b - 1 shuffles), a fixed-order sum over the 16 warps by the producer.
-//    The producer turns GATE results into u -> v = SiLU(u) -> keep = |v| >= t -> ballot compaction
-//    (idx / tokmask / vals / cnt, the same per-tile layout as K12) and UP results into
-//    x1 = (x W_up[j]) * v_j (Optimization 1), written per compact position.
+//  * KA (gate + up, dynamic): the K12 dataflow (persistent CTAs, tile counter, TMA bulk rings) with x
+//    staged once in shared memory and TWO independent job streams per CTA (each: a producer warp, a
+//    ring, 8 consumer warps -- one producer per SM was the bottleneck). Jobs are GATE(tile of NR
+//    W_gate rows) and UP(<= NR active neurons' W_up rows, gathered across tiles from a FIFO). Every
+//    job is the same consumer work, NR x b dot products, in one of two engines: b <= 3 FHFMA.BF16
+//    (fma.rn.f32.bf16 on the packed registers) + one warp reduce-scatter (NR*b - 1 shuffles);
+//    b >= 4 warp-level mma.sync m16n8k16 bf16 -> fp32 (x = A, the job's rows = B, both via ldmatrix
+//    from 16-byte-padded rows). The producer sums the group's 8 warp partials in fixed order and
+//    turns GATE results into u -> v = SiLU(u) -> keep = |v| >= t -> ballot compaction (idx / tokmask /
+//    vals / cnt, the same per-tile layout as K12, plus one mask word per tile for KB) and UP results
+//    into x1 = (x W_up[j]) * v_j (Optimization 1), written per compact position.
 //    Each neuron's u and x1 are computed entirely inside one CTA in a fixed order: deterministic.
-//  * KB (down, static): the compact active list (tile segments, prefix-summed in every CTA) is cut
-//    into R equal ranges; CTA (r, q) streams the W_down rows of range r, column part q (d / Q
-//    columns, so y stays in <= 32 registers per thread), accumulates y_r = sum_j x1_j W_down[j] in
-//    fp32 in list order, writes the partial, and after a grid barrier every CTA sums a slice of the
-//    R partials in fixed order r = 0..R-1 into y: the deterministic two-phase split-K reduction of
-//    the north star. The equal ranges balance the data-dependent work exactly.
+//  * KB (down, static): starts from KA's per-tile mask words while KA drains; the compact active list
+//    (prefix-summed in every CTA) is cut into R equal ranges; CTA (r, q) streams the W_down rows of
+//    range r, column part q, accumulates y_r = sum_j x1_j W_down[j] in fp32 in list order (CUDA
+//    cores for b <= 3; for b >= 4 MMA with W_down^T via ldmatrix.trans and x1 as exact bf16 hi + lo),
+//    writes the partial, and after a grid barrier every CTA sums a slice of the R partials in fixed
+//    order r = 0..R-1 into y: the deterministic two-phase split-K reduction of the north star. The
+//    equal ranges balance the data-dependent work exactly.
 //
 // KA -> KB -> next decode run as programmatic dependent launches: a kernel's CTAs become resident
 // while its predecessor drains and wait (griddepcontrol.wait) only before touching its outputs.
