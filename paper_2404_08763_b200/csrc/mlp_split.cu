@@ -477,7 +477,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     constexpr int EB = EPT * (int)sizeof(T);  // bytes of a thread's columns in one row (8 or 16)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nth = blockDim.x, NCW = nth / 32 - 1, NCt = NCW * 32;  // consumer warps / threads
-    const int rr = blockIdx.x / Q, q = blockIdx.x % Q;
+    const int q = blockIdx.x % Q;  // column part; the range index rr is taken in arrival order below
     const int part_cols = d / Q;
     const uint32_t seg_bytes = (uint32_t)part_cols * (uint32_t)sizeof(T);
     const uint32_t sst = seg_bytes + 16u;  // stage row stride (padded: conflict-free ldmatrix)
@@ -493,6 +493,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     int *lpos = lj + maxr;                                                                    // [maxr]
     float *lx = reinterpret_cast<float *>(lpos + maxr);                                       // [maxr][B]
     uint8_t *rowm = reinterpret_cast<uint8_t *>(lx + (size_t)maxr * B);                       // [ntiles]
+    __shared__ int s_rr;
 
     trace_stamp(trace, 1, 0);
     pdl_launch_dependents();
@@ -561,8 +562,17 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     }
     __syncthreads();
     trace_stamp(trace, 1, 6);
+    // Ranges in ARRIVAL order with tapered sizes: KB's CTAs become resident as KA's CTAs drain (a few
+    // us apart), so the r-th CTA of part q to arrive takes range r, and range sizes shrink linearly
+    // (weights 4R - r : 4R - r ... about +-14%) so that late arrivals finish with the early ones. The
+    // boundaries are a fixed function of (U, R) and the partials are summed in range order: which CTA
+    // computes which range does not change a bit of y.
+    if (tid == 0) s_rr = (int)atomicAdd(&sched[8 + q], 1u);
+    __syncthreads();
+    const int rr = s_rr;
     const long long U = pre[ntiles];
-    const int lo = (int)(U * rr / R), hi = (int)(U * (rr + 1) / R), len = hi - lo;
+    auto wcum = [R](long long r) { return r * (4LL * R + 1) - r * (r - 1) / 2; };  // sum_{i<r} (4R - i)
+    const int lo = (int)(U * wcum(rr) / wcum(R)), hi = (int)(U * wcum(rr + 1) / wcum(R)), len = hi - lo;
 
     // ---- this range's neurons: compact rank g -> (tile, k) by binary search; neuron = k-th set row ----
     for (int i = tid; i < len; i += nth) {
@@ -723,6 +733,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     __syncthreads();
     trace_stamp(trace, 1, 3);
     for (int i = blockIdx.x * nth + tid; i < ntiles; i += gridDim.x * nth) tmask[i] = 0u;  // for the next call
+    if (blockIdx.x == 0 && tid < Q) sched[8 + tid] = 0u;  // arrival tickets (every CTA took one before the barrier)
 
     // ---- fixed-order reduction: y[e] = sum_{r=0..R-1} part[r][e], this CTA's slice of B*d ----
     {
@@ -809,9 +820,10 @@ static int split_kb_rows_per_stage(const PlanData &p, int b) {
     const size_t seg = (size_t)split_part_cols(p, b) * p.esize;
     return (int)std::max<size_t>(1, std::min<size_t>(32, (32 * 1024) / seg));
 }
-static int split_kb_maxr(const PlanData &p, int b) {
-    const int R = split_ranges(p, b);
-    return (p.m + R - 1) / R + 1;
+static int split_kb_maxr(const PlanData &p, int b) {  // the largest (first) tapered range, + rounding
+    const long long R = split_ranges(p, b);
+    const long long wtot = R * (4 * R + 1) - R * (R - 1) / 2;
+    return (int)(((long long)p.m * 4 * R + wtot - 1) / wtot) + 2;
 }
 size_t split_kb_smem(const PlanData &p, int b, int stages) {
     const size_t seg = (size_t)split_part_cols(p, b) * p.esize + 16;  // padded rows
