@@ -325,6 +325,8 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.esize = esize;
         p.vec = 16 / esize;
         p.nchunks = d * esize / 16;
+        const char *abl = std::getenv("CATS_ABLATION_PREDICATED");
+        p.ablation_predicated = abl && abl[0] == '1';
         const char *nrf = std::getenv("CATS_K12_NR");
         p.nr_force = nrf ? std::atoi(nrf) : 0;
         // K12: persistent CTAs pulling NR-row tiles from a global counter
@@ -449,7 +451,8 @@ cudaError_t launch_mlp(const PlanData &p, const void *x, int b, const void *Wg, 
 cats_status_t run_mlp(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd, float t,
                       int dense, float *y, void *ws, cudaStream_t st) {
     cudaError_t e = cudaSetDevice(p.device);
-    if (e == cudaSuccess) e = launch_mlp(p, x, b, Wg, Wu, Wd, t, dense ? kModeDense : kModeCats, y, ws, st, nullptr);
+    const int mode = dense ? kModeDense : (p.ablation_predicated && b == 1 ? kModePredicated : kModeCats);
+    if (e == cudaSuccess) e = launch_mlp(p, x, b, Wg, Wu, Wd, t, mode, y, ws, st, nullptr);
     return cuda_status(e);
 }
 

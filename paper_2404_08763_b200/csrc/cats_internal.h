@@ -26,6 +26,8 @@ constexpr int kMaxStages = 8;
 constexpr int kModeCats = 0;          // CATS_t decode
 constexpr int kModeDense = 1;         // every neuron active (the library's dense MLP)
 constexpr int kModeGateOnly = 2;      // SiLU(x W_gate) only (calibration data collection)
+constexpr int kModePredicated = 3;    // ablation (CATS_ABLATION_PREDICATED=1): CATS y, but every row's W_up /
+                                      // W_down loaded (App. D Alg. 2, mask-predicated, no compaction)
 
 struct PlanData {
     int d, m, max_batch;
@@ -45,6 +47,7 @@ struct PlanData {
     int k12_eager;      // K12 fills every stage with claimed tiles at start (CATS_K12_EAGER)
     int k12_l2pf;       // K12 static tiles per CTA prefetched into L2 at start (CATS_K12_L2PF)
     int nr_force;       // 0 = automatic tile height; 2 / 4 forces it (CATS_K12_NR)
+    bool ablation_predicated;  // CATS_ABLATION_PREDICATED=1: decode in kModePredicated (K12 only)
     size_t off_x1, off_part;  // split path: x1 per compact position [m][max_b]; KB partials [R][max_b][d]
     size_t off_tmask;         // split path: per-tile active-row mask words (KA -> KB), zero between calls
     size_t off_trace, trace_bytes;

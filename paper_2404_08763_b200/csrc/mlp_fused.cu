@@ -271,7 +271,9 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     bits |= (keep ? 1u : 0u) << tk;
                     if (acts && lane < n) acts[(size_t)tk * m + (size_t)(r0 + lane)] = v;
                 }
-                const bool act = (lane < n) && bits != 0u;
+                // (ablation mode: every row of the tile is queued -- the paper's Alg. 2 mask-predicated
+                //  loads at tile granularity; inactive rows carry v = 0, so y is unchanged)
+                const bool act = (lane < n) && (bits != 0u || mode == kModePredicated);
                 const uint32_t bal = __ballot_sync(0xffffffffu, act);
                 const int rank = __popc(bal & ((1u << lane) - 1u));
                 const int nact = __popc(bal);
