@@ -57,6 +57,9 @@ def _load():
             lib.oracle_mlp.restype = ctypes.c_int
             lib.oracle_mlp.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                        P, P, P, P, ctypes.c_double, ctypes.c_int, P, P, P, P]
+            lib.oracle_xsparse_gemv.restype = ctypes.c_int
+            lib.oracle_xsparse_gemv.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, P, P,
+                                                ctypes.c_double, P, P]
             lib.oracle_rank.restype = ctypes.c_uint64
             lib.oracle_rank.argtypes = [ctypes.c_double, ctypes.c_uint64]
             lib.oracle_calibrate_sort.restype = ctypes.c_int
@@ -126,6 +129,30 @@ def mlp(x: np.ndarray, Wg: np.ndarray, Wu: np.ndarray, Wd: np.ndarray, t: float,
     if rc != 0:
         raise ValueError(f"oracle_mlp failed ({rc})")
     return y, v, keep
+
+
+def xsparse_gemv(x: np.ndarray, W: np.ndarray, t: float):
+    """App. B attention-input CATS: y = CATS_t(x) W per token (Eq. 4 on x itself).
+
+    x: [b][d_in]; W: input-major [d_in][d_out]; both float32 or both uint16 (bf16 bits).
+    Returns (y [b][d_out] float64, keep [b][d_in] uint8).
+    """
+    x = np.ascontiguousarray(x)
+    if x.ndim == 1:
+        x = x[None, :]
+    W = np.ascontiguousarray(W)
+    dt = _dtype_code(x)
+    if _dtype_code(W) != dt:
+        raise TypeError("x and W must share a dtype")
+    b, d_in = x.shape
+    assert W.shape[0] == d_in
+    d_out = W.shape[1]
+    y = np.zeros((b, d_out), dtype=np.float64)
+    keep = np.zeros((b, d_in), dtype=np.uint8)
+    rc = _load().oracle_xsparse_gemv(d_in, d_out, b, dt, _ptr(x), _ptr(W), float(t), _ptr(y), _ptr(keep))
+    if rc != 0:
+        raise ValueError(f"oracle_xsparse_gemv failed ({rc})")
+    return y, keep
 
 
 def rank(k: float, n: int) -> int:

@@ -130,6 +130,27 @@ int oracle_mlp(int64_t d, int64_t m, int64_t b, int dtype,
     return 0;
 }
 
+/* App. B: CATS applied to the hidden vector before the attention projections,
+ * CATS_t(x) (Eq. 4, applied to x itself: no SiLU), followed by the projection
+ * y = CATS_t(x) W, W stored input-major [d_in][d_out] (row i = the weights input i feeds).
+ * Per token: keep_i = |x_i| >= t (ties kept, G1); y_n = sum over kept i, ascending, of x_i W[i][n].
+ * fp64 accumulation of the exactly widened inputs. keep_out [b][d_in] may be NULL. */
+int oracle_xsparse_gemv(int64_t d_in, int64_t d_out, int64_t b, int dtype, const void *x, const void *W,
+                        double t, double *y_out, uint8_t *keep_out) {
+    if (d_in <= 0 || d_out <= 0 || b <= 0 || (dtype != ORACLE_F32 && dtype != ORACLE_BF16)) return -1;
+    for (int64_t bt = 0; bt < b; ++bt) {
+        for (int64_t n = 0; n < d_out; ++n) y_out[bt * d_out + n] = 0.0;
+        for (int64_t i = 0; i < d_in; ++i) {
+            const double xi = widen(x, (uint64_t)(bt * d_in + i), dtype);
+            const int keep = fabs(xi) >= t;
+            if (keep_out) keep_out[bt * d_in + i] = (uint8_t)keep;
+            if (!keep) continue;
+            for (int64_t n = 0; n < d_out; ++n) y_out[bt * d_out + n] += xi * widen(W, (uint64_t)(i * d_out + n), dtype);
+        }
+    }
+    return 0;
+}
+
 /* Eq. 3 rank: t = min{t' : F(t') >= k}, F the empirical CDF of N
  * magnitudes. F(a_(r)) = r/N >= k  <=>  r >= k N, so the answer is the r-th smallest
  * magnitude with r = ceil(k N), computed exactly on the binary value of the double k

@@ -384,3 +384,48 @@ def test_nonfinite_rejected():
     bits = cats_synth.bf16_bits(torch.tensor([0.5, float("nan")], dtype=torch.bfloat16))
     with pytest.raises(FloatingPointError):
         oracle.calibrate_bf16_counts(oracle.bf16_counts(bits), 0.5)
+
+
+# ------------------------------------------------------ App. B: CATS before the attention projections
+
+def test_xsparse_gemv_worked_example():
+    """CATS_t(x) (Eq. 4, applied to the hidden vector, App. B) then x W: with
+    x = (1, -0.2, 0.5, 0.05), t = 0.3 only inputs 0 and 2 survive, so y = W[0] + 0.5 W[2]
+    (computed by hand for W[i][n] = 3 i + n)."""
+    x = np.array([[1.0, -0.2, 0.5, 0.05]], np.float32)
+    W = np.arange(12, dtype=np.float32).reshape(4, 3)
+    y, keep = oracle.xsparse_gemv(x, W, 0.3)
+    assert keep.tolist() == [[1, 0, 1, 0]]
+    assert y.tolist() == [[3.0, 4.5, 6.0]]
+    y_tie, keep_tie = oracle.xsparse_gemv(x, W, 0.5)   # |x_2| = t: kept (ties, reading G1)
+    assert keep_tie.tolist() == [[1, 0, 1, 0]]
+
+
+def test_xsparse_gemv_t0_is_the_dense_product_and_masking_is_exact():
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((3, 40)).astype(np.float32)
+    W = rng.standard_normal((40, 24)).astype(np.float32)
+    y0, k0 = oracle.xsparse_gemv(x, W, 0.0)
+    assert k0.all()
+    np.testing.assert_allclose(y0, x.astype(np.float64) @ W.astype(np.float64), rtol=1e-12, atol=1e-12)
+    t = 0.8
+    y, keep = oracle.xsparse_gemv(x, W, t)
+    assert (keep == (np.abs(x.astype(np.float64)) >= t)).all()
+    np.testing.assert_allclose(y, (x.astype(np.float64) * keep) @ W.astype(np.float64), rtol=1e-12, atol=1e-12)
+    y_hi, k_hi = oracle.xsparse_gemv(x, W, float(np.abs(x).max()) * 2)
+    assert not k_hi.any() and not y_hi.any()
+
+
+def test_xsparse_gemv_brute_force_rationals():
+    from fractions import Fraction
+    rng = np.random.default_rng(6)
+    for _ in range(20):
+        x = (rng.integers(-8, 9, size=(2, 5)) / 8).astype(np.float32)
+        W = (rng.integers(-8, 9, size=(5, 3)) / 4).astype(np.float32)
+        t = float(rng.integers(0, 8) / 8)
+        y, _ = oracle.xsparse_gemv(x, W, t)
+        for bt in range(2):
+            for n in range(3):
+                exact = sum((Fraction(float(x[bt, i])) * Fraction(float(W[i, n])) for i in range(5)
+                             if abs(Fraction(float(x[bt, i]))) >= Fraction(t)), Fraction(0))
+                assert Fraction(y[bt, n]) == exact
