@@ -15,7 +15,8 @@ Recipe:
   * all weights NEURON-MAJOR [m][d] (HF gate_proj.weight, up_proj.weight, down_proj.weight.T)
   * calibration activations: i.i.d. N(0, sigma^2) (heavy: sigma * t_3/sqrt(3)), rounded to
     the requested dtype; the quantile only depends on the multiset of bit patterns.
-Seeds: 0 calibration, 1 decode tokens, 2/3/4 W_gate/W_up/W_down, +1000*layer per layer.
+  * App. B projections: W input-major [d_in][d_out] ~ N(0, 1/d_in); attention inputs are tokens x
+Seeds: 0 calibration, 1 decode tokens, 2/3/4 W_gate/W_up/W_down, 5 App. B W, +1000*layer per layer.
 """
 from __future__ import annotations
 
@@ -67,6 +68,14 @@ def mlp_weights(d: int, m: int, dtype=torch.bfloat16, layer: int = 0, heavy: boo
     wu = torch.randn((m, d), generator=gu, dtype=torch.float32) / math.sqrt(d)
     wd = torch.randn((m, d), generator=gd, dtype=torch.float32) / math.sqrt(d)
     return wg.to(dtype).contiguous(), wu.to(dtype).contiguous(), wd.to(dtype).contiguous()
+
+
+def attn_weights(d_in: int, d_out: int, dtype=torch.bfloat16, layer: int = 0):
+    """App. B projection weights, INPUT-major [d_in][d_out] (q/k/v_proj.weight.T concatenated along
+    d_out), rows ~ N(0, 1/d_in). Seed 5 + 1000*layer."""
+    g = _gen(5 + 1000 * layer)
+    w = torch.randn((d_in, d_out), generator=g, dtype=torch.float32) / math.sqrt(d_in)
+    return w.to(dtype).contiguous()
 
 
 def calib_acts(n: int, dtype=torch.bfloat16, seed: int = 0, sigma: float = SIGMA_U, heavy: bool = False,

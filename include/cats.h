@@ -246,6 +246,36 @@ cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const void *ws, 
  * Errors: CATS_E_NULL, CATS_E_BATCH (b outside [1, max_batch]). Host-only. */
 cats_status_t cats_mlp_kernels_per_call(const cats_mlp_plan_t *plan, int b, int *kernels);
 
+/* ---- App. B: CATS on the attention input -------------------------------------------
+ * y[b][d_out] = CATS_t(x) W for x[b][d_in], CATS_t(x)_i = x_i if |x_i| >= t else 0 (Eq. 4 applied
+ * to the hidden vector itself, ties kept), W stored INPUT-major [d_in][d_out] row-major (row i = the
+ * weights input i feeds, i.e. the transpose of a q/k/v_proj weight; several projections sharing
+ * the input may be concatenated along d_out). Only the rows of inputs kept for at least one of the
+ * b tokens are read from HBM.
+ * The plan is a cats_mlp_plan_t of a second kind: cats_mlp_plan_destroy / _info / _workspace_bytes /
+ * _workspace_init / _last_active / _kernels_per_call accept it (last_active reports the kept INPUT
+ * dimensions); the gated-MLP calls reject it with CATS_E_UNSUPPORTED, and cats_xsparse_gemv rejects
+ * a gated-MLP plan the same way.
+ * cats_mlp_plan_info on this kind: grid = CTAs, rows_per_tile = cluster size (ranges of the kept
+ * list per column slab), stages = clusters resident at once (-1 when planned without a device),
+ * smem = dynamic shared memory at max_batch.
+ * Errors of _plan_create: as cats_mlp_plan_create (d_out plays d: d_out * esize % 16 == 0;
+ * CATS_E_UNSUPPORTED when x [max_batch][d_in] does not fit in shared memory: b x d_in x esize
+ * above ~200 KB). */
+cats_status_t cats_xsparse_plan_create(int d_in, int d_out, int max_batch, cats_dtype_t w_dtype, int device,
+                                       int num_sms, cats_mlp_plan_t **out);
+/* x [b][d_in] (w_dtype), W_in_major [d_in][d_out] (w_dtype), y [b][d_out] fp32, all device memory
+ * with 16-byte aligned bases; t >= 0 finite (t = 0 keeps every input: the dense GEMV).
+ * ONE launch on s (DESIGN.md §5 XS, thread-block clusters + programmatic dependent launch): every CTA
+ * thresholds x and ranks the kept inputs; the CTAs of a cluster stream equal ranges of the kept rows
+ * for one slab of output columns and sum their partials in rank order through distributed shared
+ * memory: bit-identical y for identical inputs. The workspace holds only the introspection bytes
+ * (no state between calls; cats_mlp_workspace_init only zeroes the scheduler words). Asynchronous.
+ * Errors: CATS_E_NULL, CATS_E_UNSUPPORTED (plan kind), CATS_E_BATCH, CATS_E_WORKSPACE, CATS_E_ALIGN,
+ *         CATS_E_THRESHOLD (t < 0, NaN or Inf), CATS_E_CUDA. */
+cats_status_t cats_xsparse_gemv(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_in_major,
+                                float t, float *y, void *ws, size_t ws_bytes, cats_stream_t s);
+
 /* Diagnostics. When the environment variable CATS_TRACE=1 is set at plan creation, the kernels
  * record %globaltimer stamps (ns) per CTA into a trace area of the workspace:
  * uint64 trace[3][512 CTAs][8 slots] at byte `offset` (bytes = 0 when tracing is off).

@@ -20,6 +20,7 @@ __all__ = [
     "cats_calib_window_init", "cats_calib_hist", "cats_calib_step", "cats_mlp_decode", "cats_mlp_dense",
     "cats_mlp_decode_profiled",
     "cats_mlp_decode_host", "cats_mlp_gate_act", "cats_mlp_last_active", "cats_mlp_kernels_per_call", "library_path",
+    "XsparsePlan", "cats_xsparse_gemv",
 ]
 
 
@@ -132,14 +133,17 @@ def cats_calib_step(hist_host: np.ndarray, counts_host: np.ndarray, n: int, dtyp
 class MlpPlan:
     """Host-only plan for one MLP shape (d, m) -- see cats_mlp_plan_create."""
 
+    _create = "cats_mlp_plan_create"
+
     def __init__(self, d: int, m: int, max_batch: int = 1, dtype: torch.dtype = torch.bfloat16, device: int = 0,
                  num_sms: int = 0):
         self._lib = _lib.load()
         self._h = ctypes.c_void_p()
         self.dtype = dtype
         dt = CATS_BF16 if dtype == torch.bfloat16 else CATS_F32
-        _check(self._lib.cats_mlp_plan_create(int(d), int(m), int(max_batch), dt, int(device), int(num_sms),
-                                              ctypes.byref(self._h)), "cats_mlp_plan_create")
+        args = (int(m), int(d)) if self._create == "cats_xsparse_plan_create" else (int(d), int(m))
+        _check(getattr(self._lib, self._create)(*args, int(max_batch), dt, int(device), int(num_sms),
+                                                ctypes.byref(self._h)), self._create)
         info = PlanInfo()
         _check(self._lib.cats_mlp_plan_info(self._h, ctypes.byref(info)), "cats_mlp_plan_info")
         self.info = {f: getattr(info, f) for f, _ in PlanInfo._fields_}
@@ -160,11 +164,23 @@ class MlpPlan:
         _check(rc, "cats_mlp_workspace_init")
         return ws
 
-    def __del__(self):
+    def __del__(self, _void_p=ctypes.c_void_p):  # bound early: module globals may be gone at exit
         h = getattr(self, "_h", None)
         if h is not None and h.value:
             self._lib.cats_mlp_plan_destroy(h)
-            self._h = ctypes.c_void_p()
+            self._h = _void_p()
+
+
+class XsparsePlan(MlpPlan):
+    """Host-only plan for one App. B input-sparse projection d_in -> d_out (cats_xsparse_plan_create).
+    plan.d = d_out (the output width), plan.m = d_in (the thresholded inputs)."""
+
+    _create = "cats_xsparse_plan_create"
+
+    def __init__(self, d_in: int, d_out: int, max_batch: int = 1, dtype: torch.dtype = torch.bfloat16,
+                 device: int = 0, num_sms: int = 0):
+        super().__init__(d_out, d_in, max_batch, dtype, device, num_sms)
+        self.d_in, self.d_out = d_in, d_out
 
 
 def _prep(plan: MlpPlan, x: torch.Tensor, y, ws):
@@ -185,6 +201,15 @@ def cats_mlp_decode(plan: MlpPlan, x, W_gate, W_up, W_down_nm, t: float, y=None,
                                    _dev_ptr(W_up, "W_up"), _dev_ptr(W_down_nm, "W_down_nm"), float(t),
                                    _dev_ptr(y, "y"), _dev_ptr(ws, "ws"), ws.numel(), _stream(stream, x.device))
     _check(rc, "cats_mlp_decode")
+    return y
+
+
+def cats_xsparse_gemv(plan: XsparsePlan, x, W_in_major, t: float, y=None, ws=None, stream=None):
+    """y[b][d_out] (fp32) = CATS_t(x) W for x[b][d_in]; W input-major [d_in][d_out] (App. B)."""
+    x, b, y, ws = _prep(plan, x, y, ws)
+    rc = plan._lib.cats_xsparse_gemv(plan.handle, _dev_ptr(x, "x"), b, _dev_ptr(W_in_major, "W_in_major"), float(t),
+                                     _dev_ptr(y, "y"), _dev_ptr(ws, "ws"), ws.numel(), _stream(stream, x.device))
+    _check(rc, "cats_xsparse_gemv")
     return y
 
 

@@ -61,6 +61,8 @@ _SIGS = {
     "cats_mlp_last_active": (I, [P, P, I, P, P, P, P, P]),
     "cats_mlp_trace_info": (I, [P, P, P]),
     "cats_mlp_kernels_per_call": (I, [P, I, P]),
+    "cats_xsparse_plan_create": (I, [I, I, I, I, I, I, P]),
+    "cats_xsparse_gemv": (I, [P, P, I, P, F, P, P, SZ, P]),
 }
 
 

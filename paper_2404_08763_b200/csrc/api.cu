@@ -302,14 +302,17 @@ cudaError_t ensure_smem_attr(const void *func, size_t smem) {
 
 }  // namespace cats
 
-extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_dtype_t dt, int device, int num_sms,
-                                              cats_mlp_plan_t **out) {
+namespace {
+// kind 0: gated-MLP plan (d, m); kind 1: App. B input-sparse projection plan (d = d_out, m = d_in)
+cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int device, int num_sms, int kind,
+                          cats_mlp_plan_t **out) {
     if (!out) return CATS_E_NULL;
     if (d <= 0 || m <= 0) return CATS_E_SHAPE;
     if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
     if (max_batch < 1 || max_batch > CATS_MAX_BATCH) return CATS_E_BATCH;
     const int esize = dt == CATS_BF16 ? 2 : 4;
     if (((size_t)d * esize) % 16 != 0) return CATS_E_ALIGN;
+    const bool query_device = num_sms <= 0;
     if (num_sms <= 0) {
         cudaError_t e = cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device);
         if (e != cudaSuccess) return cuda_status(e);
@@ -329,9 +332,73 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         p.ablation_predicated = abl && abl[0] == '1';
         const char *nrf = std::getenv("CATS_K12_NR");
         p.nr_force = nrf ? std::atoi(nrf) : 0;
-        // K12: persistent CTAs pulling NR-row tiles from a global counter
+        p.kind = kind;
         p.g1 = 0;
+        if (kind == 1) {  // App. B: kernel XS only (xsparse.cu)
+            // column parts of C = 16 * nch / esize columns (nch | 32 threads per row segment), clusters of
+            // R <= 8 ranges of the kept list: the most CTAs up to `cps` per SM, ties to the widest segment;
+            // segments under 128 B only when no wider one divides d_out. Two CTAs per SM unless x (staged
+            // in shared memory) needs the whole SM.
+            bool fits = false;
+            for (int cps = 2; cps >= 1 && !fits; --cps) {
+                const int slots = cps * num_sms;
+                const size_t budget = cps == 2 ? kXsSmemBudget : kSmemBudget;
+                int best = 0;
+                bool wide_ok = false;  // some segment of >= 128 B divides d_out
+                for (int nch = 32; nch >= 1; nch /= 2) {
+                    const int c = 16 * nch / esize;
+                    if (d % c != 0 || (nch < 8 && wide_ok)) continue;
+                    if (nch >= 8) wide_ok = true;
+                    PlanData cand = p;
+                    cand.xs_cols = c;
+                    cand.xs_q = d / c;
+                    cand.xs_r = std::max(1, std::min(8, slots / cand.xs_q));
+                    const int qr = cand.xs_q * cand.xs_r;
+                    const int score = qr <= slots ? qr : 1;  // Q alone over a wave: last resort
+                    if (score > best && xs_smem_bytes(cand, max_batch) <= budget) {
+                        best = score;
+                        p.xs_cols = cand.xs_cols;
+                        p.xs_q = cand.xs_q;
+                        p.xs_r = cand.xs_r;
+                    }
+                }
+                fits = best > 0;
+            }
+            if (!fits) return CATS_E_UNSUPPORTED;
+            const char *xc = std::getenv("CATS_XS_COLS"), *xr = std::getenv("CATS_XS_R");  // experiments
+            if (xc && std::atoi(xc) > 0 && d % std::atoi(xc) == 0 && (std::atoi(xc) * esize) % 16 == 0 &&
+                std::atoi(xc) * esize <= 512) {
+                p.xs_cols = std::atoi(xc);
+                p.xs_q = d / p.xs_cols;
+            }
+            if (xr && std::atoi(xr) >= 1 && std::atoi(xr) <= 8) p.xs_r = std::atoi(xr);
+            if (xs_smem_bytes(p, max_batch) > kSmemBudget) return CATS_E_UNSUPPORTED;
+            // with a device: shrink the clusters until every one of them is resident at once (the GPCs'
+            // SM counts need not be multiples of the cluster footprint)
+            p.xs_clusters = -1;
+            if (query_device && cudaSetDevice(device) == cudaSuccess) {
+                for (;;) {
+                    p.xs_clusters = xs_active_clusters(p, max_batch);
+                    if (p.xs_clusters < 0 || p.xs_clusters >= p.xs_q || p.xs_r == 1) break;
+                    --p.xs_r;
+                }
+            }
+            size_t off = 0;
+            p.off_sched = off;   off = align_up(off + kSchedBytes, 256);
+            p.off_tokmask = off; off = align_up(off + (size_t)m, 256);  // per-input keep bits (introspection)
+            const char *trc = std::getenv("CATS_TRACE");
+            p.trace = trc && trc[0] == '1';
+            p.off_trace = off;
+            p.trace_bytes = p.trace ? (size_t)kTraceKernels * kTraceCtas * kTraceSlots * 8 : 0;
+            off = align_up(off + p.trace_bytes, 256);
+            p.ws_bytes = off;
+            cats_mlp_plan *plan = new cats_mlp_plan;
+            plan->p = p;
+            *out = plan;
+            return CATS_OK;
+        }
         for (int b = 1; b <= max_batch; ++b) {
+            // K12: persistent CTAs pulling NR-row tiles from a global counter
             if (k12_cpt(p, b) > (b == 1 ? kMaxCPT : 2)) return CATS_E_UNSUPPORTED;
             if (k12_stages(p, b) < 2 || k12_smem_bytes(p, b, k12_stages(p, b)) > k12_smem_budget_c(b))
                 return CATS_E_UNSUPPORTED;
@@ -339,7 +406,7 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         }
         // workspace
         size_t off = 0;
-        p.off_sched = off;   off = align_up(off + 64, 256);
+        p.off_sched = off;   off = align_up(off + kSchedBytes, 256);
         p.off_idx = off;     off = align_up(off + (size_t)m * 4, 256);
         p.off_tokmask = off; off = align_up(off + (size_t)m, 256);
         p.off_vals = off;    off = align_up(off + (size_t)m * max_batch * 4, 256);
@@ -381,6 +448,30 @@ extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_
         return CATS_OK;
     })
 }
+}  // namespace
+
+extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_dtype_t dt, int device, int num_sms,
+                                              cats_mlp_plan_t **out) {
+    return plan_create(d, m, max_batch, dt, device, num_sms, 0, out);
+}
+
+extern "C" cats_status_t cats_xsparse_plan_create(int d_in, int d_out, int max_batch, cats_dtype_t dt, int device,
+                                                  int num_sms, cats_mlp_plan_t **out) {
+    return plan_create(d_out, d_in, max_batch, dt, device, num_sms, 1, out);
+}
+
+extern "C" cats_status_t cats_xsparse_gemv(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_in_major,
+                                           float t, float *y, void *ws, size_t ws_bytes, cats_stream_t s) {
+    if (!plan || !x || !W_in_major || !y) return CATS_E_NULL;
+    if (plan->p.kind != 1) return CATS_E_UNSUPPORTED;
+    if (b < 1 || b > plan->p.max_batch) return CATS_E_BATCH;
+    if (!ws || ws_bytes < plan->p.ws_bytes) return CATS_E_WORKSPACE;
+    if (!aligned16(x) || !aligned16(W_in_major) || !aligned16(y) || !aligned16(ws)) return CATS_E_ALIGN;
+    if (!(t >= 0.0f) || std::isinf(t)) return CATS_E_THRESHOLD;
+    cudaError_t e = cudaSetDevice(plan->p.device);
+    if (e == cudaSuccess) e = launch_xsparse(plan->p, x, b, W_in_major, t, y, ws, static_cast<cudaStream_t>(s));
+    return cuda_status(e);
+}
 
 extern "C" void cats_mlp_plan_destroy(cats_mlp_plan_t *plan) { delete plan; }
 
@@ -394,11 +485,19 @@ extern "C" cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_ml
     info->w_dtype = p.dt;
     info->device = p.device;
     info->num_sms = p.num_sms;
-    info->grid = k12_grid(p, b);
-    info->threads = k12_threads_c(b);
-    info->rows_per_tile = k12_rows_per_tile(p, b);
-    info->stages = k12_stages(p, b);
-    info->smem = k12_smem_bytes(p, b, info->stages);
+    if (p.kind == 1) {  // kernel XS: Q x R CTAs (clusters of R), W rows per ring stage
+        info->grid = p.xs_q * p.xs_r;
+        info->threads = kXsThreads;
+        info->rows_per_tile = p.xs_r;  // cluster size: ranges of the kept list per column part
+        info->stages = p.xs_clusters;  // clusters resident at once (-1: planned without a device)
+        info->smem = xs_smem_bytes(p, b);
+    } else {
+        info->grid = k12_grid(p, b);
+        info->threads = k12_threads_c(b);
+        info->rows_per_tile = k12_rows_per_tile(p, b);
+        info->stages = k12_stages(p, b);
+        info->smem = k12_smem_bytes(p, b, info->stages);
+    }
     info->workspace_bytes = p.ws_bytes;
     return CATS_OK;
 }
@@ -415,8 +514,9 @@ extern "C" cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, vo
     if (!ws || ws_bytes < plan->p.ws_bytes) return CATS_E_WORKSPACE;
     if (!aligned16(ws)) return CATS_E_ALIGN;
     cudaError_t e = cudaSetDevice(plan->p.device);
-    if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_sched, 0, 64,
+    if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_sched, 0, kSchedBytes,
                                               static_cast<cudaStream_t>(s));
+    if (plan->p.kind == 1) return cuda_status(e);  // XS keeps no state between calls
     if (e == cudaSuccess)
         e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_ypart, 0, (size_t)plan->p.max_batch * plan->p.d * 8,
                             static_cast<cudaStream_t>(s));
@@ -432,6 +532,7 @@ namespace {
 cats_status_t validate_common(const cats_mlp_plan_t *plan, const void *x, int b, const void *a, const void *bptr,
                               const void *c, const void *y, const void *ws, size_t ws_bytes) {
     if (!plan || !x || !a || !bptr || !c || !y) return CATS_E_NULL;
+    if (plan->p.kind != 0) return CATS_E_UNSUPPORTED;  // an input-sparse projection plan
     if (b < 1 || b > plan->p.max_batch) return CATS_E_BATCH;
     if (!ws || ws_bytes < plan->p.ws_bytes) return CATS_E_WORKSPACE;
     if (!aligned16(x) || !aligned16(a) || !aligned16(bptr) || !aligned16(c) || !aligned16(y) || !aligned16(ws))
@@ -549,6 +650,25 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
     CATS_TRY({
         cudaStream_t st = static_cast<cudaStream_t>(s);
         const char *w = static_cast<const char *>(ws);
+        if (p.kind == 1) {  // XS: one keep-bit byte per input, written by CTA 0
+            std::vector<uint8_t> kin(p.m);
+            cudaError_t e = cudaSetDevice(p.device);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(kin.data(), w + p.off_tokmask, (size_t)p.m, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) return cuda_status(e);
+            uint32_t k = 0;
+            if (nnz_per_token) std::fill(nnz_per_token, nnz_per_token + b, 0u);
+            for (int i = 0; i < p.m; ++i) {
+                if (!kin[i]) continue;
+                idx_host[k] = i;
+                tokmask_host[k] = kin[i];
+                if (nnz_per_token)
+                    for (int tk = 0; tk < b; ++tk) nnz_per_token[tk] += (kin[i] >> tk) & 1u;
+                ++k;
+            }
+            *nnz_union = k;
+            return CATS_OK;
+        }
         const int tr = k12_rows_per_tile(p, b), ntiles = k12_ntiles(p, b);
         std::vector<int32_t> idx(p.m), cnt(ntiles);
         std::vector<uint8_t> tm(p.m);
@@ -580,7 +700,7 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
 extern "C" cats_status_t cats_mlp_kernels_per_call(const cats_mlp_plan_t *plan, int b, int *kernels) {
     if (!plan || !kernels) return CATS_E_NULL;
     if (b < 1 || b > plan->p.max_batch) return CATS_E_BATCH;
-    *kernels = (b >= plan->p.split_min_b && split_supported(plan->p, b)) ? 2 : 1;
+    *kernels = plan->p.kind == 1 ? 1 : (b >= plan->p.split_min_b && split_supported(plan->p, b)) ? 2 : 1;
     return CATS_OK;
 }
 

@@ -47,6 +47,9 @@ struct PlanData {
     int k12_eager;      // K12 fills every stage with claimed tiles at start (CATS_K12_EAGER)
     int k12_l2pf;       // K12 static tiles per CTA prefetched into L2 at start (CATS_K12_L2PF)
     int nr_force;       // 0 = automatic tile height; 2 / 4 forces it (CATS_K12_NR)
+    int kind;           // 0 = gated-MLP plan, 1 = App. B input-sparse projection plan (d = d_out, m = d_in)
+    int xs_cols, xs_q, xs_r;  // kind 1 (xsparse.cu): columns per CTA, column parts, cluster size
+    int xs_clusters;          // kind 1: clusters resident at once at max_batch (-1: planned without a device)
     bool ablation_predicated;  // CATS_ABLATION_PREDICATED=1: decode in kModePredicated (K12 only)
     size_t off_x1, off_part;  // split path: x1 per compact position [m][max_b]; KB partials [R][max_b][d]
     size_t off_tmask;         // split path: per-tile active-row mask words (KA -> KB), zero between calls
@@ -107,7 +110,15 @@ constexpr int kSplitMmaMinB = 4;  // batches from which KA / KB use warp-level b
 inline bool split_kb_mma(const PlanData &p, int b) {  // instantiated for 1, 4, 5 tiles per warp
     return b >= kSplitMmaMinB && p.esize == 2 && (p.d == 1024 || p.d == 4096 || p.d == 5120);
 }
-inline int split_q(const PlanData &p, int b) { return split_kb_mma(p, b) ? 4 : 2; }  // KB column parts
+// scheduler words at the workspace base: [0..1] tile counter / CTA exits, [2] KB grid barrier,
+// [8 + q] KB arrival tickets of column part q (q < 16)
+constexpr size_t kSchedBytes = 128;
+inline int split_q(const PlanData &p, int b) {  // KB column parts (<= 16)
+    if (split_kb_mma(p, b)) return 4;
+    for (int q = 2; q <= 16; ++q)  // CUDA-core path: <= 640 consumer threads of 4 columns each
+        if (p.d % (4 * q) == 0 && ((size_t)(p.d / q) * p.esize) % 16 == 0 && p.d / q / 4 <= 640) return q;
+    return 2;
+}
 inline int split_ept(const PlanData &, int) { return 4; }  // KB (FFMA path) columns per thread
 inline int split_part_cols(const PlanData &p, int b) { return p.d / split_q(p, b); }
 inline int split_kb_mt(const PlanData &p, int b) {  // 16-column MMA tiles per KB warp (0 = FFMA path)
@@ -143,6 +154,20 @@ cudaError_t launch_k12(const PlanData &p, const void *x, int b, const void *Wg, 
 // split path (b >= 2): KA then KB, both PDL launches; ev (optional) = event recorded between them
 cudaError_t launch_split(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd,
                          float t, int mode, float *y, void *ws, cudaStream_t s, cudaEvent_t ev_mid);
+
+// KB alone for batch b (1..8), and the App. B input-sparse projection (KX then KB)
+// ---- App. B input-sparse projection (xsparse.cu): one kernel XS, clusters of xs_r CTAs ----
+constexpr int kXsThreads = 256;
+// W rows in flight per thread: as many as the registers left by the b x 8 accumulators allow (each
+// thread's rows are a latency chain of ceil(rows / unroll) HBM round trips)
+__host__ __device__ constexpr int xs_unroll(int b) { return b <= 2 ? 16 : b <= 4 ? 12 : 8; }
+constexpr size_t kXsSmemBudget = 113 * 1024;  // two CTAs per SM (228 KB less 1 KB reserved per CTA)
+inline int xs_maxr(const PlanData &p) { return (p.m + p.xs_r - 1) / p.xs_r; }  // longest range of the kept list
+size_t xs_smem_bytes(const PlanData &p, int b);
+int xs_active_clusters(const PlanData &p, int b);  // occupancy query (-1 without a device)
+cudaError_t launch_xsparse(const PlanData &p, const void *x, int b, const void *W, float t, float *y, void *ws,
+                           cudaStream_t s);
+bool kb_supported(const PlanData &p, int b);
 
 cudaError_t launch_calib_hist(const void *acts, uint64_t n, cats_dtype_t dt, const cats_calib_window_t &w,
                               uint64_t *hist, uint64_t *counts, cudaStream_t s);

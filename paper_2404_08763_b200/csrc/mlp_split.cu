@@ -843,15 +843,18 @@ int split_kb_stages(const PlanData &p, int b) {
     while (st > 0 && (size_t)st * stage < (size_t)kSplitBMaxThreads * 16) ++st;
     return st;
 }
-bool split_supported(const PlanData &p, int b) {
-    if (b < 2 || b > 8) return false;
+bool kb_supported(const PlanData &p, int b) {  // KB alone fits this shape and batch
+    if (b < 1 || b > 8) return false;
     if (p.d % (split_q(p, b) * split_ept(p, b)) != 0) return false;
     if (((size_t)split_part_cols(p, b) * p.esize) % 16 != 0) return false;
     if (split_kb_consumers(p, b) + 32 > kSplitBMaxThreads) return false;
-    const int sa = split_ka_stages(p, b), sb = split_kb_stages(p, b);
-    if (sa < 2 || split_ka_smem(p, b, sa) > kSmemBudget) return false;  // >= 2 stages per group
-    if (sb < 2 || split_kb_smem(p, b, sb) > kSmemBudget) return false;
-    return true;
+    const int sb = split_kb_stages(p, b);
+    return sb >= 2 && split_kb_smem(p, b, sb) <= kSmemBudget;
+}
+bool split_supported(const PlanData &p, int b) {
+    if (b < 2 || b > 8 || !kb_supported(p, b)) return false;
+    const int sa = split_ka_stages(p, b);
+    return sa >= 2 && split_ka_smem(p, b, sa) <= kSmemBudget;  // >= 2 stages per group
 }
 
 static cudaLaunchConfig_t pdl_config(cudaLaunchAttribute *attr, int grid, int threads, size_t smem,
@@ -910,6 +913,20 @@ static cudaError_t launch_kb(const PlanData &p, const void *Wd, float *y, void *
                               p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
 }
 
+// KB for batch B: tensor-core variant where instantiated (split_kb_mt), else CUDA cores
+template <typename T, int B>
+static cudaError_t launch_kb_b(const PlanData &p, const void *Wd, float *y, void *ws, cudaStream_t s) {
+    constexpr int EPT = 4;  // = split_ept()
+    if constexpr (sizeof(T) == 2 && B >= kSplitMmaMinB) {
+        const int mt = split_kb_mt(p, B);
+        if (mt == 1) return launch_kb<T, B, EPT, 1>(p, Wd, y, ws, s);
+        if (mt == 4) return launch_kb<T, B, EPT, 4>(p, Wd, y, ws, s);
+        if (mt == 5) return launch_kb<T, B, EPT, 5>(p, Wd, y, ws, s);
+        if (mt != 0) return cudaErrorInvalidValue;
+    }
+    return launch_kb<T, B, EPT, 0>(p, Wd, y, ws, s);
+}
+
 template <typename T, int B>
 static cudaError_t launch_split_b(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
                                   float t, int mode, float *y, void *ws, cudaStream_t s, cudaEvent_t ev_mid) {
@@ -928,15 +945,7 @@ static cudaError_t launch_split_b(const PlanData &p, const void *x, const void *
         e = cudaEventRecord(ev_mid, s);
         if (e != cudaSuccess) return e;
     }
-    constexpr int EPT = 4;  // = split_ept()
-    if constexpr (sizeof(T) == 2 && B >= kSplitMmaMinB) {
-        const int mt = split_kb_mt(p, B);
-        if (mt == 1) return launch_kb<T, B, EPT, 1>(p, Wd, y, ws, s);
-        if (mt == 4) return launch_kb<T, B, EPT, 4>(p, Wd, y, ws, s);
-        if (mt == 5) return launch_kb<T, B, EPT, 5>(p, Wd, y, ws, s);
-        if (mt != 0) return cudaErrorInvalidValue;
-    }
-    return launch_kb<T, B, EPT, 0>(p, Wd, y, ws, s);
+    return launch_kb_b<T, B>(p, Wd, y, ws, s);
 }
 
 template <typename T>

@@ -226,3 +226,34 @@ def test_kernels_per_call_path_choice():
     with pytest.raises(cats.CatsError) as e:
         cats.cats_mlp_kernels_per_call(p, 9)
     assert e.value.name == "CATS_E_BATCH"
+
+
+def _xs_rc(plan, x=FAKE, b=1, W=FAKE, t=0.1, y=FAKE, ws=FAKE, wsb=None):
+    wsb = plan.workspace_bytes if wsb is None else wsb
+    return lib.cats_status_string(lib.cats_xsparse_gemv(plan.handle, x, b, W, t, y, ws, wsb, None)).decode()
+
+
+def test_xsparse_plan_and_validation_without_gpu():
+    """App. B plan (d_in -> d_out): host-only planning, argument checks before any CUDA call, and the
+    two plan kinds rejected by each other's entry points."""
+    p = cats.XsparsePlan(4096, 6144, max_batch=8, dtype=torch.bfloat16, num_sms=148)
+    assert (p.d, p.m, p.d_in, p.d_out) == (6144, 4096, 4096, 6144)
+    assert [cats.cats_mlp_kernels_per_call(p, b) for b in range(1, 9)] == [1] * 8  # kernel XS
+    for shape in [(4096, 12288), (5120, 5120), (1001, 264), (64, 64), (8192, 8192)]:
+        cats.XsparsePlan(*shape, max_batch=8, dtype=torch.bfloat16, num_sms=148)
+    with pytest.raises(cats.CatsError) as e:
+        cats.XsparsePlan(4096, 100, max_batch=1, num_sms=148)  # 200-byte rows: not 16-byte aligned
+    assert e.value.name == "CATS_E_ALIGN"
+    assert _xs_rc(p, x=None) == "CATS_E_NULL"
+    assert _xs_rc(p, W=None) == "CATS_E_NULL"
+    assert _xs_rc(p, b=0) == "CATS_E_BATCH"
+    assert _xs_rc(p, b=9) == "CATS_E_BATCH"
+    assert _xs_rc(p, wsb=p.workspace_bytes - 1) == "CATS_E_WORKSPACE"
+    assert _xs_rc(p, W=FAKE + 4) == "CATS_E_ALIGN"
+    assert _xs_rc(p, t=-1.0) == "CATS_E_THRESHOLD"
+    assert _xs_rc(p, t=float("nan")) == "CATS_E_THRESHOLD"
+    mp = cats.MlpPlan(4096, 14336, max_batch=1, dtype=torch.bfloat16, num_sms=148)
+    assert _xs_rc(mp) == "CATS_E_UNSUPPORTED"
+    assert _decode_rc(p) == "CATS_E_UNSUPPORTED"
+    if not torch.cuda.is_available():
+        assert _xs_rc(p) == "CATS_E_CUDA"
