@@ -335,52 +335,51 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.kind = kind;
         p.g1 = 0;
         if (kind == 1) {  // App. B: kernel XS only (xsparse.cu)
-            // column parts of C = 16 * nch / esize columns (nch | 32 threads per row segment), clusters of
-            // R <= 8 ranges of the kept list: the most CTAs up to `cps` per SM, ties to the widest segment;
-            // segments under 128 B only when no wider one divides d_out. Two CTAs per SM unless x (staged
-            // in shared memory) needs the whole SM.
-            bool fits = false;
-            for (int cps = 2; cps >= 1 && !fits; --cps) {
-                const int slots = cps * num_sms;
-                const size_t budget = cps == 2 ? kXsSmemBudget : kSmemBudget;
-                int best = 0;
-                bool wide_ok = false;  // some segment of >= 128 B divides d_out
-                for (int nch = 32; nch >= 1; nch /= 2) {
-                    const int c = 16 * nch / esize;
-                    if (d % c != 0 || (nch < 8 && wide_ok)) continue;
-                    if (nch >= 8) wide_ok = true;
-                    PlanData cand = p;
-                    cand.xs_cols = c;
-                    cand.xs_q = d / c;
-                    cand.xs_r = std::max(1, std::min(8, slots / cand.xs_q));
-                    const int qr = cand.xs_q * cand.xs_r;
-                    const int score = qr <= slots ? qr : 1;  // Q alone over a wave: last resort
-                    if (score > best && xs_smem_bytes(cand, max_batch) <= budget) {
-                        best = score;
-                        p.xs_cols = cand.xs_cols;
-                        p.xs_q = cand.xs_q;
-                        p.xs_r = cand.xs_r;
-                    }
-                }
-                fits = best > 0;
-            }
-            if (!fits) return CATS_E_UNSUPPORTED;
+            // per batch size b: column parts of C = 16 * nch / esize columns (nch | 32 threads per row
+            // segment), clusters of R <= 8 ranges of the kept list; the most CTAs up to `cps` per SM whose
+            // shared memory fits, ties to the widest segment; segments under 128 B only when no wider one
+            // divides d_out. Two CTAs per SM unless x (staged in shared memory) needs the whole SM.
             const char *xc = std::getenv("CATS_XS_COLS"), *xr = std::getenv("CATS_XS_R");  // experiments
-            if (xc && std::atoi(xc) > 0 && d % std::atoi(xc) == 0 && (std::atoi(xc) * esize) % 16 == 0 &&
-                std::atoi(xc) * esize <= 512) {
-                p.xs_cols = std::atoi(xc);
-                p.xs_q = d / p.xs_cols;
-            }
-            if (xr && std::atoi(xr) >= 1 && std::atoi(xr) <= 8) p.xs_r = std::atoi(xr);
-            if (xs_smem_bytes(p, max_batch) > kSmemBudget) return CATS_E_UNSUPPORTED;
-            // with a device: shrink the clusters until every one of them is resident at once (the GPCs'
-            // SM counts need not be multiples of the cluster footprint)
-            p.xs_clusters = -1;
-            if (query_device && cudaSetDevice(device) == cudaSuccess) {
-                for (;;) {
-                    p.xs_clusters = xs_active_clusters(p, max_batch);
-                    if (p.xs_clusters < 0 || p.xs_clusters >= p.xs_q || p.xs_r == 1) break;
-                    --p.xs_r;
+            for (int b = 1; b <= max_batch; ++b) {
+                PlanData::XsCfg &c = p.xs[b];
+                bool fits = false;
+                for (int cps = 2; cps >= 1 && !fits; --cps) {
+                    const int slots = cps * num_sms;
+                    const size_t budget = cps == 2 ? kXsSmemBudget : kSmemBudget;
+                    int best = 0;
+                    bool wide_ok = false;  // some segment of >= 128 B divides d_out
+                    for (int nch = 32; nch >= 1; nch /= 2) {
+                        const int cols = 16 * nch / esize;
+                        if (d % cols != 0 || (nch < 8 && wide_ok)) continue;
+                        if (nch >= 8) wide_ok = true;
+                        const PlanData::XsCfg keep = c;
+                        c.cols = cols;
+                        c.q = d / cols;
+                        c.r = std::max(1, std::min(8, slots / c.q));
+                        const int qr = c.q * c.r;
+                        const int score = qr <= slots ? qr : 1;  // Q alone over a wave: last resort
+                        if (score > best && xs_smem_bytes(p, b) <= budget) best = score;
+                        else c = keep;
+                    }
+                    fits = best > 0;
+                }
+                if (!fits) return CATS_E_UNSUPPORTED;
+                if (xc && std::atoi(xc) > 0 && d % std::atoi(xc) == 0 && (std::atoi(xc) * esize) % 16 == 0 &&
+                    std::atoi(xc) * esize <= 512) {
+                    c.cols = std::atoi(xc);
+                    c.q = d / c.cols;
+                }
+                if (xr && std::atoi(xr) >= 1 && std::atoi(xr) <= 8) c.r = std::atoi(xr);
+                if (xs_smem_bytes(p, b) > kSmemBudget) return CATS_E_UNSUPPORTED;
+                // with a device: shrink the clusters until every one of them is resident at once (the GPCs'
+                // SM counts need not be multiples of the cluster footprint)
+                c.clusters = -1;
+                if (query_device && cudaSetDevice(device) == cudaSuccess) {
+                    for (;;) {
+                        c.clusters = xs_active_clusters(p, b);
+                        if (c.clusters < 0 || c.clusters >= c.q || c.r == 1) break;
+                        --c.r;
+                    }
                 }
             }
             size_t off = 0;
@@ -486,10 +485,10 @@ extern "C" cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_ml
     info->device = p.device;
     info->num_sms = p.num_sms;
     if (p.kind == 1) {  // kernel XS: Q x R CTAs (clusters of R), W rows per ring stage
-        info->grid = p.xs_q * p.xs_r;
+        info->grid = p.xs[b].q * p.xs[b].r;
         info->threads = kXsThreads;
-        info->rows_per_tile = p.xs_r;  // cluster size: ranges of the kept list per column part
-        info->stages = p.xs_clusters;  // clusters resident at once (-1: planned without a device)
+        info->rows_per_tile = p.xs[b].r;  // cluster size: ranges of the kept list per column part
+        info->stages = p.xs[b].clusters;  // clusters resident at once (-1: planned without a device)
         info->smem = xs_smem_bytes(p, b);
     } else {
         info->grid = k12_grid(p, b);

@@ -48,8 +48,10 @@ struct PlanData {
     int k12_l2pf;       // K12 static tiles per CTA prefetched into L2 at start (CATS_K12_L2PF)
     int nr_force;       // 0 = automatic tile height; 2 / 4 forces it (CATS_K12_NR)
     int kind;           // 0 = gated-MLP plan, 1 = App. B input-sparse projection plan (d = d_out, m = d_in)
-    int xs_cols, xs_q, xs_r;  // kind 1 (xsparse.cu): columns per CTA, column parts, cluster size
-    int xs_clusters;          // kind 1: clusters resident at once at max_batch (-1: planned without a device)
+    struct XsCfg {            // kind 1 (xsparse.cu), per batch size b = 1..8:
+        int cols, q, r;       //   columns per CTA, column parts, cluster size (ranges of the kept list)
+        int clusters;         //   clusters resident at once (-1: planned without a device)
+    } xs[9];
     bool ablation_predicated;  // CATS_ABLATION_PREDICATED=1: decode in kModePredicated (K12 only)
     size_t off_x1, off_part;  // split path: x1 per compact position [m][max_b]; KB partials [R][max_b][d]
     size_t off_tmask;         // split path: per-tile active-row mask words (KA -> KB), zero between calls
@@ -156,13 +158,13 @@ cudaError_t launch_split(const PlanData &p, const void *x, int b, const void *Wg
                          float t, int mode, float *y, void *ws, cudaStream_t s, cudaEvent_t ev_mid);
 
 // KB alone for batch b (1..8), and the App. B input-sparse projection (KX then KB)
-// ---- App. B input-sparse projection (xsparse.cu): one kernel XS, clusters of xs_r CTAs ----
+// ---- App. B input-sparse projection (xsparse.cu): one kernel XS, clusters of xs[b].r CTAs ----
 constexpr int kXsThreads = 256;
 // W rows in flight per thread: as many as the registers left by the b x 8 accumulators allow (each
 // thread's rows are a latency chain of ceil(rows / unroll) HBM round trips)
 __host__ __device__ constexpr int xs_unroll(int b) { return b <= 2 ? 16 : b <= 4 ? 12 : 8; }
 constexpr size_t kXsSmemBudget = 113 * 1024;  // two CTAs per SM (228 KB less 1 KB reserved per CTA)
-inline int xs_maxr(const PlanData &p) { return (p.m + p.xs_r - 1) / p.xs_r; }  // longest range of the kept list
+inline int xs_maxr(const PlanData &p, int b) { return (p.m + p.xs[b].r - 1) / p.xs[b].r; }  // longest kept range
 size_t xs_smem_bytes(const PlanData &p, int b);
 int xs_active_clusters(const PlanData &p, int b);  // occupancy query (-1 without a device)
 cudaError_t launch_xsparse(const PlanData &p, const void *x, int b, const void *W, float t, float *y, void *ws,

@@ -270,8 +270,8 @@ xs_gemv(const T *__restrict__ x, const T *__restrict__ W, float *__restrict__ y,
 
 size_t xs_smem_bytes(const PlanData &p, int b) {
     const int nw = (p.m + 31) / 32;
-    const int maxr = xs_maxr(p);
-    const size_t region = std::max((size_t)b * p.m * p.esize, (size_t)(kXsThreads / 32 + p.xs_r) * b * p.xs_cols * 4);
+    const int maxr = xs_maxr(p, b);
+    const size_t region = std::max((size_t)b * p.m * p.esize, (size_t)(kXsThreads / 32 + p.xs[b].r) * b * p.xs[b].cols * 4);
     const int lxs = p.esize == 2 ? (b + 1) & ~1 : b;
     return ((region + 15) & ~(size_t)15) + (size_t)nw * 4 + (size_t)(nw + 1) * 4 +
            (size_t)maxr * 4 + (size_t)maxr * lxs * p.esize;
@@ -288,11 +288,11 @@ static cudaError_t launch_xs_b(const PlanData &p, const void *x, const void *W, 
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = (unsigned)p.xs_r;
+    attr[1].val.clusterDim.x = (unsigned)p.xs[B].r;
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(p.xs_q * p.xs_r));
+    cfg.gridDim = dim3((unsigned)(p.xs[B].q * p.xs[B].r));
     cfg.blockDim = dim3((unsigned)kXsThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -300,7 +300,7 @@ static cudaError_t launch_xs_b(const PlanData &p, const void *x, const void *W, 
     cfg.numAttrs = 2;
     char *w = static_cast<char *>(ws);
     return cudaLaunchKernelEx(&cfg, kern, static_cast<const T *>(x), static_cast<const T *>(W), y, p.m, p.d,
-                              p.xs_cols, t, xs_maxr(p), reinterpret_cast<uint8_t *>(w + p.off_tokmask),
+                              p.xs[B].cols, t, xs_maxr(p, B), reinterpret_cast<uint8_t *>(w + p.off_tokmask),
                               p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
 }
 
@@ -311,11 +311,11 @@ static int xs_active_clusters_b(const PlanData &p) {
     if (ensure_smem_attr(reinterpret_cast<const void *>(kern), smem) != cudaSuccess) return -1;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)p.xs_r;
+    attr[0].val.clusterDim.x = (unsigned)p.xs[B].r;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(p.xs_q * p.xs_r));
+    cfg.gridDim = dim3((unsigned)(p.xs[B].q * p.xs[B].r));
     cfg.blockDim = dim3((unsigned)kXsThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.attrs = attr;
@@ -328,7 +328,7 @@ static int xs_active_clusters_b(const PlanData &p) {
     return n;
 }
 
-// clusters of p.xs_r CTAs of the batch-b kernel that can be resident at once (-1: no device to ask)
+// clusters of p.xs[b].r CTAs of the batch-b kernel that can be resident at once (-1: no device to ask)
 int xs_active_clusters(const PlanData &p, int b) {
     const bool bf = p.dt == CATS_BF16;
     switch (b) {
