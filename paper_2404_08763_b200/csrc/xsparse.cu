@@ -122,7 +122,8 @@ xs_gemv(const T *__restrict__ x, const T *__restrict__ W, float *__restrict__ y,
     // ---- exclusive prefix of the word popcounts, block-wide, 256 words per pass:
     //      woff[w] = kept inputs before word w, woff[NW] = U ----
     __shared__ int wsum[kXsThreads / 32];
-    int carry = 0;
+    __shared__ int s_wr[2];
+    int carry = 0, my_off = 0, my_pc = 0;  // my_*: word tid (kept when NW fits one pass)
     for (int base = 0; base < NW; base += kXsThreads) {
         const int w = base + tid;
         const int pc = w < NW ? __popc(kmask[w]) : 0;
@@ -138,24 +139,47 @@ xs_gemv(const T *__restrict__ x, const T *__restrict__ W, float *__restrict__ y,
 #pragma unroll
         for (int k = 0; k < NW_; ++k) before += k < warp ? wsum[k] : 0;
         if (w < NW) woff[w] = before + incl - pc;
+        my_off = before + incl - pc;
+        my_pc = pc;
 #pragma unroll
         for (int k = 0; k < NW_; ++k) carry += wsum[k];
         __syncthreads();
     }
     if (tid == 0) woff[NW] = carry;
     trace_stamp(trace, 0, 7);
-    // ---- this CTA's range [lo, hi) of the kept list (equal split into csize ranges): the words that
-    //      cover it (binary search on woff), one thread per input ----
+    // ---- this CTA's range [lo, hi) of the kept list (equal split into csize ranges): the words
+    //      [wa, we) that hold its first and last kept input, then one thread per input of those ----
     const long long U = carry;
     const int lo = (int)(U * rank / csize), hi = (int)(U * (rank + 1) / csize), len = hi - lo;
-    int wa = 0, wb = NW;  // wa = last word with woff <= lo
-    while (wb - wa > 1) {
-        const int mid = (wa + wb) >> 1;
-        if (woff[mid] <= lo) wa = mid; else wb = mid;
+    int wa = 0, we = 0;
+    if (NW <= kXsThreads) {  // the owning threads know it from the prefix pass
+        if (tid < NW && my_pc > 0) {
+            if (my_off <= lo && lo < my_off + my_pc) s_wr[0] = tid;
+            if (my_off <= hi - 1 && hi - 1 < my_off + my_pc) s_wr[1] = tid + 1;
+        }
+        __syncthreads();
+        wa = s_wr[0];
+        we = s_wr[1];
+    } else {  // binary searches on woff: last word with woff <= lo, first word with woff >= hi
+        int a = 0, b2 = NW;
+        while (b2 - a > 1) {
+            const int mid = (a + b2) >> 1;
+            if (woff[mid] <= lo) a = mid; else b2 = mid;
+        }
+        wa = a;
+        a = 0, b2 = NW;
+        while (b2 - a > 1) {
+            const int mid = (a + b2) >> 1;
+            if (woff[mid] < hi) a = mid; else b2 = mid;
+        }
+        we = a + 1;
     }
-    for (int i = wa * 32 + tid; i < d_in; i += kXsThreads) {
+    if (len == 0) wa = we = 0;
+    trace_stamp(trace, 1, 0);
+    const int iend = min(we * 32, d_in);
+#pragma unroll 2
+    for (int i = wa * 32 + tid; i < iend; i += kXsThreads) {
         const int w = i >> 5;
-        if (woff[w] >= hi) break;
         const uint32_t m = kmask[w];
         if (!((m >> (i & 31)) & 1u)) continue;
         const int gi = woff[w] + __popc(m & ((1u << (i & 31)) - 1u));
@@ -169,7 +193,9 @@ xs_gemv(const T *__restrict__ x, const T *__restrict__ W, float *__restrict__ y,
             lx[(size_t)(gi - lo) * LXS + tk] = fabsf(v) >= t ? xv : T(0);
         }
     }
+    trace_stamp(trace, 1, 1);
     __syncthreads();
+    trace_stamp(trace, 1, 2);
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // this CTA is done with xs
 
     trace_stamp(trace, 0, 1);

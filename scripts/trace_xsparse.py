@@ -41,7 +41,8 @@ tr = ws[off.value:off.value + nbytes.value].cpu().numpy().view(np.uint64).reshap
 g = int((tr[0, :, 0] > 0).sum())
 t0 = tr[0, :g, 0].min()
 print(f"XS ({g} CTAs, grid {plan.info['grid']}, R {plan.info['rows_per_tile']}), us from the first CTA start:")
-for s, nm in [(0, "start"), (5, "x_staged"), (6, "mask_done"), (7, "prefix_done"), (1, "list_ready"),
-              (2, "rows_done"), (3, "cluster_sync1"), (4, "exit")]:
-    v = (tr[0, :g, s] - t0) / 1e3
+for k, s, nm in [(0, 0, "start"), (0, 5, "x_staged"), (0, 6, "mask_done"), (0, 7, "prefix_done"),
+                 (1, 0, "range_found"), (1, 1, "list_written"), (1, 2, "list_synced"), (0, 1, "list_ready"),
+                 (0, 2, "rows_done"), (0, 3, "cluster_sync1"), (0, 4, "exit")]:
+    v = (tr[k, :g, s] - t0) / 1e3
     print(f"   {nm:14s} min {v.min():7.2f}  p50 {np.median(v):7.2f}  max {v.max():7.2f}")
