@@ -340,6 +340,8 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
             // shared memory fits, ties to the widest segment; segments under 128 B only when no wider one
             // divides d_out. Two CTAs per SM unless x (staged in shared memory) needs the whole SM.
             const char *xc = std::getenv("CATS_XS_COLS"), *xr = std::getenv("CATS_XS_R");  // experiments
+            const char *xm = std::getenv("CATS_XS_MMA");
+            p.xs_no_mma = xm && xm[0] == '0';
             for (int b = 1; b <= max_batch; ++b) {
                 PlanData::XsCfg &c = p.xs[b];
                 bool fits = false;
@@ -348,9 +350,12 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
                     const size_t budget = cps == 2 ? kXsSmemBudget : kSmemBudget;
                     int best = 0;
                     bool wide_ok = false;  // some segment of >= 128 B divides d_out
+                    // tensor-core batches take 64- or 128-column slabs when d_out allows
+                    const bool mma = esize == 2 && b >= kXsMmaMinB && !p.xs_no_mma && d % 64 == 0;
                     for (int nch = 32; nch >= 1; nch /= 2) {
                         const int cols = 16 * nch / esize;
                         if (d % cols != 0 || (nch < 8 && wide_ok)) continue;
+                        if (mma && cols != 64 && cols != 128) continue;
                         if (nch >= 8) wide_ok = true;
                         const PlanData::XsCfg keep = c;
                         c.cols = cols;

@@ -52,6 +52,7 @@ struct PlanData {
         int cols, q, r;       //   columns per CTA, column parts, cluster size (ranges of the kept list)
         int clusters;         //   clusters resident at once (-1: planned without a device)
     } xs[9];
+    bool xs_no_mma;           // CATS_XS_MMA=0: XS keeps the FFMA2 path at every batch (experiments)
     bool ablation_predicated;  // CATS_ABLATION_PREDICATED=1: decode in kModePredicated (K12 only)
     size_t off_x1, off_part;  // split path: x1 per compact position [m][max_b]; KB partials [R][max_b][d]
     size_t off_tmask;         // split path: per-tile active-row mask words (KA -> KB), zero between calls
@@ -165,6 +166,8 @@ constexpr int kXsThreads = 256;
 __host__ __device__ constexpr int xs_unroll(int b) { return b <= 2 ? 16 : b <= 4 ? 12 : 8; }
 constexpr size_t kXsSmemBudget = 113 * 1024;  // two CTAs per SM (228 KB less 1 KB reserved per CTA)
 inline int xs_maxr(const PlanData &p, int b) { return (p.m + p.xs[b].r - 1) / p.xs[b].r; }  // longest kept range
+constexpr int kXsMmaMinB = 4;  // batches from which XS uses bf16 MMA (C = 64 or 128 columns)
+int xs_mt(const PlanData &p, int b);
 size_t xs_smem_bytes(const PlanData &p, int b);
 int xs_active_clusters(const PlanData &p, int b);  // occupancy query (-1 without a device)
 cudaError_t launch_xsparse(const PlanData &p, const void *x, int b, const void *W, float t, float *y, void *ws,

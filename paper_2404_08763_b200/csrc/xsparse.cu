@@ -29,7 +29,23 @@ __device__ __forceinline__ uint32_t cluster_rank() {
     return r;
 }
 
-template <typename T, int B>
+__device__ __forceinline__ void xs_mma_bf16(float (&dd)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                            uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+                 "{%8, %9}, {%0, %1, %2, %3};"
+                 : "+f"(dd[0]), "+f"(dd[1]), "+f"(dd[2]), "+f"(dd[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void xs_ldsm_x4_trans(uint32_t saddr, uint32_t &r0, uint32_t &r1, uint32_t &r2,
+                                                 uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(saddr)
+                 : "memory");
+}
+
+// MT > 0: bf16 tensor-core main loop (C = 16 MT columns, b >= kXsMmaMinB); MT = 0: CUDA-core FFMA2
+template <typename T, int B, int MT>
 __global__ void __launch_bounds__(kXsThreads, 2)
 xs_gemv(const T *__restrict__ x, const T *__restrict__ W, float *__restrict__ y, int d_in, int d_out, int C,
         float t, int maxr, uint8_t *__restrict__ kin, unsigned long long *__restrict__ trace) {
@@ -47,8 +63,11 @@ xs_gemv(const T *__restrict__ x, const T *__restrict__ W, float *__restrict__ y,
     extern __shared__ __align__(128) unsigned char smem[];
     T *xs = reinterpret_cast<T *>(smem);                            // [B][d_in] staged x
     float *wred = reinterpret_cast<float *>(smem);                  // [NW_][B][C] per-warp partials (after xs)
-    float *slots = wred + (size_t)NW_ * B * C;                      // [R][B][C] rank partials (rank 0, after xs)
-    const size_t region = max((size_t)B * d_in * sizeof(T), (size_t)(NW_ + csize) * B * C * 4);
+    unsigned char *tiles = smem;                                    // MT > 0: [NW_][16][C + 8] bf16 (after xs)
+    const size_t tile_bytes = MT > 0 ? (size_t)NW_ * 16 * (C * 2 + 16) : 0;
+    const size_t a_bytes = (max((size_t)NW_ * B * C * 4, tile_bytes) + 15) & ~(size_t)15;
+    float *slots = reinterpret_cast<float *>(smem + a_bytes);       // [R][B][C] rank partials (rank 0, after xs)
+    const size_t region = max((size_t)B * d_in * sizeof(T), a_bytes + (size_t)csize * B * C * 4);
     uint32_t *kmask = reinterpret_cast<uint32_t *>(smem + ((region + 15) & ~(size_t)15));  // [NW]
     int *woff = reinterpret_cast<int *>(kmask + NW);                // [NW + 1]
     int *lj = woff + NW + 1;                                        // [maxr] kept inputs of this range
@@ -202,6 +221,73 @@ xs_gemv(const T *__restrict__ x, const T *__restrict__ W, float *__restrict__ y,
     // ---- acc[tk][e] += CATS_t(x)[tk][i] * W[i][col]: thread (g, ch) takes rows g, g + G, ... of the
     //      range in list order, UN rows' 16-byte chunks in flight ----
     const int g = tid / nch, ch = tid % nch;
+    if constexpr (MT > 0) {
+        // ---- tensor cores: warp w takes 16-row groups w, w + 8, ... of the range; a group's C-column
+        //      segments go through the warp's shared-memory tile (zero rows past the range), A = W^T by
+        //      ldmatrix .trans, B = CATS_t(x) (exact bf16), D[16 cols x 8 tokens] in fp32; the next
+        //      group's loads are issued before this group's MMAs ----
+        static_assert(sizeof(T) == 2, "MMA path is bf16");
+        constexpr int NL = MT;  // 16-byte chunks per lane per group: 16 rows x 2 MT chunks / 32 lanes
+        const int ng = (len + 15) / 16;
+        const uint32_t tst = (uint32_t)C * 2u + 16u;  // padded row stride: conflict-free ldmatrix
+        const uint32_t tile = smem_u32(tiles) + (uint32_t)warp * 16u * tst;
+        const int g4 = lane >> 2, t4 = lane & 3, mat = lane >> 3, r8 = lane & 7;
+        float dacc[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) dacc[mt][e] = 0.f;
+        auto load_group = [&](uint4 (&v)[NL], int grp) {
+#pragma unroll
+            for (int j = 0; j < NL; ++j) {
+                const int idx = lane + 32 * j, r = idx / (2 * MT), chk = idx % (2 * MT), row = grp * 16 + r;
+                v[j] = row < len ? ldg_stream(W + (size_t)lj[row] * d_out + (size_t)q * C + (size_t)chk * 8)
+                                 : make_uint4(0u, 0u, 0u, 0u);
+            }
+        };
+        uint4 cur[NL], nxt[NL];
+        if (warp < ng) load_group(cur, warp);
+        for (int grp = warp; grp < ng; grp += NW_) {
+            if (grp + NW_ < ng) load_group(nxt, grp + NW_);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < NL; ++j) {
+                const int idx = lane + 32 * j, r = idx / (2 * MT), chk = idx % (2 * MT);
+                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(tile + (uint32_t)r * tst + (uint32_t)chk * 16u),
+                             "r"(cur[j].x), "r"(cur[j].y), "r"(cur[j].z), "r"(cur[j].w) : "memory");
+            }
+            __syncwarp();
+            // B fragments: rows 2 t4, 2 t4 + 1 (b0) and 2 t4 + 8, + 9 (b1) of the group, token g4
+            uint32_t bf[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int k0 = grp * 16 + 2 * t4 + 8 * h;
+                const uint32_t lo16 = (g4 < B && k0 < len) ? (uint32_t)lx[(size_t)k0 * LXS + g4] : 0u;
+                const uint32_t hi16 = (g4 < B && k0 + 1 < len) ? (uint32_t)lx[(size_t)(k0 + 1) * LXS + g4] : 0u;
+                bf[h] = lo16 | (hi16 << 16);
+            }
+            const uint32_t abase = tile + (uint32_t)(r8 + 8 * (mat >> 1)) * tst + (uint32_t)(8 * (mat & 1)) * 2u;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                uint32_t a0, a1, a2, a3;
+                xs_ldsm_x4_trans(abase + (uint32_t)mt * 32u, a0, a1, a2, a3);
+                xs_mma_bf16(dacc[mt], a0, a1, a2, a3, bf[0], bf[1]);
+            }
+#pragma unroll
+            for (int j = 0; j < NL; ++j) cur[j] = nxt[j];
+        }
+        __syncthreads();  // every warp is past its tile: wred may overwrite the tiles
+        trace_stamp(trace, 0, 2);
+        // lane (g4, t4): D[col 16 mt + g4 (+8)][token 2 t4 (+1)]
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int c = mt * 16 + g4 + 8 * (e >> 1), tk = 2 * t4 + (e & 1);
+                if (tk < B) wred[((size_t)warp * B + tk) * C + c] = dacc[mt][e];
+            }
+        __syncthreads();
+    } else {
     const T *wcol = W + (size_t)q * C + (size_t)ch * VEC;
     float2 acc2[B][VEC / 2];  // column pairs: one FFMA2 per pair (same rounding as two FFMAs)
 #pragma unroll
@@ -265,6 +351,7 @@ xs_gemv(const T *__restrict__ x, const T *__restrict__ W, float *__restrict__ y,
             for (int e = 0; e < VEC; ++e) wred[((size_t)warp * B + tk) * C + ch * VEC + e] = acc[tk][e];
     }
     __syncthreads();
+    }  // MT
     // ---- cluster reduction, fixed order: every rank stores its partial (sum over its warps in warp
     //      order) into slot [rank] of rank 0's shared memory (DSMEM), one cluster barrier, then rank 0
     //      writes y[tk][q*C + c] = sum over ranks 0..R-1 in order. The slots alias rank 0's x staging:
@@ -294,20 +381,38 @@ xs_gemv(const T *__restrict__ x, const T *__restrict__ W, float *__restrict__ y,
     trace_stamp(trace, 0, 4);
 }
 
+int xs_mt(const PlanData &p, int b) {  // tensor-core tile count per warp for batch b (0 = FFMA2 path)
+    const int c = p.xs[b].cols;
+    return (p.esize == 2 && b >= kXsMmaMinB && !p.xs_no_mma && (c == 64 || c == 128)) ? c / 16 : 0;
+}
+
 size_t xs_smem_bytes(const PlanData &p, int b) {
     const int nw = (p.m + 31) / 32;
     const int maxr = xs_maxr(p, b);
-    const size_t region = std::max((size_t)b * p.m * p.esize, (size_t)(kXsThreads / 32 + p.xs[b].r) * b * p.xs[b].cols * 4);
+    const int c = p.xs[b].cols, mt = xs_mt(p, b);
+    const size_t tiles = mt > 0 ? (size_t)(kXsThreads / 32) * 16 * (c * 2 + 16) : 0;
+    const size_t a_bytes = (std::max((size_t)(kXsThreads / 32) * b * c * 4, tiles) + 15) & ~(size_t)15;
+    const size_t region = std::max((size_t)b * p.m * p.esize, a_bytes + (size_t)p.xs[b].r * b * c * 4);
     const int lxs = p.esize == 2 ? (b + 1) & ~1 : b;
     return ((region + 15) & ~(size_t)15) + (size_t)nw * 4 + (size_t)(nw + 1) * 4 +
            (size_t)maxr * 4 + (size_t)maxr * lxs * p.esize;
 }
 
 template <typename T, int B>
+static decltype(&xs_gemv<T, B, 0>) xs_kernel(const PlanData &p) {
+    if constexpr (sizeof(T) == 2 && B >= kXsMmaMinB) {
+        const int mt = xs_mt(p, B);
+        if (mt == 4) return xs_gemv<T, B, 4>;
+        if (mt == 8) return xs_gemv<T, B, 8>;
+    }
+    return xs_gemv<T, B, 0>;
+}
+
+template <typename T, int B>
 static cudaError_t launch_xs_b(const PlanData &p, const void *x, const void *W, float t, float *y, void *ws,
                                cudaStream_t s) {
     const size_t smem = xs_smem_bytes(p, B);
-    auto kern = xs_gemv<T, B>;
+    auto kern = xs_kernel<T, B>(p);
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
     if (e != cudaSuccess) return e;
     cudaLaunchAttribute attr[2];
@@ -333,7 +438,7 @@ static cudaError_t launch_xs_b(const PlanData &p, const void *x, const void *W, 
 template <typename T, int B>
 static int xs_active_clusters_b(const PlanData &p) {
     const size_t smem = xs_smem_bytes(p, B);
-    auto kern = xs_gemv<T, B>;
+    auto kern = xs_kernel<T, B>(p);
     if (ensure_smem_attr(reinterpret_cast<const void *>(kern), smem) != cudaSuccess) return -1;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
