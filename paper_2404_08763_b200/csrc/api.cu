@@ -351,7 +351,7 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
                     int best = 0;
                     bool wide_ok = false;  // some segment of >= 128 B divides d_out
                     // tensor-core batches take 64- or 128-column slabs when d_out allows
-                    const bool mma = esize == 2 && b >= kXsMmaMinB && !p.xs_no_mma && d % 64 == 0;
+                    const bool mma = esize == 2 && b >= kXsMmaForceB && !p.xs_no_mma && d % 64 == 0;
                     for (int nch = 32; nch >= 1; nch /= 2) {
                         const int cols = 16 * nch / esize;
                         if (d % cols != 0 || (nch < 8 && wide_ok)) continue;

@@ -166,7 +166,11 @@ constexpr int kXsThreads = 256;
 __host__ __device__ constexpr int xs_unroll(int b) { return b <= 2 ? 16 : b <= 4 ? 12 : 8; }
 constexpr size_t kXsSmemBudget = 113 * 1024;  // two CTAs per SM (228 KB less 1 KB reserved per CTA)
 inline int xs_maxr(const PlanData &p, int b) { return (p.m + p.xs[b].r - 1) / p.xs[b].r; }  // longest kept range
-constexpr int kXsMmaMinB = 4;  // batches from which XS uses bf16 MMA (C = 64 or 128 columns)
+// XS uses bf16 MMA from b = 2 whenever its column slab is 64 or 128 wide; from b = 4 the slab width is
+// restricted to those (measured: b = 2 4096 -> 6144 13.8 -> 13.0 us, 4096 -> 4096 14.3 -> 11.1; forcing
+// 128 columns at 4096 -> 12288 b = 2 cost 20.5 -> 23.5, so below b = 4 the width stays free)
+constexpr int kXsMmaMinB = 2;
+constexpr int kXsMmaForceB = 4;
 int xs_mt(const PlanData &p, int b);
 size_t xs_smem_bytes(const PlanData &p, int b);
 int xs_active_clusters(const PlanData &p, int b);  // occupancy query (-1 without a device)
