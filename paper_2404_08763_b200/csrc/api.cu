@@ -379,7 +379,8 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
                 // with a device: shrink the clusters until every one of them is resident at once (the GPCs'
                 // SM counts need not be multiples of the cluster footprint)
                 c.clusters = -1;
-                if (query_device && cudaSetDevice(device) == cudaSuccess) {
+                const char *xns = std::getenv("CATS_XS_NOSHRINK");  // experiment: keep R, allow a partial second wave
+                if (query_device && !(xns && xns[0] == '1') && cudaSetDevice(device) == cudaSuccess) {
                     for (;;) {
                         c.clusters = xs_active_clusters(p, b);
                         if (c.clusters < 0 || c.clusters >= c.q || c.r == 1) break;
