@@ -179,6 +179,52 @@ typedef struct {
  *         register/shared-memory tiling), CATS_E_CUDA (device query failed). */
 cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_dtype_t w_dtype, int device,
                                    int num_sms, cats_mlp_plan_t **out);
+
+/* ---- explicit plan options (kernel-path selection, the App. D ablation, tuning knobs) ---------
+ * The library reads no environment variables: every choice that changes which kernels run is an
+ * explicit field here, fixed at plan creation. cats_mlp_plan_create(...) == _ex(..., NULL). */
+typedef enum {
+    CATS_PATH_AUTO = 0,   /* K12 at b = 1; KA + KB at b >= 2 where their shared memory fits */
+    CATS_PATH_FUSED = 1   /* K12 (the single fused kernel) at every batch size */
+} cats_path_t;
+
+/* How the active set reaches the sparse up / down projection (App. D; the ablation
+ * figure). Every mode computes the same y (Eq. 5); they differ in launches and traffic. */
+typedef enum {
+    CATS_COMPACT_BALLOT = 0,     /* default: per-tile warp ballot + popc prefix inside K12 / KA (no atomics) */
+    CATS_COMPACT_PREDICATED = 1, /* App. D Alg. 2 (Triton P:803-866): no index list; every tile's rows
+                                    are visited in fixed halves and Mask predicates the row loads (inactive rows
+                                    are not read, they enter the arithmetic as zeros). K12 only */
+    CATS_COMPACT_ATOMIC = 2      /* App. D Alg. 1: "idcs <- indices where Mask = 1" by atomic appends
+                                    into one global list (arbitrary order), then a second kernel walks idcs.
+                                    Two launches (gate kernel, list kernel) */
+} cats_compaction_t;
+
+typedef struct {
+    uint32_t size;           /* = sizeof(cats_mlp_plan_options_t) (ABI check; CATS_E_SHAPE otherwise) */
+    int32_t path;            /* cats_path_t */
+    int32_t compaction;      /* cats_compaction_t (gated-MLP plans; non-default modes always run K12 kernels) */
+    int32_t trace;           /* 1: kernels stamp %globaltimer into the workspace (cats_mlp_trace_info) */
+    /* tuning (measurement knobs; cats_mlp_plan_options_init sets the planner's defaults) */
+    int32_t rows_per_tile;   /* K12 tile height NR: 0 = auto, else 2, 4 or (b = 1 only) 6 */
+    int32_t max_stages;      /* K12 ring depth cap: 0 = as many stages as fit, else >= 2 */
+    int32_t lazy_tail;       /* K12 / KA reserve no tile ahead for the last lazy_tail x grid tiles (>= 0) */
+    int32_t min_tiles;       /* K12 grid <= ntiles / min_tiles (>= 1) */
+    int32_t eager;           /* K12 fills every ring stage with claimed tiles at start (0 / 1) */
+    int32_t l2_prefetch;     /* K12 static tiles per CTA prefetched into L2 before griddepcontrol.wait (>= 0) */
+    int32_t xs_cols;         /* App. B XS: columns per CTA (0 = auto) */
+    int32_t xs_ranges;       /* App. B XS: cluster size R (0 = auto, else 1..8) */
+    int32_t xs_mma;          /* App. B XS: 1 = tensor cores where the slab allows (default), 0 = FFMA2 only */
+    int32_t xs_no_shrink;    /* App. B XS: 1 = keep R even when not every cluster is co-resident */
+} cats_mlp_plan_options_t;
+
+/* Fill *opt with the defaults (size set, path AUTO, compaction BALLOT, lazy_tail 8, min_tiles 2,
+ * xs_mma 1, the rest 0). Errors: CATS_E_NULL. */
+cats_status_t cats_mlp_plan_options_init(cats_mlp_plan_options_t *opt);
+/* cats_mlp_plan_create with options (opt == NULL: the defaults). Additional errors: CATS_E_SHAPE
+ * (opt->size mismatch or a tuning field out of range), CATS_E_UNSUPPORTED (unknown path / compaction). */
+cats_status_t cats_mlp_plan_create_ex(int d, int m, int max_batch, cats_dtype_t w_dtype, int device, int num_sms,
+                                      const cats_mlp_plan_options_t *opt, cats_mlp_plan_t **out);
 void cats_mlp_plan_destroy(cats_mlp_plan_t *plan);
 cats_status_t cats_mlp_plan_info(const cats_mlp_plan_t *plan, cats_mlp_plan_info_t *info);
 cats_status_t cats_mlp_workspace_bytes(const cats_mlp_plan_t *plan, size_t *bytes);
@@ -197,8 +243,9 @@ cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, void *ws, siz
  * the active list + a fixed-order two-phase reduction); b >= 4 uses warp-level bf16 MMA for the
  * dot products. cats_mlp_kernels_per_call() tells which. All launches use programmatic dependent
  * launch (a successor's CTAs start streaming weights while the predecessor drains).
- * KB keeps all of its CTAs (<= the plan's SM count) co-resident for a grid barrier: do not run the
- * decode concurrently with a kernel that occupies SMs indefinitely.
+ * KB has no grid barrier: the last 64 of its CTAs to finish do the fixed-order reduction while the
+ * others exit, so it completes whenever more than 64 of its CTAs (one per SM) can be resident at once;
+ * plans for <= 64 SMs take K12 at every batch size.
  * Deterministic: bit-identical y for identical inputs, whatever the dynamic tile schedule.
  * Errors: CATS_E_NULL, CATS_E_ALIGN, CATS_E_BATCH, CATS_E_THRESHOLD, CATS_E_WORKSPACE,
  *         CATS_E_CUDA. */
@@ -264,6 +311,9 @@ cats_status_t cats_mlp_kernels_per_call(const cats_mlp_plan_t *plan, int b, int 
  * above ~200 KB). */
 cats_status_t cats_xsparse_plan_create(int d_in, int d_out, int max_batch, cats_dtype_t w_dtype, int device,
                                        int num_sms, cats_mlp_plan_t **out);
+/* with explicit options (only trace and the xs_* fields apply; NULL = defaults) */
+cats_status_t cats_xsparse_plan_create_ex(int d_in, int d_out, int max_batch, cats_dtype_t w_dtype, int device,
+                                          int num_sms, const cats_mlp_plan_options_t *opt, cats_mlp_plan_t **out);
 /* x [b][d_in] (w_dtype), W_in_major [d_in][d_out] (w_dtype), y [b][d_out] fp32, all device memory
  * with 16-byte aligned bases; t >= 0 finite (t = 0 keeps every input: the dense GEMV).
  * ONE launch on s (DESIGN.md §5 XS, thread-block clusters + programmatic dependent launch): every CTA
@@ -276,7 +326,7 @@ cats_status_t cats_xsparse_plan_create(int d_in, int d_out, int max_batch, cats_
 cats_status_t cats_xsparse_gemv(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_in_major,
                                 float t, float *y, void *ws, size_t ws_bytes, cats_stream_t s);
 
-/* Diagnostics. When the environment variable CATS_TRACE=1 is set at plan creation, the kernels
+/* Diagnostics. When the plan was created with options.trace = 1, the kernels
  * record %globaltimer stamps (ns) per CTA into a trace area of the workspace:
  * uint64 trace[3][512 CTAs][8 slots] at byte `offset` (bytes = 0 when tracing is off).
  * [0] K12 / KA slots: 0 start, 1 ring primed, 2 jobs done, 3 exit, 4 K12 partial reduced;

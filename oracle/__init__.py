@@ -25,8 +25,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "cats_oracle.c")
 _LIB_PATH = os.path.join(_HERE, "libcats_oracle.so")
+_OMP_PATH = os.path.join(_HERE, "libcats_oracle_omp.so")  # timing build (all cores), same source
 _lock = threading.Lock()
 _lib = None
+_omp = None
 
 F32 = 0
 BF16 = 1
@@ -34,21 +36,23 @@ SPARSE, MASKED, DENSE = 0, 1, 2
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (plain C, fp64, no FMA contraction, no fast-math)."""
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
-        tmp = _LIB_PATH + f".tmp{os.getpid()}"
-        subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=gnu11", "-fPIC", "-shared",
-                        _SRC, "-o", tmp, "-lm"], check=True)
-        os.replace(tmp, _LIB_PATH)
+    """Compile the oracle with gcc (plain C, fp64, no FMA contraction, no fast-math): the serial
+    checker, and the same source with -fopenmp as the all-core timing build."""
+    for path, extra in ((_LIB_PATH, []), (_OMP_PATH, ["-fopenmp"])):
+        if force or not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(_SRC):
+            tmp = path + f".tmp{os.getpid()}"
+            subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=gnu11", "-fPIC", "-shared",
+                            *extra, _SRC, "-o", tmp, "-lm"], check=True)
+            os.replace(tmp, path)
     return _LIB_PATH
 
 
-def _load():
-    global _lib
+def _load(omp: bool = False):
+    global _lib, _omp
     with _lock:
-        if _lib is None:
+        if (_omp if omp else _lib) is None:
             build()
-            lib = ctypes.CDLL(_LIB_PATH)
+            lib = ctypes.CDLL(_OMP_PATH if omp else _LIB_PATH)
             P = ctypes.c_void_p
             lib.oracle_silu.restype = ctypes.c_double
             lib.oracle_silu.argtypes = [ctypes.c_double]
@@ -69,8 +73,11 @@ def _load():
             lib.oracle_bf16_count.argtypes = [P, ctypes.c_uint64, P]
             lib.oracle_calibrate_bf16_counts.restype = ctypes.c_int
             lib.oracle_calibrate_bf16_counts.argtypes = [P, ctypes.c_double, P, P, P, P, P]
-            _lib = lib
-    return _lib
+            if omp:
+                _omp = lib
+            else:
+                _lib = lib
+    return _omp if omp else _lib
 
 
 def _ptr(a: np.ndarray) -> int:
@@ -100,8 +107,9 @@ def cats_mask(v: np.ndarray, t: float) -> np.ndarray:
 
 
 def mlp(x: np.ndarray, Wg: np.ndarray, Wu: np.ndarray, Wd: np.ndarray, t: float, mode: int = SPARSE,
-        keep_in: np.ndarray | None = None):
+        keep_in: np.ndarray | None = None, all_cores: bool = False):
     """CATS gated MLP per token (Eq. 1 + Eq. 5, Alg. "MLP using CATS" P:289-298).
+    all_cores=True runs the OpenMP build of the same source (timing only; identical results).
 
     x: [b][d]; Wg, Wu, Wd: neuron-major [m][d]; all float32 or all uint16 (bf16 bits).
     Returns (y [b][d] float64, v [b][m] float64, keep [b][m] uint8).
@@ -124,8 +132,8 @@ def mlp(x: np.ndarray, Wg: np.ndarray, Wu: np.ndarray, Wd: np.ndarray, t: float,
     if keep_in is not None:
         keep_in = np.ascontiguousarray(keep_in, dtype=np.uint8).reshape(b, m)
         kp = _ptr(keep_in)
-    rc = _load().oracle_mlp(d, m, b, dt, _ptr(x), _ptr(Wg), _ptr(Wu), _ptr(Wd), float(t), int(mode),
-                            kp, _ptr(y), _ptr(v), _ptr(keep))
+    rc = _load(all_cores).oracle_mlp(d, m, b, dt, _ptr(x), _ptr(Wg), _ptr(Wu), _ptr(Wd), float(t), int(mode),
+                                     kp, _ptr(y), _ptr(v), _ptr(keep))
     if rc != 0:
         raise ValueError(f"oracle_mlp failed ({rc})")
     return y, v, keep

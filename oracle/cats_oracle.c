@@ -8,7 +8,11 @@
  *
  * Build: gcc -O2 -ffp-contract=off -fPIC -shared cats_oracle.c -o libcats_oracle.so -lm
  * (no -ffast-math, no FMA contraction: every sum is a chain of correctly rounded
- * fp64 additions in ascending index order).
+ * fp64 additions in ascending index order). That serial build is the checker.
+ * A second build of the SAME source with -fopenmp (libcats_oracle_omp.so) is used only to time
+ * the CPU baseline on all host cores: the `omp parallel for` pragmas below split independent
+ * iterations (neurons j for u / v / x1, output columns c for y) across threads and change no
+ * summation order, so both builds return identical bits (tests/test_oracle_pins.py checks it).
  *
  * Citations: "P:n" = /root/reference/PAPER.md line n, "S:n" = SPEC.md line n.
  *
@@ -93,6 +97,7 @@ int oracle_mlp(int64_t d, int64_t m, int64_t b, int dtype,
         for (int64_t i = 0; i < d; ++i) xs[i] = widen(x, (uint64_t)(bt * d + i), dtype);
 
         /* v <- SiLU(x W_gate) */
+#pragma omp parallel for schedule(static)
         for (int64_t j = 0; j < m; ++j) {
             double u = 0.0;
             for (int64_t i = 0; i < d; ++i) u += xs[i] * widen(Wg, (uint64_t)(j * d + i), dtype);
@@ -107,6 +112,7 @@ int oracle_mlp(int64_t d, int64_t m, int64_t b, int dtype,
             oracle_cats_mask(v, m, t, keep);
         }
         /* x1 <- (x W_up[Mask]) * v[Mask] */
+#pragma omp parallel for schedule(static)
         for (int64_t j = 0; j < m; ++j) {
             if (mode == 0 && !keep[j]) { x1[j] = 0.0; continue; }
             double up = 0.0;
@@ -114,7 +120,8 @@ int oracle_mlp(int64_t d, int64_t m, int64_t b, int dtype,
             double vj = keep[j] ? v[j] : 0.0; /* v' of P:702 */
             x1[j] = vj * up;
         }
-        /* y <- x1 W_down[Mask] */
+        /* y <- x1 W_down[Mask]; each y_c is the ascending-j sum */
+#pragma omp parallel for schedule(static)
         for (int64_t c = 0; c < d; ++c) {
             double acc = 0.0;
             for (int64_t j = 0; j < m; ++j) {

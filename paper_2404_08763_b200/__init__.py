@@ -13,14 +13,16 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import CATS_BF16, CATS_F32, CalibInfo, CalibWindow, PlanInfo
+from ._lib import (CATS_BF16, CATS_COMPACT_ATOMIC, CATS_COMPACT_BALLOT, CATS_COMPACT_PREDICATED, CATS_F32,
+                   CATS_PATH_AUTO, CATS_PATH_FUSED, CalibInfo, CalibWindow, PlanInfo, PlanOptions)
 
 __all__ = [
     "CatsError", "MlpPlan", "cats_calib_rank", "cats_calibrate_workspace_bytes", "cats_calibrate_threshold",
     "cats_calib_window_init", "cats_calib_hist", "cats_calib_step", "cats_mlp_decode", "cats_mlp_dense",
     "cats_mlp_decode_profiled",
     "cats_mlp_decode_host", "cats_mlp_gate_act", "cats_mlp_last_active", "cats_mlp_kernels_per_call", "library_path",
-    "XsparsePlan", "cats_xsparse_gemv",
+    "XsparsePlan", "cats_xsparse_gemv", "plan_options", "CATS_PATH_AUTO", "CATS_PATH_FUSED", "CATS_COMPACT_BALLOT",
+    "CATS_COMPACT_PREDICATED", "CATS_COMPACT_ATOMIC",
 ]
 
 
@@ -66,6 +68,29 @@ def _stream(stream, device) -> int:
     if stream is None:
         stream = torch.cuda.current_stream(device)
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _stream_obj(stream, device):
+    """The torch stream a call runs on (allocations for it are made under this stream)."""
+    if stream is None:
+        return torch.cuda.current_stream(device)
+    if isinstance(stream, torch.cuda.Stream):
+        return stream
+    return torch.cuda.ExternalStream(int(stream), device=device)
+
+
+def plan_options(**kw) -> PlanOptions:
+    """cats_mlp_plan_options_t with the library defaults, fields overridden by keyword
+    (path, compaction, trace, rows_per_tile, max_stages, lazy_tail, min_tiles, eager, l2_prefetch,
+    xs_cols, xs_ranges, xs_mma, xs_no_shrink)."""
+    o = PlanOptions()
+    _check(_lib.load().cats_mlp_plan_options_init(ctypes.byref(o)), "cats_mlp_plan_options_init")
+    names = {f for f, _ in PlanOptions._fields_} - {"size"}
+    for k, v in kw.items():
+        if k not in names:
+            raise TypeError(f"unknown plan option {k!r}")
+        setattr(o, k, int(v))
+    return o
 
 
 # ------------------------------------------------------------------------------- calibration
@@ -136,14 +161,17 @@ class MlpPlan:
     _create = "cats_mlp_plan_create"
 
     def __init__(self, d: int, m: int, max_batch: int = 1, dtype: torch.dtype = torch.bfloat16, device: int = 0,
-                 num_sms: int = 0):
+                 num_sms: int = 0, **options):
+        """options: cats_mlp_plan_options_t fields (see plan_options); none = the library defaults."""
         self._lib = _lib.load()
         self._h = ctypes.c_void_p()
         self.dtype = dtype
         dt = CATS_BF16 if dtype == torch.bfloat16 else CATS_F32
         args = (int(m), int(d)) if self._create == "cats_xsparse_plan_create" else (int(d), int(m))
-        _check(getattr(self._lib, self._create)(*args, int(max_batch), dt, int(device), int(num_sms),
-                                                ctypes.byref(self._h)), self._create)
+        self.options = plan_options(**options)
+        fn = self._create + "_ex"
+        _check(getattr(self._lib, fn)(*args, int(max_batch), dt, int(device), int(num_sms),
+                                      ctypes.byref(self.options), ctypes.byref(self._h)), fn)
         info = PlanInfo()
         _check(self._lib.cats_mlp_plan_info(self._h, ctypes.byref(info)), "cats_mlp_plan_info")
         self.info = {f: getattr(info, f) for f, _ in PlanInfo._fields_}
@@ -158,9 +186,11 @@ class MlpPlan:
         return self.info["workspace_bytes"]
 
     def workspace(self, stream=None) -> torch.Tensor:
-        """Allocate and initialise (cats_mlp_workspace_init) a decode workspace."""
-        ws = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=f"cuda:{self.device}")
-        rc = self._lib.cats_mlp_workspace_init(self.handle, ws.data_ptr(), ws.numel(), _stream(stream, ws.device))
+        """Allocate (on `stream`) and initialise (cats_mlp_workspace_init, on `stream`) a decode workspace."""
+        st = _stream_obj(stream, torch.device(f"cuda:{self.device}"))
+        with torch.cuda.stream(st):
+            ws = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+        rc = self._lib.cats_mlp_workspace_init(self.handle, ws.data_ptr(), ws.numel(), st.cuda_stream)
         _check(rc, "cats_mlp_workspace_init")
         return ws
 
@@ -178,37 +208,62 @@ class XsparsePlan(MlpPlan):
     _create = "cats_xsparse_plan_create"
 
     def __init__(self, d_in: int, d_out: int, max_batch: int = 1, dtype: torch.dtype = torch.bfloat16,
-                 device: int = 0, num_sms: int = 0):
-        super().__init__(d_out, d_in, max_batch, dtype, device, num_sms)
+                 device: int = 0, num_sms: int = 0, **options):
+        super().__init__(d_out, d_in, max_batch, dtype, device, num_sms, **options)
         self.d_in, self.d_out = d_in, d_out
 
 
-def _prep(plan: MlpPlan, x: torch.Tensor, y, ws):
+def _check_tensor(t: torch.Tensor, name: str, shape, dtype, device):
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)} != {tuple(shape)}")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: dtype {t.dtype} != {dtype}")
+    if t.device != device:
+        raise ValueError(f"{name}: on {t.device}, expected {device}")
+
+
+def _prep(plan: MlpPlan, x: torch.Tensor, y, ws, stream, weights=(), wshape=None):
+    """Validate shapes / dtypes / devices against the plan (the C ABI carries no sizes), and allocate
+    y / the workspace on the stream the call runs on (so the caching allocator and the workspace
+    initialisation are ordered with the launch)."""
     if x.dim() == 1:
         x = x.unsqueeze(0)
     b = x.shape[0]
-    if y is None:
-        y = torch.empty((b, plan.d), dtype=torch.float32, device=x.device)
-    if ws is None:
-        ws = plan.workspace()
-    return x, b, y, ws
+    dev = torch.device(f"cuda:{plan.device}")
+    _check_tensor(x, "x", (b, plan.m if isinstance(plan, XsparsePlan) else plan.d), plan.dtype, dev)
+    for name, w in weights:
+        _check_tensor(w, name, wshape, plan.dtype, dev)
+    st = _stream_obj(stream, dev)
+    with torch.cuda.stream(st):
+        if y is None:
+            y = torch.empty((b, plan.d), dtype=torch.float32, device=dev)
+        if ws is None:
+            ws = plan.workspace(stream=st)
+    _check_tensor(y, "y", (b, plan.d), torch.float32, dev)
+    if ws.dtype != torch.uint8 or ws.numel() < plan.workspace_bytes:
+        raise ValueError(f"workspace must be uint8 with >= {plan.workspace_bytes} bytes")
+    return x, b, y, ws, st
+
+
+def _mlp_w(W_gate, W_up, W_down_nm):
+    return [("W_gate", W_gate), ("W_up", W_up), ("W_down_nm", W_down_nm)]
 
 
 def cats_mlp_decode(plan: MlpPlan, x, W_gate, W_up, W_down_nm, t: float, y=None, ws=None, stream=None):
     """y[b][d] (fp32) = CATS_t gated MLP of x[b][d]; weights neuron-major [m][d]."""
-    x, b, y, ws = _prep(plan, x, y, ws)
+    x, b, y, ws, st = _prep(plan, x, y, ws, stream, _mlp_w(W_gate, W_up, W_down_nm), (plan.m, plan.d))
     rc = plan._lib.cats_mlp_decode(plan.handle, _dev_ptr(x, "x"), b, _dev_ptr(W_gate, "W_gate"),
                                    _dev_ptr(W_up, "W_up"), _dev_ptr(W_down_nm, "W_down_nm"), float(t),
-                                   _dev_ptr(y, "y"), _dev_ptr(ws, "ws"), ws.numel(), _stream(stream, x.device))
+                                   _dev_ptr(y, "y"), _dev_ptr(ws, "ws"), ws.numel(), st.cuda_stream)
     _check(rc, "cats_mlp_decode")
     return y
 
 
 def cats_xsparse_gemv(plan: XsparsePlan, x, W_in_major, t: float, y=None, ws=None, stream=None):
     """y[b][d_out] (fp32) = CATS_t(x) W for x[b][d_in]; W input-major [d_in][d_out] (App. B)."""
-    x, b, y, ws = _prep(plan, x, y, ws)
+    x, b, y, ws, st = _prep(plan, x, y, ws, stream, [("W_in_major", W_in_major)], (plan.m, plan.d))
     rc = plan._lib.cats_xsparse_gemv(plan.handle, _dev_ptr(x, "x"), b, _dev_ptr(W_in_major, "W_in_major"), float(t),
-                                     _dev_ptr(y, "y"), _dev_ptr(ws, "ws"), ws.numel(), _stream(stream, x.device))
+                                     _dev_ptr(y, "y"), _dev_ptr(ws, "ws"), ws.numel(), st.cuda_stream)
     _check(rc, "cats_xsparse_gemv")
     return y
 
@@ -216,24 +271,23 @@ def cats_xsparse_gemv(plan: XsparsePlan, x, W_in_major, t: float, y=None, ws=Non
 def cats_mlp_decode_profiled(plan: MlpPlan, x, W_gate, W_up, W_down_nm, t: float, events, y=None, ws=None,
                              stream=None):
     """cats_mlp_decode with 3 torch.cuda.Event(enable_timing=True) recorded around K12 and K3."""
-    x, b, y, ws = _prep(plan, x, y, ws)
+    x, b, y, ws, st = _prep(plan, x, y, ws, stream, _mlp_w(W_gate, W_up, W_down_nm), (plan.m, plan.d))
     for e in events:
         if e.cuda_event == 0:
-            e.record()  # materialise the lazily created event on this device
+            e.record(st)  # materialise the lazily created event on this device
     arr = (ctypes.c_void_p * 3)(*[e.cuda_event for e in events])
     rc = plan._lib.cats_mlp_decode_profiled(plan.handle, _dev_ptr(x, "x"), b, _dev_ptr(W_gate, "W_gate"),
                                             _dev_ptr(W_up, "W_up"), _dev_ptr(W_down_nm, "W_down_nm"), float(t),
-                                            _dev_ptr(y, "y"), _dev_ptr(ws, "ws"), ws.numel(),
-                                            _stream(stream, x.device), arr)
+                                            _dev_ptr(y, "y"), _dev_ptr(ws, "ws"), ws.numel(), st.cuda_stream, arr)
     _check(rc, "cats_mlp_decode_profiled")
     return y
 
 
 def cats_mlp_dense(plan: MlpPlan, x, W_gate, W_up, W_down_nm, y=None, ws=None, stream=None):
-    x, b, y, ws = _prep(plan, x, y, ws)
+    x, b, y, ws, st = _prep(plan, x, y, ws, stream, _mlp_w(W_gate, W_up, W_down_nm), (plan.m, plan.d))
     rc = plan._lib.cats_mlp_dense(plan.handle, _dev_ptr(x, "x"), b, _dev_ptr(W_gate, "W_gate"),
                                   _dev_ptr(W_up, "W_up"), _dev_ptr(W_down_nm, "W_down_nm"), _dev_ptr(y, "y"),
-                                  _dev_ptr(ws, "ws"), ws.numel(), _stream(stream, x.device))
+                                  _dev_ptr(ws, "ws"), ws.numel(), st.cuda_stream)
     _check(rc, "cats_mlp_dense")
     return y
 
@@ -243,16 +297,26 @@ def cats_mlp_decode_host(plan: MlpPlan, x_host: torch.Tensor, W_gate, W_up, W_do
     """Host x in (pinned recommended), host y out; blocks on the stream."""
     if x_host.dim() == 1:
         x_host = x_host.unsqueeze(0)
-    assert not x_host.is_cuda and x_host.is_contiguous()
+    if x_host.is_cuda or not x_host.is_contiguous():
+        raise ValueError("x_host must be a contiguous host tensor")
     b = x_host.shape[0]
+    cpu = torch.device("cpu")
+    _check_tensor(x_host, "x_host", (b, plan.d), plan.dtype, cpu)
+    dev = torch.device(f"cuda:{plan.device}")
+    for name, w in _mlp_w(W_gate, W_up, W_down_nm):
+        _check_tensor(w, name, (plan.m, plan.d), plan.dtype, dev)
+    st = _stream_obj(stream, dev)
     if y_host is None:
         y_host = torch.empty((b, plan.d), dtype=torch.float32, pin_memory=x_host.is_pinned())
+    _check_tensor(y_host, "y_host", (b, plan.d), torch.float32, cpu)
+    if not y_host.is_contiguous():
+        raise ValueError("y_host must be contiguous")
     if ws is None:
-        ws = plan.workspace()
+        with torch.cuda.stream(st):
+            ws = plan.workspace(stream=st)
     rc = plan._lib.cats_mlp_decode_host(plan.handle, x_host.data_ptr(), b, _dev_ptr(W_gate, "W_gate"),
                                         _dev_ptr(W_up, "W_up"), _dev_ptr(W_down_nm, "W_down_nm"), float(t),
-                                        y_host.data_ptr(), _dev_ptr(ws, "ws"), ws.numel(),
-                                        _stream(stream, W_gate.device))
+                                        y_host.data_ptr(), _dev_ptr(ws, "ws"), ws.numel(), st.cuda_stream)
     _check(rc, "cats_mlp_decode_host")
     return y_host
 
@@ -262,13 +326,18 @@ def cats_mlp_gate_act(plan: MlpPlan, x, W_gate, acts=None, ws=None, stream=None)
     if x.dim() == 1:
         x = x.unsqueeze(0)
     b = x.shape[0]
-    if acts is None:
-        acts = torch.empty((b, plan.m), dtype=torch.float32, device=x.device)
-    if ws is None:
-        ws = plan.workspace()
+    dev = torch.device(f"cuda:{plan.device}")
+    _check_tensor(x, "x", (b, plan.d), plan.dtype, dev)
+    _check_tensor(W_gate, "W_gate", (plan.m, plan.d), plan.dtype, dev)
+    st = _stream_obj(stream, dev)
+    with torch.cuda.stream(st):
+        if acts is None:
+            acts = torch.empty((b, plan.m), dtype=torch.float32, device=dev)
+        if ws is None:
+            ws = plan.workspace(stream=st)
+    _check_tensor(acts, "acts", (b, plan.m), torch.float32, dev)
     rc = plan._lib.cats_mlp_gate_act(plan.handle, _dev_ptr(x, "x"), b, _dev_ptr(W_gate, "W_gate"),
-                                     _dev_ptr(acts, "acts"), _dev_ptr(ws, "ws"), ws.numel(),
-                                     _stream(stream, x.device))
+                                     _dev_ptr(acts, "acts"), _dev_ptr(ws, "ws"), ws.numel(), st.cuda_stream)
     _check(rc, "cats_mlp_gate_act")
     return acts
 

@@ -26,6 +26,19 @@ class CalibWindow(ctypes.Structure):
                 ("nbins", ctypes.c_uint32), ("sample_stride", ctypes.c_uint64)]
 
 
+class PlanOptions(ctypes.Structure):
+    """cats_mlp_plan_options_t (include/cats.h)."""
+    _fields_ = [("size", ctypes.c_uint32), ("path", ctypes.c_int32), ("compaction", ctypes.c_int32),
+                ("trace", ctypes.c_int32), ("rows_per_tile", ctypes.c_int32), ("max_stages", ctypes.c_int32),
+                ("lazy_tail", ctypes.c_int32), ("min_tiles", ctypes.c_int32), ("eager", ctypes.c_int32),
+                ("l2_prefetch", ctypes.c_int32), ("xs_cols", ctypes.c_int32), ("xs_ranges", ctypes.c_int32),
+                ("xs_mma", ctypes.c_int32), ("xs_no_shrink", ctypes.c_int32)]
+
+
+CATS_PATH_AUTO, CATS_PATH_FUSED = 0, 1
+CATS_COMPACT_BALLOT, CATS_COMPACT_PREDICATED, CATS_COMPACT_ATOMIC = 0, 1, 2
+
+
 class PlanInfo(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int), ("m", ctypes.c_int), ("max_batch", ctypes.c_int), ("w_dtype", ctypes.c_int),
                 ("device", ctypes.c_int), ("num_sms", ctypes.c_int), ("grid", ctypes.c_int),
@@ -49,6 +62,9 @@ _SIGS = {
     "cats_calib_hist": (I, [P, U64, I, P, P, P, P]),
     "cats_calib_step": (I, [P, P, U64, I, D, P, P, P, P, P]),
     "cats_mlp_plan_create": (I, [I, I, I, I, I, I, P]),
+    "cats_mlp_plan_options_init": (I, [P]),
+    "cats_mlp_plan_create_ex": (I, [I, I, I, I, I, I, P, P]),
+    "cats_xsparse_plan_create_ex": (I, [I, I, I, I, I, I, P, P]),
     "cats_mlp_plan_destroy": (None, [P]),
     "cats_mlp_plan_info": (I, [P, P]),
     "cats_mlp_workspace_bytes": (I, [P, P]),

@@ -305,8 +305,20 @@ cudaError_t ensure_smem_attr(const void *func, size_t smem) {
 namespace {
 // kind 0: gated-MLP plan (d, m); kind 1: App. B input-sparse projection plan (d = d_out, m = d_in)
 cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int device, int num_sms, int kind,
-                          cats_mlp_plan_t **out) {
+                          const cats_mlp_plan_options_t *opt_in, cats_mlp_plan_t **out) {
     if (!out) return CATS_E_NULL;
+    cats_mlp_plan_options_t o;
+    cats_mlp_plan_options_init(&o);
+    if (opt_in) {
+        if (opt_in->size != sizeof(cats_mlp_plan_options_t)) return CATS_E_SHAPE;
+        o = *opt_in;
+    }
+    if (o.path != CATS_PATH_AUTO && o.path != CATS_PATH_FUSED) return CATS_E_UNSUPPORTED;
+    if (o.compaction < CATS_COMPACT_BALLOT || o.compaction > CATS_COMPACT_ATOMIC) return CATS_E_UNSUPPORTED;
+    if (o.lazy_tail < 0 || o.min_tiles < 1 || o.l2_prefetch < 0 || o.max_stages < 0 || o.max_stages == 1 ||
+        (o.rows_per_tile != 0 && o.rows_per_tile != 2 && o.rows_per_tile != 4 && o.rows_per_tile != 6) ||
+        o.xs_cols < 0 || o.xs_ranges < 0 || o.xs_ranges > 8)
+        return CATS_E_SHAPE;
     if (d <= 0 || m <= 0) return CATS_E_SHAPE;
     if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
     if (max_batch < 1 || max_batch > CATS_MAX_BATCH) return CATS_E_BATCH;
@@ -328,10 +340,9 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.esize = esize;
         p.vec = 16 / esize;
         p.nchunks = d * esize / 16;
-        const char *abl = std::getenv("CATS_ABLATION_PREDICATED");
-        p.ablation_predicated = abl && abl[0] == '1';
-        const char *nrf = std::getenv("CATS_K12_NR");
-        p.nr_force = nrf ? std::atoi(nrf) : 0;
+        p.compaction = kind == 0 ? o.compaction : CATS_COMPACT_BALLOT;
+        p.nr_force = o.rows_per_tile;
+        p.trace = o.trace != 0;
         p.kind = kind;
         p.g1 = 0;
         if (kind == 1) {  // App. B: kernel XS only (xsparse.cu)
@@ -339,9 +350,7 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
             // segment), clusters of R <= 8 ranges of the kept list; the most CTAs up to `cps` per SM whose
             // shared memory fits, ties to the widest segment; segments under 128 B only when no wider one
             // divides d_out. Two CTAs per SM unless x (staged in shared memory) needs the whole SM.
-            const char *xc = std::getenv("CATS_XS_COLS"), *xr = std::getenv("CATS_XS_R");  // experiments
-            const char *xm = std::getenv("CATS_XS_MMA");
-            p.xs_no_mma = xm && xm[0] == '0';
+            p.xs_no_mma = o.xs_mma == 0;
             for (int b = 1; b <= max_batch; ++b) {
                 PlanData::XsCfg &c = p.xs[b];
                 bool fits = false;
@@ -369,18 +378,16 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
                     fits = best > 0;
                 }
                 if (!fits) return CATS_E_UNSUPPORTED;
-                if (xc && std::atoi(xc) > 0 && d % std::atoi(xc) == 0 && (std::atoi(xc) * esize) % 16 == 0 &&
-                    std::atoi(xc) * esize <= 512) {
-                    c.cols = std::atoi(xc);
+                if (o.xs_cols > 0 && d % o.xs_cols == 0 && (o.xs_cols * esize) % 16 == 0 && o.xs_cols * esize <= 512) {
+                    c.cols = o.xs_cols;
                     c.q = d / c.cols;
                 }
-                if (xr && std::atoi(xr) >= 1 && std::atoi(xr) <= 8) c.r = std::atoi(xr);
+                if (o.xs_ranges >= 1) c.r = o.xs_ranges;
                 if (xs_smem_bytes(p, b) > kSmemBudget) return CATS_E_UNSUPPORTED;
                 // with a device: shrink the clusters until every one of them is resident at once (the GPCs'
                 // SM counts need not be multiples of the cluster footprint)
                 c.clusters = -1;
-                const char *xns = std::getenv("CATS_XS_NOSHRINK");  // experiment: keep R, allow a partial second wave
-                if (query_device && !(xns && xns[0] == '1') && cudaSetDevice(device) == cudaSuccess) {
+                if (query_device && !o.xs_no_shrink && cudaSetDevice(device) == cudaSuccess) {
                     for (;;) {
                         c.clusters = xs_active_clusters(p, b);
                         if (c.clusters < 0 || c.clusters >= c.q || c.r == 1) break;
@@ -391,8 +398,6 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
             size_t off = 0;
             p.off_sched = off;   off = align_up(off + kSchedBytes, 256);
             p.off_tokmask = off; off = align_up(off + (size_t)m, 256);  // per-input keep bits (introspection)
-            const char *trc = std::getenv("CATS_TRACE");
-            p.trace = trc && trc[0] == '1';
             p.off_trace = off;
             p.trace_bytes = p.trace ? (size_t)kTraceKernels * kTraceCtas * kTraceSlots * 8 : 0;
             off = align_up(off + p.trace_bytes, 256);
@@ -420,8 +425,8 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.off_xstage = off;  off = align_up(off + (size_t)max_batch * d * esize, 256);
         p.off_ystage = off;  off = align_up(off + (size_t)max_batch * d * 4, 256);
         // split path (b >= 2): x1 per compact position and the KB range partials
-        const char *sm = std::getenv("CATS_SPLIT_MIN_B");
-        p.split_min_b = sm ? std::max(2, std::atoi(sm)) : 2;
+        // non-default compaction modes (the App. D ablation) run K12-based kernels at every batch size
+        p.split_min_b = (o.path == CATS_PATH_FUSED || p.compaction != CATS_COMPACT_BALLOT) ? CATS_MAX_BATCH + 1 : 2;
         size_t part_bytes = 0, x1_bytes = 0;
         for (int b = 2; b <= max_batch; ++b) {
             if (!split_supported(p, b)) continue;
@@ -431,18 +436,14 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.off_x1 = off;      off = align_up(off + x1_bytes, 256);
         p.off_tmask = off;   off = align_up(off + (size_t)((m + 1) / 2) * 4, 256);
         p.off_part = off;    off = align_up(off + part_bytes, 256);
-        const char *mtl = std::getenv("CATS_K12_MIN_TILES");
-        p.k12_min_tiles = mtl ? std::max(1, std::atoi(mtl)) : 2;
-        const char *pf = std::getenv("CATS_K12_L2PF");
-        p.k12_l2pf = pf ? std::max(0, std::atoi(pf)) : 0;  // measured: prefetching only slows the drain
-        const char *eg = std::getenv("CATS_K12_EAGER");
-        p.k12_eager = eg ? std::atoi(eg) : 0;
-        const char *ks = std::getenv("CATS_K12_STAGES");
-        p.k12_max_stages = ks ? std::max(2, std::atoi(ks)) : 0;
-        const char *tr = std::getenv("CATS_TRACE");
-        p.trace = tr && tr[0] == '1';
-        const char *lt = std::getenv("CATS_LAZY_TAIL");
-        p.lazy_tail = lt ? std::max(0, std::atoi(lt)) : 8;
+        const bool atomic_list = p.compaction == CATS_COMPACT_ATOMIC;  // App. D Alg. 1: global idcs list
+        p.off_gidx = off;    off = align_up(off + (atomic_list ? (size_t)m * 4 : 0), 256);
+        p.off_gval = off;    off = align_up(off + (atomic_list ? (size_t)m * max_batch * 4 : 0), 256);
+        p.k12_min_tiles = o.min_tiles;
+        p.k12_l2pf = o.l2_prefetch;  // measured: prefetching only slows the drain (default 0)
+        p.k12_eager = o.eager;
+        p.k12_max_stages = o.max_stages;
+        p.lazy_tail = o.lazy_tail;
         p.off_trace = off;
         p.trace_bytes = p.trace ? (size_t)kTraceKernels * kTraceCtas * kTraceSlots * 8 : 0;
         off = align_up(off + p.trace_bytes, 256);
@@ -455,14 +456,37 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
 }
 }  // namespace
 
+extern "C" cats_status_t cats_mlp_plan_options_init(cats_mlp_plan_options_t *o) {
+    if (!o) return CATS_E_NULL;
+    std::memset(o, 0, sizeof *o);
+    o->size = sizeof *o;
+    o->path = CATS_PATH_AUTO;
+    o->compaction = CATS_COMPACT_BALLOT;
+    o->lazy_tail = 8;
+    o->min_tiles = 2;
+    o->xs_mma = 1;
+    return CATS_OK;
+}
+
 extern "C" cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_dtype_t dt, int device, int num_sms,
                                               cats_mlp_plan_t **out) {
-    return plan_create(d, m, max_batch, dt, device, num_sms, 0, out);
+    return plan_create(d, m, max_batch, dt, device, num_sms, 0, nullptr, out);
+}
+
+extern "C" cats_status_t cats_mlp_plan_create_ex(int d, int m, int max_batch, cats_dtype_t dt, int device, int num_sms,
+                                                 const cats_mlp_plan_options_t *opt, cats_mlp_plan_t **out) {
+    return plan_create(d, m, max_batch, dt, device, num_sms, 0, opt, out);
 }
 
 extern "C" cats_status_t cats_xsparse_plan_create(int d_in, int d_out, int max_batch, cats_dtype_t dt, int device,
                                                   int num_sms, cats_mlp_plan_t **out) {
-    return plan_create(d_out, d_in, max_batch, dt, device, num_sms, 1, out);
+    return plan_create(d_out, d_in, max_batch, dt, device, num_sms, 1, nullptr, out);
+}
+
+extern "C" cats_status_t cats_xsparse_plan_create_ex(int d_in, int d_out, int max_batch, cats_dtype_t dt, int device,
+                                                     int num_sms, const cats_mlp_plan_options_t *opt,
+                                                     cats_mlp_plan_t **out) {
+    return plan_create(d_out, d_in, max_batch, dt, device, num_sms, 1, opt, out);
 }
 
 extern "C" cats_status_t cats_xsparse_gemv(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_in_major,
@@ -555,10 +579,19 @@ cudaError_t launch_mlp(const PlanData &p, const void *x, int b, const void *Wg, 
 }
 
 cats_status_t run_mlp(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd, float t,
-                      int dense, float *y, void *ws, cudaStream_t st) {
+                      int dense, float *y, void *ws, cudaStream_t st, cudaEvent_t ev_mid = nullptr) {
     cudaError_t e = cudaSetDevice(p.device);
-    const int mode = dense ? kModeDense : (p.ablation_predicated && b == 1 ? kModePredicated : kModeCats);
-    if (e == cudaSuccess) e = launch_mlp(p, x, b, Wg, Wu, Wd, t, mode, y, ws, st, nullptr);
+    if (e != cudaSuccess) return cuda_status(e);
+    if (!dense && p.compaction == CATS_COMPACT_ATOMIC) {
+        // App. D Alg. 1: launch 1 = gate GEMV, SiLU, Mask and atomic appends to idcs; launch 2 = sparse up x v
+        // and down projection over idcs (both K12 instantiations, chained by programmatic dependent launch)
+        e = launch_k12(p, x, b, Wg, Wu, Wd, t, kModeAtomicGate, nullptr, y, ws, st);
+        if (e == cudaSuccess && ev_mid) e = cudaEventRecord(ev_mid, st);
+        if (e == cudaSuccess) e = launch_k12(p, x, b, Wg, Wu, Wd, t, kModeAtomicList, nullptr, y, ws, st);
+        return cuda_status(e);
+    }
+    const int mode = dense ? kModeDense : (p.compaction == CATS_COMPACT_PREDICATED ? kModePredicated : kModeCats);
+    e = launch_mlp(p, x, b, Wg, Wu, Wd, t, mode, y, ws, st, ev_mid);
     return cuda_status(e);
 }
 
@@ -587,10 +620,11 @@ extern "C" cats_status_t cats_mlp_decode_profiled(const cats_mlp_plan_t *plan, c
     for (int i = 0; i < 3; ++i) ev[i] = static_cast<cudaEvent_t>(events[i]);
     cudaError_t e = cudaSetDevice(p.device);
     if (e == cudaSuccess) e = cudaEventRecord(ev[0], st);
-    // K12: ev[1] right after the kernel (= ev[2]); split path: ev[1] between KA and KB
-    if (e == cudaSuccess) e = launch_mlp(p, x, b, W_gate, W_up, W_down_nm, t, kModeCats, y, ws, st, ev[1]);
-    if (e == cudaSuccess) e = cudaEventRecord(ev[2], st);
-    return cuda_status(e);
+    if (e != cudaSuccess) return cuda_status(e);
+    // K12: ev[1] right after the kernel (= ev[2]); two-launch paths: ev[1] between the launches
+    rc = run_mlp(p, x, b, W_gate, W_up, W_down_nm, t, 0, y, ws, st, ev[1]);
+    if (rc != CATS_OK) return rc;
+    return cuda_status(cudaEventRecord(ev[2], st));
 }
 
 extern "C" cats_status_t cats_mlp_dense(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
@@ -605,6 +639,7 @@ extern "C" cats_status_t cats_mlp_decode_host(const cats_mlp_plan_t *plan, const
                                               const void *W_gate, const void *W_up, const void *W_down_nm, float t,
                                               float *y_host, void *ws, size_t ws_bytes, cats_stream_t s) {
     if (!plan || !x_host || !y_host || !W_gate || !W_up || !W_down_nm) return CATS_E_NULL;
+    if (plan->p.kind != 0) return CATS_E_UNSUPPORTED;  // an input-sparse projection plan
     if (b < 1 || b > plan->p.max_batch) return CATS_E_BATCH;
     if (!ws || ws_bytes < plan->p.ws_bytes) return CATS_E_WORKSPACE;
     if (!aligned16(ws) || !aligned16(W_gate) || !aligned16(W_up) || !aligned16(W_down_nm)) return CATS_E_ALIGN;
@@ -636,6 +671,7 @@ extern "C" cats_status_t cats_mlp_decode_host(const cats_mlp_plan_t *plan, const
 extern "C" cats_status_t cats_mlp_gate_act(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
                                            float *acts, void *ws, size_t ws_bytes, cats_stream_t s) {
     if (!plan || !x || !W_gate || !acts) return CATS_E_NULL;
+    if (plan->p.kind != 0) return CATS_E_UNSUPPORTED;  // an input-sparse projection plan
     if (b < 1 || b > plan->p.max_batch) return CATS_E_BATCH;
     if (!ws || ws_bytes < plan->p.ws_bytes) return CATS_E_WORKSPACE;
     if (!aligned16(x) || !aligned16(W_gate) || !aligned16(ws)) return CATS_E_ALIGN;
@@ -705,7 +741,9 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
 extern "C" cats_status_t cats_mlp_kernels_per_call(const cats_mlp_plan_t *plan, int b, int *kernels) {
     if (!plan || !kernels) return CATS_E_NULL;
     if (b < 1 || b > plan->p.max_batch) return CATS_E_BATCH;
-    *kernels = plan->p.kind == 1 ? 1 : (b >= plan->p.split_min_b && split_supported(plan->p, b)) ? 2 : 1;
+    const PlanData &p = plan->p;
+    *kernels = p.kind == 1 ? 1 : p.compaction == CATS_COMPACT_ATOMIC ? 2
+                               : (b >= p.split_min_b && split_supported(p, b)) ? 2 : 1;
     return CATS_OK;
 }
 

@@ -2,7 +2,7 @@
 //
 // 128-bit streaming loads, bf16 unpacking, mbarrier + cp.async.bulk (the TMA bulk-copy engine)
 // wrappers, programmatic-dependent-launch controls and warp reductions. Nothing here knows about
-// CATS; the method's arithmetic lives in k1_gate.cu / k2_sparse.cu / calib.cu.
+// CATS; the method's arithmetic lives in mlp_fused.cu / mlp_split.cu / xsparse.cu / calib.cu.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -170,12 +170,14 @@ __device__ __forceinline__ void trace_put(unsigned long long *tr, int kernel, in
 }
 
 // ---- exact fixed point for order-independent (deterministic) accumulation ----
-// A value y is accumulated as the integer q = round(y * 2^30) held in two int32 halves,
-// q = hi * 2^22 + lo. The split uses the fp32 "magic number" rounding trick (all full-rate FADD /
-// IADD, no slow float->int64 conversion): t = y * 2^8 is pre-scaled by the caller (exact),
-// hi = round(t) via t + 1.5*2^23, the exact remainder f = t - hi (|f| <= 1/2), lo = round(f * 2^22).
-// Only lo is rounded, so q = round(y * 2^30) exactly (|t| < 2^21). Larger |t| take a slow path.
-constexpr int kFixLoBits = 22;
+// A value y is accumulated as the integer q = round(y * 2^38) held in two int32 halves,
+// q = hi * 2^30 + lo with lo kept in [0, 2^30). The caller pre-scales t = y * 2^8 (exact);
+// hi += round(t) via the fp32 "magic number" trick (t + 1.5*2^23: full-rate FADD / IADD), the exact
+// remainder f = t - round(t) (|f| <= 1/2) gives lo += round(f * 2^30) (|.| <= 2^29), and a carry
+// renormalises lo after every add. Only f * 2^30 is rounded, so each add is exactly round(y * 2^38)
+// (|t| < 2^21; larger |t| take a slow int64 path). Resolution 2^-38 (3.6e-12) absolute; range:
+// |y| < 2^25 (3.4e7) for the int64 total, |partial of one thread| < 2^23.
+constexpr int kFixLoBits = 30;
 constexpr float kFixPre = 256.0f;                  // 2^8: callers pre-scale y by this (exact)
 constexpr float kFixMagic = 12582912.0f;           // 1.5 * 2^23
 constexpr int kFixMagicBits = 0x4B400000;
@@ -184,21 +186,20 @@ __device__ __forceinline__ void fix_acc(int &hi, int &lo, float t) {
         const float h = t + kFixMagic;
         hi += __float_as_int(h) - kFixMagicBits;
         const float f = t - (h - kFixMagic);
-        lo += __float_as_int(fmaf(f, 4194304.0f, kFixMagic)) - kFixMagicBits;  // round(f * 2^22)
+        lo += __float2int_rn(f * 1073741824.0f);  // round(f * 2^30), |f| <= 1/2
     } else {
-        const long long q = __float2ll_rn(t * 4194304.0f);
+        const long long q = __float2ll_rn(t * 1073741824.0f);
         hi += (int)(q >> kFixLoBits);
         lo += (int)(q & ((1ll << kFixLoBits) - 1));
     }
-}
-__device__ __forceinline__ void fix_renorm(int &hi, int &lo) {  // keep |lo| < 2^22 (exact)
-    const int c = lo >> kFixLoBits;
+    const int c = lo >> kFixLoBits;  // carry (floor): lo back into [0, 2^30)
     hi += c;
     lo -= c << kFixLoBits;
 }
 __device__ __forceinline__ long long fix_value(int hi, int lo) { return ((long long)hi << kFixLoBits) + lo; }
-constexpr int kFixShift = 30;  // q is in units of 2^-30
-__device__ __forceinline__ float fix_to_float(long long q) { return (float)((double)q * (1.0 / 1073741824.0)); }
+constexpr int kFixShift = 38;  // q is in units of 2^-38
+// one correct rounding int64 -> fp32, then an exact power-of-two scale
+__device__ __forceinline__ float fix_to_float(long long q) { return __ll2float_rn(q) * 3.637978807091713e-12f; }
 
 // ---- warp reductions (fixed xor-butterfly: every lane ends with the same, order-fixed sum) ----
 __device__ __forceinline__ float warp_allreduce_sum(float v) {

@@ -26,8 +26,11 @@ constexpr int kMaxStages = 8;
 constexpr int kModeCats = 0;          // CATS_t decode
 constexpr int kModeDense = 1;         // every neuron active (the library's dense MLP)
 constexpr int kModeGateOnly = 2;      // SiLU(x W_gate) only (calibration data collection)
-constexpr int kModePredicated = 3;    // ablation (CATS_ABLATION_PREDICATED=1): CATS y, but every row's W_up /
-                                      // W_down loaded (App. D Alg. 2, mask-predicated, no compaction)
+constexpr int kModePredicated = 3;    // App. D Alg. 2 (CATS_COMPACT_PREDICATED): no compaction, UD jobs = fixed
+                                      // tile halves, Mask predicates the row loads (inactive rows read as 0)
+constexpr int kModeAtomicGate = 4;    // App. D Alg. 1 (CATS_COMPACT_ATOMIC), launch 1: gate + SiLU + Mask +
+                                      // atomic appends of (id, v) to the global idcs list
+constexpr int kModeAtomicList = 5;    // App. D Alg. 1, launch 2: up / down over the idcs list (no GATE jobs)
 
 struct PlanData {
     int d, m, max_batch;
@@ -39,29 +42,30 @@ struct PlanData {
     int g1;             // max K12 CTAs over batch sizes (sizes the partial buffer)
     // workspace layout (byte offsets)
     size_t off_sched, off_idx, off_tokmask, off_vals, off_cnt, off_ypart, off_xstage, off_ystage, ws_bytes;
-    bool trace;         // CATS_TRACE=1 at plan creation: kernels stamp %globaltimer into the workspace
-    int lazy_tail;      // K12 stops reserving tile ids for the last lazy_tail * grid tiles (CATS_LAZY_TAIL)
-    int split_min_b;    // batches b >= split_min_b run the split path KA + KB (CATS_SPLIT_MIN_B)
-    int k12_max_stages; // 0 = as many K12 stages as fit (CATS_K12_STAGES caps it, for experiments)
-    int k12_min_tiles;  // K12 grid <= ntiles / k12_min_tiles (CATS_K12_MIN_TILES)
-    int k12_eager;      // K12 fills every stage with claimed tiles at start (CATS_K12_EAGER)
-    int k12_l2pf;       // K12 static tiles per CTA prefetched into L2 at start (CATS_K12_L2PF)
-    int nr_force;       // 0 = automatic tile height; 2 / 4 forces it (CATS_K12_NR)
+    bool trace;         // options.trace: kernels stamp %globaltimer into the workspace
+    int lazy_tail;      // K12 stops reserving tile ids for the last lazy_tail * grid tiles (options.lazy_tail)
+    int split_min_b;    // batches b >= split_min_b run the split path KA + KB (9 = never: options.path FUSED)
+    int k12_max_stages; // 0 = as many K12 stages as fit (options.max_stages caps it)
+    int k12_min_tiles;  // K12 grid <= ntiles / k12_min_tiles (options.min_tiles)
+    int k12_eager;      // K12 fills every stage with claimed tiles at start (options.eager)
+    int k12_l2pf;       // K12 static tiles per CTA prefetched into L2 at start (options.l2_prefetch)
+    int nr_force;       // 0 = automatic tile height; 2 / 4 / 6 forces it (options.rows_per_tile)
+    int compaction;     // cats_compaction_t (options.compaction)
     int kind;           // 0 = gated-MLP plan, 1 = App. B input-sparse projection plan (d = d_out, m = d_in)
     struct XsCfg {            // kind 1 (xsparse.cu), per batch size b = 1..8:
         int cols, q, r;       //   columns per CTA, column parts, cluster size (ranges of the kept list)
         int clusters;         //   clusters resident at once (-1: planned without a device)
     } xs[9];
-    bool xs_no_mma;           // CATS_XS_MMA=0: XS keeps the FFMA2 path at every batch (experiments)
-    bool ablation_predicated;  // CATS_ABLATION_PREDICATED=1: decode in kModePredicated (K12 only)
+    bool xs_no_mma;           // options.xs_mma = 0: XS keeps the FFMA2 path at every batch (experiments)
     size_t off_x1, off_part;  // split path: x1 per compact position [m][max_b]; KB partials [R][max_b][d]
     size_t off_tmask;         // split path: per-tile active-row mask words (KA -> KB), zero between calls
     size_t off_trace, trace_bytes;
+    size_t off_gidx, off_gval;  // App. D Alg. 1 mode: the global idcs list (ids, v per token), arbitrary order
 };
 
 // K12 tile height NR (W_gate rows per GATE job; a UD job carries NR/2 neurons = the same bytes).
 inline int k12_rows_per_tile(const PlanData &p, int b) {
-    if (p.nr_force == 2 || p.nr_force == 4 || (p.nr_force == 6 && b == 1)) return p.nr_force;  // CATS_K12_NR
+    if (p.nr_force == 2 || p.nr_force == 4 || (p.nr_force == 6 && b == 1)) return p.nr_force;  // options
     // 4-row tiles whenever two 4-row stages fit (measured at d = 5120, b = 1: 4 rows x 2 stages beats
     // 2 rows x 5 stages, 55.6 vs 60.6 us; per-job costs are per row pair)
     const size_t row = (size_t)p.d * p.esize;
@@ -94,6 +98,7 @@ constexpr int kSplitAGroups = 2;                         // KA job streams per C
 constexpr int kSplitAThreads = (kSplitAWarps + kSplitAGroups) * 32;
 constexpr int kSplitBMaxThreads = 672;                   // KB: <= 20 consumer warps + 1 producer warp
 constexpr int kSplitFifo = 64;                           // KA active-neuron FIFO (power of two)
+constexpr int kKbReducers = 64;                          // KB: the last K CTAs to finish sum the partials
 
 template <int NR, int B>
 struct SplitDesc {   // one KA ring stage: GATE(tile) or UP(<= NR active neurons)
@@ -113,8 +118,8 @@ constexpr int kSplitMmaMinB = 4;  // batches from which KA / KB use warp-level b
 inline bool split_kb_mma(const PlanData &p, int b) {  // instantiated for 1, 4, 5 tiles per warp
     return b >= kSplitMmaMinB && p.esize == 2 && (p.d == 1024 || p.d == 4096 || p.d == 5120);
 }
-// scheduler words at the workspace base: [0..1] tile counter / CTA exits, [2] KB grid barrier,
-// [8 + q] KB arrival tickets of column part q (q < 16)
+// scheduler words at the workspace base: [0..1] tile counter / CTA exits, [2] KB arrival tickets,
+// [3] App. D Alg. 1 append counter, [8 + q] KB range tickets of column part q (q < 16)
 constexpr size_t kSchedBytes = 128;
 inline int split_q(const PlanData &p, int b) {  // KB column parts (<= 16)
     if (split_kb_mma(p, b)) return 4;

@@ -30,7 +30,7 @@
 //    consumer barrier; UD jobs one named barrier.
 //  * Determinism under dynamic scheduling: a UD job's contribution y_job[c] = sum_i x1_i Wd[i][c]
 //    (<= NU neurons of ONE tile, ascending, fp32, fixed order) is converted once to an exact
-//    fixed-point integer round(y_job * 2^30) (split into two int32 halves, cats_device.cuh
+//    fixed-point integer round(y_job * 2^38) (split into two int32 halves, cats_device.cuh
 //    fix_acc) and added to the thread's integer accumulator. Integer
 //    addition is associative, so y does not depend on which CTA took which tile or in which order:
 //    bit-reproducible. (Replaces the paper's fp16 tl.atomic_add into Y.)
@@ -75,6 +75,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
              int d, int m, int stages, float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask,
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
              unsigned long long *__restrict__ yacc, float *__restrict__ y, unsigned int *__restrict__ sched,
+             int32_t *__restrict__ gidx, float *__restrict__ gval,
              int lazy_tail, int eager, int l2pf, unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
@@ -93,6 +94,8 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     const uint32_t row_bytes = (uint32_t)d * (uint32_t)sizeof(T);
     const uint32_t stage_bytes = (uint32_t)NR * row_bytes;
     const int ntiles = (m + NR - 1) / NR;
+    const bool list_mode = mode == kModeAtomicList;  // App. D Alg. 1, launch 2: work units = chunks of idcs
+    const bool has_y = mode != kModeGateOnly && mode != kModeAtomicGate;
 
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char *ring = smem;                                                           // [stages][stage_bytes]
@@ -117,7 +120,8 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     if (warp == NW) {
         // ===================================== PRODUCER WARP =====================================
         const bool dense = mode == kModeDense;
-        const bool gate_only = mode == kModeGateOnly;
+        const bool gate_only = mode == kModeGateOnly || mode == kModeAtomicGate;  // no UD jobs from this launch
+        const bool predicated = mode == kModePredicated;
         const uint64_t policy = l2_evict_first_policy();
         // Tile claims (lane 0). While many tiles remain, the next GATE tile is reserved one issue ahead
         // (t_res: a predicated atomic whose round trip overlaps the jobs in between; nothing reads
@@ -125,10 +129,12 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         // claimed when a stage is free to stream it, so no CTA sits on unstarted work while others
         // drain (balanced tail), and small layers spread over all CTAs.
         unsigned int t_res = kNoTile;  // raw counter value; tile id = dyn_base + counter
+        unsigned int sched_list_n = 0; // list mode: length of the global idcs list
         // static first tiles per CTA: `stages` of them go straight into the ring, up to l2pf more are
         // prefetched into L2 (cp.async.bulk.prefetch) -- both before griddepcontrol.wait, so they use
         // the HBM time while the previous kernel drains -- and taken in order before any claim
-        const int batch = max(1, min(stages + l2pf, ntiles / (int)gridDim.x));
+        const int batch = list_mode ? 0 : max(1, min(stages + l2pf, ntiles / (int)gridDim.x));
+        int ntl = ntiles;            // claimable work units: GATE tiles, or (list mode) idcs chunks of NU
         const unsigned int dyn_base = gridDim.x * (unsigned)batch;        // first dynamically claimed tile
         const unsigned int sbase = blockIdx.x * (unsigned)batch;          // this CTA's static tiles
         int snext = min(batch, stages);                                    // next static tile to issue
@@ -148,18 +154,57 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             if (q_head != q_tail) {  // UD job: W_up and W_down rows of <= NU active neurons
                 const Desc &Q = queue[q_head % QCAP];
                 const int qn = Q.n;
+                // a negative id marks a row whose load Mask predicates off (Alg. 2 mode): no copy, read as 0
+                const bool has = lane < 2 * qn && Q.id[lane >> 1] >= 0;
+                const uint32_t nrows = (uint32_t)__popc(__ballot_sync(0xffffffffu, has));
                 if (lane == 0) {
                     D = Q;
-                    mbar_arrive_expect_tx(&full[s], (uint32_t)qn * 2u * row_bytes);
+                    mbar_arrive_expect_tx(&full[s], nrows * row_bytes);
                 }
                 __syncwarp();
-                if (lane < 2 * qn) {  // one bulk copy per lane: row (lane & 1) of neuron lane >> 1
+                if (has) {  // one bulk copy per lane: row (lane & 1) of neuron lane >> 1
                     const int i = lane >> 1;
                     const size_t j = (size_t)Q.id[i];
                     bulk_g2s(dst + (size_t)lane * row_bytes, ((lane & 1) ? Wd : Wu) + j * d, row_bytes, &full[s],
                              policy);
                 }
                 ++q_head;
+            } else if (list_mode) {  // Alg. 1 list kernel: UD job = the next NU entries of the global idcs
+                unsigned int tile = t_res;
+                if (lane == 0 && tile == kNoTile) tile = atomicAdd(&sched[0], 1u);
+                tile = __shfl_sync(0xffffffffu, tile, 0);
+                if (tile < (unsigned)ntl) {
+                    if (lane == 0) {
+                        t_res = kNoTile;
+                        claim_tile_async(t_res, sched, tile + (unsigned)lazy_tail < (unsigned)ntl);
+                    }
+                    const int base = (int)tile * NU;
+                    const int qn = min(NU, (int)sched_list_n - base);
+                    if (lane < qn) {
+                        D.id[lane] = __ldcg(gidx + base + lane);
+#pragma unroll
+                        for (int tk = 0; tk < B; ++tk) D.v[lane][tk] = __ldcg(gval + (size_t)(base + lane) * B + tk);
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        D.type = kJobUD;
+                        D.tile = (int)tile;
+                        D.n = qn;
+                        mbar_arrive_expect_tx(&full[s], (uint32_t)qn * 2u * row_bytes);
+                    }
+                    __syncwarp();
+                    if (lane < 2 * qn)
+                        bulk_g2s(dst + (size_t)lane * row_bytes, ((lane & 1) ? Wd : Wu) + (size_t)D.id[lane >> 1] * d,
+                                 row_bytes, &full[s], policy);
+                } else {
+                    if (lane == 0) {
+                        t_res = tile;  // past the end: keep it, no further claims
+                        D.type = kJobEnd;
+                        D.n = 0;
+                        mbar_arrive_expect_tx(&full[s], 0u);
+                    }
+                    ended = true;
+                }
             } else {
                 unsigned int tile;
                 const bool from_static = snext < batch;
@@ -177,7 +222,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                         ++snext;
                     } else if (lane == 0) {
                         t_res = kNoTile;
-                        claim_tile_async(t_res, sched, tile + (unsigned)lazy_tail < (unsigned)ntiles);
+                        claim_tile_async(t_res, sched, tile + (unsigned)lazy_tail < (unsigned)ntl);
                     }
                     if (lane == 0) {
                         D.type = kJobGate;
@@ -231,13 +276,19 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             }
         }
         pdl_wait_primary();
-        if (lane == 0) claim_tile_async(t_res, sched, dyn_base + (unsigned)lazy_tail < (unsigned)ntiles);
+        if (list_mode) {  // the gate launch's atomic appends are complete: chunks of NU list entries
+            unsigned int n_app = 0;
+            if (lane == 0) n_app = *reinterpret_cast<volatile unsigned int *>(sched + 3);
+            sched_list_n = __shfl_sync(0xffffffffu, n_app, 0);
+            ntl = (int)((sched_list_n + NU - 1) / NU);
+        }
+        if (lane == 0) claim_tile_async(t_res, sched, dyn_base + (unsigned)lazy_tail < (unsigned)ntl);
         prod = __shfl_sync(0xffffffffu, prod, 0);
         ps = prod % stages;
         gates_inflight = prod;
-        // the rest of the ring fills as jobs retire (UD work first); with `eager` (small layers) the
-        // free stages are filled with claimed tiles right away
-        if (eager) {
+        // the rest of the ring fills as jobs retire (UD work first); with `eager` (small layers, and the
+        // list kernel, which has no static GATE tiles to prime the ring) the free stages are filled now
+        if (eager || list_mode) {
             while (!ended && prod < stages && issue_job()) {
             }
         }
@@ -273,17 +324,37 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 }
                 // (ablation mode: every row of the tile is queued -- the paper's Alg. 2 mask-predicated
                 //  loads at tile granularity; inactive rows carry v = 0, so y is unchanged)
-                const bool act = (lane < n) && (bits != 0u || mode == kModePredicated);
+                const bool act = (lane < n) && bits != 0u;
                 const uint32_t bal = __ballot_sync(0xffffffffu, act);
                 const int rank = __popc(bal & ((1u << lane) - 1u));
                 const int nact = __popc(bal);
+                if (predicated && lane < n) {
+                    // App. D Alg. 2 (no compaction): the tile's rows in two fixed halves, one UD job each
+                    // whatever the mask; Mask predicates each row's load (negative id = not loaded, 0)
+                    Desc &Q = queue[(q_tail + lane / NU) % QCAP];
+                    const int i = lane % NU;
+                    Q.id[i] = act ? r0 + lane : -1 - (r0 + lane);
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) Q.v[i][tk] = ((bits >> tk) & 1u) ? vrow[tk] : 0.0f;
+                    if (i == 0) {
+                        Q.type = kJobUD;
+                        Q.tile = tile;
+                        Q.n = min(NU, n - lane);
+                    }
+                }
                 if (act) {
                     const int pos = r0 + rank;
                     idx[pos] = r0 + lane;
                     tokmask[pos] = (uint8_t)bits;
 #pragma unroll
                     for (int tk = 0; tk < B; ++tk) vals[(size_t)pos * B + tk] = ((bits >> tk) & 1u) ? vrow[tk] : 0.0f;
-                    if (!gate_only) {  // queue the tile's active neurons, NU per UD job, ascending
+                    if (mode == kModeAtomicGate) {  // App. D Alg. 1 line 4: append (j, v_j) to the global idcs
+                        const unsigned int ap = atomicAdd(&sched[3], 1u);
+                        gidx[ap] = r0 + lane;
+#pragma unroll
+                        for (int tk = 0; tk < B; ++tk) gval[(size_t)ap * B + tk] = ((bits >> tk) & 1u) ? vrow[tk] : 0.0f;
+                    }
+                    if (!gate_only && !predicated) {  // queue the tile's active neurons, NU per UD job, ascending
                         Desc &Q = queue[(q_tail + rank / NU) % QCAP];
                         const int i = rank % NU;
                         Q.id[i] = r0 + lane;
@@ -297,7 +368,8 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     }
                 }
                 if (lane == 0) cnt[tile] = nact;
-                if (!gate_only) q_tail += (nact + NU - 1) / NU;
+                if (predicated) q_tail += (n + NU - 1) / NU;
+                else if (!gate_only) q_tail += (nact + NU - 1) / NU;
                 --gates_inflight;
                 __syncwarp();
             }
@@ -332,14 +404,13 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 xr[tk][k] = ch < nch ? *reinterpret_cast<const uint4 *>(x + (size_t)tk * d + (size_t)ch * VEC)
                                      : make_uint4(0u, 0u, 0u, 0u);
         }
-        int yhi[B][CPT][VEC], ylo[B][CPT][VEC];  // exact fixed-point partial of y (units 2^-30), own chunks
+        int yhi[B][CPT][VEC], ylo[B][CPT][VEC];  // exact fixed-point partial of y (units 2^-38), own chunks
 #pragma unroll
         for (int tk = 0; tk < B; ++tk)
 #pragma unroll
             for (int k = 0; k < CPT; ++k)
 #pragma unroll
                 for (int e = 0; e < VEC; ++e) yhi[tk][k][e] = ylo[tk][k][e] = 0;
-        int n_since_renorm = 0;
 
         int s = 0;
         uint32_t phase = 0;
@@ -389,17 +460,20 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             } else {  // kJobUD
                 ++n_ud;
                 float vj[NU][B];  // descriptor -> registers before releasing the stage
+                bool live[NU];    // row loaded (false: predicated off by Mask in Alg. 2 mode -> zeros)
 #pragma unroll
-                for (int i = 0; i < NU; ++i)
+                for (int i = 0; i < NU; ++i) {
+                    live[i] = i < n && (mode != kModePredicated || desc[s].id[i] >= 0);
 #pragma unroll
                     for (int tk = 0; tk < B; ++tk) vj[i][tk] = desc[s].v[i][tk];
+                }
                 uint4 wu[NU][CPT], wd[NU][CPT];
 #pragma unroll
                 for (int i = 0; i < NU; ++i)
 #pragma unroll
                     for (int k = 0; k < CPT; ++k) {
                         const int ch = tid + k * NC;
-                        const bool ok = i < n && ch < nch;
+                        const bool ok = live[i] && ch < nch;
                         wu[i][k] = ok ? lds128(sbase + (uint32_t)(2 * i) * row_bytes + (uint32_t)ch * 16u)
                                       : make_uint4(0u, 0u, 0u, 0u);
                         wd[i][k] = ok ? lds128(sbase + (uint32_t)(2 * i + 1) * row_bytes + (uint32_t)ch * 16u)
@@ -463,15 +537,6 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                             fix_acc(yhi[tk][k][e], ylo[tk][k][e], yj);
                         }
                 }
-                if (++n_since_renorm == 256) {  // keep the low halves far from int32 overflow
-                    n_since_renorm = 0;
-#pragma unroll
-                    for (int tk = 0; tk < B; ++tk)
-#pragma unroll
-                        for (int k = 0; k < CPT; ++k)
-#pragma unroll
-                            for (int e = 0; e < VEC; ++e) fix_renorm(yhi[tk][k][e], ylo[tk][k][e]);
-                }
             }
             if (++s == stages) { s = 0; phase ^= 1u; }
         }
@@ -488,7 +553,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         // (integer adds performed at L2, any order -> deterministic). The last CTA to finish converts
         // yacc to fp32 once, writes y, and re-zeroes yacc and the tile scheduler for the next call.
         __shared__ unsigned int s_last;
-        if (mode != kModeGateOnly) {
+        if (has_y) {
             consumer_barrier<NC>();  // every consumer warp is past its last job: the ring is idle
             unsigned long long *sbuf = reinterpret_cast<unsigned long long *>(ring);
             const int tpc = min(B, (int)(((size_t)stages * stage_bytes) / ((size_t)d * 8)));  // tokens per chunk
@@ -530,7 +595,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         consumer_barrier<NC>();
         if (s_last) {
             __threadfence();
-            if (mode != kModeGateOnly) {
+            if (has_y) {
                 // 8 independent L2 loads in flight per thread (the accumulator was just written by
                 // the bulk-reduce engine of every SM; a serial loop would pay one L2 trip per step)
                 const int n2 = B * d / 2;
@@ -554,6 +619,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             if (tid == 0) {
                 sched[0] = 0u;
                 sched[1] = 0u;
+                if (list_mode) sched[3] = 0u;  // the idcs list was consumed: re-arm the append counter
             }
         }
         trace_stamp(trace, 0, 3);
@@ -598,7 +664,8 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
         static_cast<const T *>(Wd), p.d, p.m, stages, t, mode, reinterpret_cast<int32_t *>(w + p.off_idx),
         reinterpret_cast<uint8_t *>(w + p.off_tokmask), reinterpret_cast<float *>(w + p.off_vals),
         reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<unsigned long long *>(w + p.off_ypart), y,
-        reinterpret_cast<unsigned int *>(w + p.off_sched), p.lazy_tail * k12_grid(p, B), p.k12_eager, p.k12_l2pf,
+        reinterpret_cast<unsigned int *>(w + p.off_sched), reinterpret_cast<int32_t *>(w + p.off_gidx),
+        reinterpret_cast<float *>(w + p.off_gval), p.lazy_tail * k12_grid(p, B), p.k12_eager, p.k12_l2pf,
         p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();

@@ -463,7 +463,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
     if (tid == 0 && atomicAdd(&sched[1], 1u) == gridDim.x - 1) {  // last CTA: reset the tile scheduler
         sched[0] = 0u;
         sched[1] = 0u;
-        sched[2] = 0u;  // KB's grid-barrier counter
+        sched[2] = 0u;  // KB's arrival-ticket counter
     }
     trace_stamp(trace, 0, 3);
 }
@@ -718,28 +718,43 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     }
     trace_stamp(trace, 1, 2);
 
-    // ---- grid barrier (all R*Q CTAs are resident: one per SM, launched together) ----
+    // ---- phase 2 by the LAST kKbReducers CTAs to finish phase 1 (no grid barrier) ----
+    // Every CTA takes an arrival ticket after its partial is written; the CTAs with the last K tickets
+    // wait until all G have arrived and then each sums a slice of the R partials in fixed order
+    // r = 0..R-1 into y. The others exit at once (their SMs go to the next kernel). A reducer only ever
+    // waits for CTAs that have not arrived yet, and at most K of the SM slots are held by reducers, so
+    // the kernel completes whenever more than K CTAs fit on the device at once -- no co-residency of the
+    // whole grid is assumed (the planner checks the occupancy).
+    __shared__ unsigned int s_ticket;
     __syncthreads();
     if (tid == 0) {
-        // arrival counter sched[2] (zeroed by KA's last CTA, which completes before KB passes
-        // griddepcontrol.wait): the barrier opens when every CTA of this grid has arrived
-        __threadfence();
-        atomicAdd(&sched[2], 1u);
+        __threadfence();  // this CTA's partial is visible before its ticket
+        s_ticket = atomicAdd(&sched[2], 1u);
+    }
+    __syncthreads();
+    const int G = gridDim.x;
+    const int K = min(G, kKbReducers);
+    const int red_idx = (int)s_ticket - (G - K);  // < 0: not a reducer
+    if (red_idx < 0) {
+        trace_stamp(trace, 1, 3);
+        trace_stamp(trace, 1, 4);
+        return;
+    }
+    if (tid == 0) {
         unsigned int seen;
         do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(sched + 2) : "memory");
-        } while (seen < gridDim.x);
+        } while (seen < (unsigned)G);
     }
     __syncthreads();
     trace_stamp(trace, 1, 3);
-    for (int i = blockIdx.x * nth + tid; i < ntiles; i += gridDim.x * nth) tmask[i] = 0u;  // for the next call
-    if (blockIdx.x == 0 && tid < Q) sched[8 + tid] = 0u;  // arrival tickets (every CTA took one before the barrier)
+    for (int i = red_idx * nth + tid; i < ntiles; i += K * nth) tmask[i] = 0u;  // for the next call
+    if (red_idx == 0 && tid < Q) sched[8 + tid] = 0u;  // arrival tickets (all taken before the tickets)
 
-    // ---- fixed-order reduction: y[e] = sum_{r=0..R-1} part[r][e], this CTA's slice of B*d ----
+    // ---- fixed-order reduction: y[e] = sum_{r=0..R-1} part[r][e], this reducer's slice of B*d ----
     {
         const int total4 = B * d / 4;
-        const int G = gridDim.x, gidx = blockIdx.x;
-        const int g0 = (int)((long long)total4 * gidx / G), g1 = (int)((long long)total4 * (gidx + 1) / G);
+        const int g0 = (int)((long long)total4 * red_idx / K), g1 = (int)((long long)total4 * (red_idx + 1) / K);
         const int ng = g1 - g0;
         // r-slices per float4 group: enough that each thread has <= 8 partials (one batch of loads)
         const int ns = ng > 0 ? max(1, min(min(R, nth / ng), max((R + 7) / 8, 4))) : 1;
@@ -852,6 +867,8 @@ bool kb_supported(const PlanData &p, int b) {  // KB alone fits this shape and b
     return sb >= 2 && split_kb_smem(p, b, sb) <= kSmemBudget;
 }
 bool split_supported(const PlanData &p, int b) {
+    // KB's phase 2 holds up to kKbReducers CTAs (one per SM) waiting for the rest: more SMs than that
+    if (p.num_sms <= kKbReducers) return false;
     if (b < 2 || b > 8 || !kb_supported(p, b)) return false;
     const int sa = split_ka_stages(p, b);
     return sa >= 2 && split_ka_smem(p, b, sa) <= kSmemBudget;  // >= 2 stages per group

@@ -22,12 +22,15 @@ ap.add_argument("--dense", action="store_true")
 ap.add_argument("--copies", type=int, default=0, help="weight copies (default: enough for >= 400 MB)")
 ap.add_argument("--reps", type=int, default=50)
 ap.add_argument("--tag", default="")
+ap.add_argument("--opt", action="append", default=[],
+                help="plan option key=value (cats_mlp_plan_options_t field), repeatable")
 a = ap.parse_args()
+opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt}
 dev = torch.device("cuda:0")
 d, m = cats_synth.MODELS[a.model]
 m = a.m or m
 dt = torch.bfloat16
-plan = cats.MlpPlan(d, m, max_batch=8, dtype=dt)
+plan = cats.MlpPlan(d, m, max_batch=8, dtype=dt, **opts)
 ws = plan.workspace()
 W0 = [w.to(dev) for w in cats_synth.mlp_weights(d, m, dt, layer=0)]
 copies = a.copies or max(4, -(-400_000_000 // (3 * 2 * d * m)))
@@ -75,4 +78,4 @@ us = min(best)
 print(json.dumps(dict(tag=a.tag, model=a.model, d=d, m=m, b=a.batch, k=a.k, dense=a.dense, copies=copies,
                       us=round(us, 3), us_runs=[round(v, 3) for v in best], union=U,
                       eff_GBps=round(eff / (us * 1e-6) / 1e9, 1), grid=plan.info["grid"],
-                      lazy_tail=os.environ.get("CATS_LAZY_TAIL", "default"))), flush=True)
+                      opts=opts)), flush=True)

@@ -24,10 +24,13 @@ ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--k", type=float, default=0.5)
 ap.add_argument("--reps", type=int, default=50)
 ap.add_argument("--tag", default="")
+ap.add_argument("--opt", action="append", default=[],
+                help="plan option key=value (cats_mlp_plan_options_t field), repeatable")
 a = ap.parse_args()
+opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt}
 dev = torch.device("cuda:0")
 dt = torch.bfloat16
-plan = cats.XsparsePlan(a.d_in, a.d_out, max_batch=8, dtype=dt)
+plan = cats.XsparsePlan(a.d_in, a.d_out, max_batch=8, dtype=dt, **opts)
 ws = plan.workspace()
 W0 = cats_synth.attn_weights(a.d_in, a.d_out, dt).to(dev)
 copies = max(4, -(-400_000_000 // (2 * a.d_in * a.d_out)))

@@ -1,6 +1,6 @@
-"""Per-CTA timeline of one pipelined decode step (CATS_TRACE=1 globaltimer stamps).
+"""Per-CTA timeline of one pipelined decode step (options.trace = 1 globaltimer stamps).
 
-    CATS_TRACE=1 python scripts/trace_decode.py [--model mistral-7b] [--batch 1] [--graph]
+    python scripts/trace_decode.py [--model mistral-7b] [--batch 1] [--graph]
 """
 import argparse
 import ctypes
@@ -8,7 +8,6 @@ import json
 import os
 import sys
 
-os.environ["CATS_TRACE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
@@ -30,7 +29,7 @@ if a.m:
 dev = torch.device("cuda:0")
 W = [w.to(dev) for w in cats_synth.mlp_weights(d, m, torch.bfloat16)]
 copies = [W] + [[w.clone() for w in W] for _ in range(3)]
-plan = cats.MlpPlan(d, m, max_batch=8)
+plan = cats.MlpPlan(d, m, max_batch=8, trace=1)
 ws = plan.workspace()
 off, nbytes = ctypes.c_size_t(), ctypes.c_size_t()
 plan._lib.cats_mlp_trace_info(plan.handle, ctypes.byref(off), ctypes.byref(nbytes))

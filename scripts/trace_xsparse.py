@@ -1,4 +1,4 @@
-"""Per-CTA timeline of the App. B kernel XS (CATS_TRACE=1 globaltimer stamps), one eager call.
+"""Per-CTA timeline of the App. B kernel XS (options.trace = 1 globaltimer stamps), one eager call.
 
     python scripts/trace_xsparse.py [--d-in 4096] [--d-out 6144] [--batch 1] [--k 0.5]
 """
@@ -7,7 +7,6 @@ import ctypes
 import os
 import sys
 
-os.environ["CATS_TRACE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
@@ -22,7 +21,7 @@ ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--k", type=float, default=0.5)
 a = ap.parse_args()
 dev = torch.device("cuda:0")
-plan = cats.XsparsePlan(a.d_in, a.d_out, max_batch=8)
+plan = cats.XsparsePlan(a.d_in, a.d_out, max_batch=8, trace=1)
 ws = plan.workspace()
 off, nbytes = ctypes.c_size_t(), ctypes.c_size_t()
 plan._lib.cats_mlp_trace_info(plan.handle, ctypes.byref(off), ctypes.byref(nbytes))

@@ -255,5 +255,60 @@ def test_xsparse_plan_and_validation_without_gpu():
     mp = cats.MlpPlan(4096, 14336, max_batch=1, dtype=torch.bfloat16, num_sms=148)
     assert _xs_rc(mp) == "CATS_E_UNSUPPORTED"
     assert _decode_rc(p) == "CATS_E_UNSUPPORTED"
+    rc = lib.cats_mlp_decode_host(p.handle, FAKE, 1, FAKE, FAKE, FAKE, 0.1, FAKE, FAKE, p.workspace_bytes, None)
+    assert lib.cats_status_string(rc).decode() == "CATS_E_UNSUPPORTED"
+    rc = lib.cats_mlp_gate_act(p.handle, FAKE, 1, FAKE, FAKE, FAKE, p.workspace_bytes, None)
+    assert lib.cats_status_string(rc).decode() == "CATS_E_UNSUPPORTED"
+    rc = lib.cats_mlp_dense(p.handle, FAKE, 1, FAKE, FAKE, FAKE, FAKE, FAKE, p.workspace_bytes, None)
+    assert lib.cats_status_string(rc).decode() == "CATS_E_UNSUPPORTED"
     if not torch.cuda.is_available():
         assert _xs_rc(p) == "CATS_E_CUDA"
+
+
+def test_plan_options():
+    """cats_mlp_plan_options_t: defaults, explicit kernel-path / App. D ablation selection, validation
+    (the library reads no environment variables)."""
+    o = cats.plan_options()
+    assert (o.size, o.path, o.compaction, o.lazy_tail, o.min_tiles, o.xs_mma) == (
+        ctypes.sizeof(_lib.PlanOptions), 0, 0, 8, 2, 1)
+    auto = cats.MlpPlan(4096, 11008, max_batch=8, num_sms=148)
+    assert [cats.cats_mlp_kernels_per_call(auto, b) for b in range(1, 9)] == [1] + [2] * 7
+    fused = cats.MlpPlan(4096, 11008, max_batch=8, num_sms=148, path=cats.CATS_PATH_FUSED)
+    assert [cats.cats_mlp_kernels_per_call(fused, b) for b in range(1, 9)] == [1] * 8
+    pred = cats.MlpPlan(4096, 11008, max_batch=8, num_sms=148, compaction=cats.CATS_COMPACT_PREDICATED)
+    assert [cats.cats_mlp_kernels_per_call(pred, b) for b in range(1, 9)] == [1] * 8
+    atom = cats.MlpPlan(4096, 11008, max_batch=8, num_sms=148, compaction=cats.CATS_COMPACT_ATOMIC)
+    assert [cats.cats_mlp_kernels_per_call(atom, b) for b in range(1, 9)] == [2] * 8  # gate + list kernel
+    assert atom.workspace_bytes >= auto.workspace_bytes + 11008 * 4 * 9  # the global idcs list (ids + v)
+    assert cats.MlpPlan(5120, 13824, num_sms=148, rows_per_tile=2).info["rows_per_tile"] == 2
+    # KB's last-64 reduction needs more than 64 SMs: smaller devices take K12 at every batch size
+    small = cats.MlpPlan(4096, 11008, max_batch=8, num_sms=64)
+    assert [cats.cats_mlp_kernels_per_call(small, b) for b in range(1, 9)] == [1] * 8
+    for bad, err in [({"path": 7}, "CATS_E_UNSUPPORTED"), ({"compaction": 3}, "CATS_E_UNSUPPORTED"),
+                     ({"rows_per_tile": 3}, "CATS_E_SHAPE"), ({"min_tiles": 0}, "CATS_E_SHAPE"),
+                     ({"max_stages": 1}, "CATS_E_SHAPE"), ({"lazy_tail": -1}, "CATS_E_SHAPE")]:
+        with pytest.raises(cats.CatsError) as e:
+            cats.MlpPlan(4096, 11008, num_sms=148, **bad)
+        assert e.value.name == err, bad
+    o = cats.plan_options()
+    o.size = 4
+    h = ctypes.c_void_p()
+    rc = lib.cats_mlp_plan_create_ex(64, 64, 1, 1, 0, 148, ctypes.byref(o), ctypes.byref(h))
+    assert lib.cats_status_string(rc).decode() == "CATS_E_SHAPE"
+    with pytest.raises(TypeError):
+        cats.plan_options(no_such_field=1)
+    src = open(os.path.join(ROOT, "paper_2404_08763_b200", "csrc", "api.cu")).read()
+    assert "getenv" not in src
+
+
+def test_binding_checks_shapes_before_the_abi():
+    """The C ABI carries no sizes: the binding checks every tensor against the plan."""
+    p = cats.MlpPlan(256, 512, max_batch=4, dtype=torch.bfloat16, num_sms=148)
+    x = torch.zeros(2, 256, dtype=torch.bfloat16)
+    w = torch.zeros(512, 256, dtype=torch.bfloat16)
+    with pytest.raises(ValueError):   # host tensors are rejected before any call
+        cats.cats_mlp_decode(p, x, w, w, w, 0.1, ws=torch.zeros(8, dtype=torch.uint8))
+    with pytest.raises(ValueError):
+        cats.cats_mlp_decode_host(p, torch.zeros(2, 255, dtype=torch.bfloat16), w, w, w, 0.1)
+    with pytest.raises(TypeError):
+        cats.cats_mlp_decode_host(p, torch.zeros(2, 256, dtype=torch.float32), w, w, w, 0.1)

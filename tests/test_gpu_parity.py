@@ -6,6 +6,9 @@ Acceptance (BASELINE.json north_star):
     those band entries only (reading R9);
   * calibration threshold bit-exact with the oracle's order statistic (and its counts).
 """
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 import pytest
 import torch
@@ -18,6 +21,7 @@ pytestmark = pytest.mark.gpu
 
 BAND = 1e-3
 Y_TOL = 2e-3
+EL_TOL = 1e-4
 
 
 def _dev(t):
@@ -35,15 +39,51 @@ def _rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def run_parity(d, m, b, dtype, k, seed=0, heavy=False, num_sms=0, check_y=True):
+def oracle_mlp(ox, og, ou, od, t, mode=oracle.SPARSE, keep_in=None):
+    """oracle.mlp token by token on host threads (the C oracle releases the GIL; tokens are
+    independent, so the results are the identical serial per-token computations)."""
+    b = ox.shape[0]
+    if b == 1:
+        return oracle.mlp(ox, og, ou, od, t=t, mode=mode, keep_in=keep_in)
+    def one(i):
+        return oracle.mlp(ox[i:i + 1], og, ou, od, t=t, mode=mode,
+                          keep_in=None if keep_in is None else keep_in[i:i + 1])
+    with ThreadPoolExecutor(max_workers=min(b, os.cpu_count() or 1)) as ex:
+        outs = list(ex.map(one, range(b)))
+    return tuple(np.concatenate([o[j] for o in outs]) for j in range(3))
+
+
+def check_y(yg, y_ref):
+    """North-star bound (rel-L2 <= 2e-3 per token) and an element-wise bound |y - y_ref| <= 1e-4 rms(y_ref)
+    per token (fp32 accumulation over <= 2 m terms: ~sqrt(n) 2^-24 relative, x1 hi/lo split 2^-16 relative
+    per term on the b >= 4 tensor-core path). Returns the worst rel-L2."""
+    errs = []
+    for i in range(y_ref.shape[0]):
+        ref = y_ref[i]
+        if not np.abs(ref).any():
+            assert not np.abs(yg[i]).any(), f"token {i}: y must be exactly 0"
+            errs.append(0.0)
+            continue
+        errs.append(_rel_l2(yg[i], ref))
+        rms = float(np.sqrt(np.mean(ref ** 2)))
+        worst = float(np.abs(yg[i] - ref).max())
+        assert worst <= EL_TOL * rms, f"token {i}: max |dy| {worst:.3g} > {EL_TOL} rms {rms:.3g}"
+    assert max(errs) <= Y_TOL, errs
+    return max(errs)
+
+
+def run_parity(d, m, b, dtype, k, seed=0, heavy=False, num_sms=0, check=True, opts=None, wd_scale=1.0):
     Wg, Wu, Wd = cats_synth.mlp_weights(d, m, dtype, layer=seed, heavy=heavy)
+    if wd_scale != 1.0:  # power of two: exact in bf16 / fp32, scales y exactly (mask unchanged)
+        Wd = (Wd.float() * wd_scale).to(dtype)
     x = cats_synth.tokens(b, d, dtype, seed=1 + seed, heavy=heavy)
     ox, og, ou, od = (cats_synth.to_oracle(a) for a in (x, Wg, Wu, Wd))
     # threshold: Eq. 3 on the oracle's |SiLU| of these tokens (any t >= 0 is a valid test point)
-    _, v64, _ = oracle.mlp(ox, og, ou, od, t=0.0, mode=oracle.DENSE)
+    zero = np.zeros((m, d), og.dtype)
+    _, v64, _ = oracle_mlp(ox, og, zero, zero, 0.0, mode=oracle.DENSE)
     t = float(oracle.calibrate_sort(v64.astype(np.float32), k).t) if k > 0 else 0.0
 
-    plan = cats.MlpPlan(d, m, max_batch=b, dtype=dtype, num_sms=num_sms)
+    plan = cats.MlpPlan(d, m, max_batch=b, dtype=dtype, num_sms=num_sms, **(opts or {}))
     ws = plan.workspace()
     dx, dg, du, dd = (_dev(a) for a in (x, Wg, Wu, Wd))
     y = cats.cats_mlp_decode(plan, dx, dg, du, dd, t, ws=ws)
@@ -59,15 +99,11 @@ def run_parity(d, m, b, dtype, k, seed=0, heavy=False, num_sms=0, check_y=True):
     mism = (keep_gpu != keep64) & ~band
     assert not mism.any(), f"{int(mism.sum())} active-set mismatches outside the band"
     res = {"t": t, "band": int(band.sum()), "flips_in_band": int(((keep_gpu != keep64) & band).sum()),
-           "nnz_union": len(idx), "sparsity": 1 - keep_gpu.mean()}
-    if check_y:
+           "nnz_union": len(idx), "sparsity": 1 - keep_gpu.mean(), "kernels": cats.cats_mlp_kernels_per_call(plan, b)}
+    if check:
         keep_sub = np.where(band, keep_gpu, keep64).astype(np.uint8)
-        y_ref, _, _ = oracle.mlp(ox, og, ou, od, t=t, keep_in=keep_sub)
-        yg = y.cpu().numpy().astype(np.float64)
-        errs = [_rel_l2(yg[i], y_ref[i]) if np.abs(y_ref[i]).max() > 0 else float(np.abs(yg[i]).max())
-                for i in range(b)]
-        res["rel_l2_max"] = max(errs)
-        assert max(errs) <= Y_TOL, errs
+        y_ref, _, _ = oracle_mlp(ox, og, ou, od, t, keep_in=keep_sub)
+        res["rel_l2_max"] = check_y(y.cpu().numpy().astype(np.float64), y_ref)
     return res, (plan, ws, dx, dg, du, dd, y)
 
 
@@ -86,6 +122,10 @@ def run_parity(d, m, b, dtype, k, seed=0, heavy=False, num_sms=0, check_y=True):
 def test_parity_small(d, m, b, dtype, k):
     res, _ = run_parity(d, m, b, dtype, k, seed=d + m + b)
     assert res["rel_l2_max"] <= Y_TOL
+    if k > 0:  # the same inputs through the App. D ablation modes (Alg. 2 predicated, Alg. 1 atomic idcs)
+        for comp in (cats.CATS_COMPACT_PREDICATED, cats.CATS_COMPACT_ATOMIC):
+            r2, _ = run_parity(d, m, b, dtype, k, seed=d + m + b, opts={"compaction": comp})
+            assert r2["nnz_union"] == res["nnz_union"]
 
 
 @pytest.mark.parametrize("model,b,k,heavy", [
@@ -101,6 +141,58 @@ def test_parity_full_size(model, b, k, heavy):
     assert res["rel_l2_max"] <= Y_TOL
     if b == 1:
         assert abs(res["sparsity"] - k) < 0.01
+
+
+# Every kernel instantiation the planner selects for the BASELINE shapes: per model,
+# b = 1 -> K12 (NR = 6 at d = 4096, NR = 4 at d = 5120); b = 2, 3 -> KA + KB on CUDA cores; b = 4..8 ->
+# KA + KB on bf16 MMA (KB MT = 4 at d = 4096, MT = 5 at d = 5120). The batch is a template parameter, so
+# each (model, b) is a distinct kernel pair.
+@pytest.mark.parametrize("model", ["mistral-7b", "llama2-7b", "llama2-13b"])
+@pytest.mark.parametrize("b", [2, 3, 4, 5, 6, 7, 8])
+def test_parity_every_planned_batch(model, b):
+    d, m = cats_synth.MODELS[model]
+    k = {2: 0.5, 3: 0.7, 4: 0.5, 5: 0.9, 6: 0.7, 7: 0.5, 8: 0.5}[b]
+    res, _ = run_parity(d, m, b, torch.bfloat16, k, seed=50 + b, heavy=(b % 2 == 1))
+    assert res["kernels"] == 2  # the split path KA + KB
+
+
+@pytest.mark.parametrize("model,b", [("mistral-7b", 2), ("llama2-7b", 5), ("llama2-13b", 8)])
+def test_parity_fused_path_full_size(model, b):
+    """K12 at b >= 2 (options.path = FUSED: the fallback the planner takes where KA / KB do not fit)."""
+    d, m = cats_synth.MODELS[model]
+    res, _ = run_parity(d, m, b, torch.bfloat16, 0.5, seed=60 + b, opts={"path": cats.CATS_PATH_FUSED})
+    assert res["kernels"] == 1
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("b", [1, 8])
+def test_parity_llama13b_tp_shard(P, b):
+    """BASELINE config 3: the per-GPU shard m / P of Llama2-13B (the decode of one rank, b = 1 and 8)."""
+    d, m = cats_synth.MODELS["llama2-13b"]
+    res, _ = run_parity(d, m // P, b, torch.bfloat16, 0.5, seed=70 + P)
+    assert res["kernels"] == (1 if b == 1 else 2)
+
+
+@pytest.mark.parametrize("comp", ["predicated", "atomic"])
+@pytest.mark.parametrize("model,b,k", [("mistral-7b", 1, 0.5), ("llama2-7b", 1, 0.9), ("llama2-7b", 4, 0.7)])
+def test_parity_app_d_ablation_modes(comp, model, b, k):
+    """App. D Alg. 2 (mask-predicated row loads, no compaction) and Alg. 1 (atomic appends to a global idcs
+    list, then a list kernel) compute the same CATS y as the default ballot compaction."""
+    d, m = cats_synth.MODELS[model]
+    c = cats.CATS_COMPACT_PREDICATED if comp == "predicated" else cats.CATS_COMPACT_ATOMIC
+    res, (plan, ws, dx, dg, du, dd, y) = run_parity(d, m, b, torch.bfloat16, k, seed=80, opts={"compaction": c})
+    assert res["kernels"] == (2 if comp == "atomic" else 1)
+    y2 = cats.cats_mlp_decode(plan, dx, dg, du, dd, res["t"], ws=ws)
+    assert torch.equal(y, y2)  # deterministic in every mode (the atomic list order varies run to run)
+
+
+@pytest.mark.parametrize("b", [1, 4])
+@pytest.mark.parametrize("e", [-16, -8, 8, 16])
+def test_parity_output_magnitude_sweep(b, e):
+    """W_down scaled by 2^e scales y by 2^e exactly (mask unchanged): exercises the K12 fixed-point
+    accumulator (resolution 2^-38, R10) at b = 1 and the fp32 split path at b = 4."""
+    res, _ = run_parity(1024, 4096, b, torch.bfloat16, 0.5, seed=90, wd_scale=2.0 ** e)
+    assert res["rel_l2_max"] <= Y_TOL
 
 
 def test_t0_and_dense_path():
@@ -285,14 +377,13 @@ def test_calibration_full_size_config4():
 
 @pytest.mark.parametrize("d,m,b,k", [(4096, 11008, 2, 0.5), (4096, 11008, 8, 0.9), (5120, 3456, 5, 0.7),
                                      (264, 1000, 3, 0.5)])
-def test_split_path_matches_fused_path(d, m, b, k, monkeypatch):
+def test_split_path_matches_fused_path(d, m, b, k):
     """b >= 2 runs the split path (KA gate+up, KB down); forcing K12 on the same inputs must give the
     same y within the parity tolerance (the two differ only in fp32 summation order)."""
     Wg, Wu, Wd = (_dev(a) for a in cats_synth.mlp_weights(d, m, torch.bfloat16, layer=b))
     x = _dev(cats_synth.tokens(b, d, torch.bfloat16, seed=21))
     plan_s = cats.MlpPlan(d, m, max_batch=b)
-    monkeypatch.setenv("CATS_SPLIT_MIN_B", "9")
-    plan_f = cats.MlpPlan(d, m, max_batch=b)
+    plan_f = cats.MlpPlan(d, m, max_batch=b, path=cats.CATS_PATH_FUSED)
     t = 0.1 if k < 0.9 else 0.3
     ys = cats.cats_mlp_decode(plan_s, x, Wg, Wu, Wd, t, ws=plan_s.workspace())
     yf = cats.cats_mlp_decode(plan_f, x, Wg, Wu, Wd, t, ws=plan_f.workspace())

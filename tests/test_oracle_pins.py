@@ -429,3 +429,38 @@ def test_xsparse_gemv_brute_force_rationals():
                 exact = sum((Fraction(float(x[bt, i])) * Fraction(float(W[i, n])) for i in range(5)
                              if abs(Fraction(float(x[bt, i]))) >= Fraction(t)), Fraction(0))
                 assert Fraction(y[bt, n]) == exact
+
+
+def test_oracle_bf16_widening_matches_torch_for_every_finite_pattern():
+    """The oracle's bf16 -> double widening (cats_oracle.c `widen`) pinned against torch's own
+    bfloat16 -> float32 conversion for all 65 280 finite bit patterns (incl. subnormals and -0):
+    y = CATS_0(x) I through oracle.xsparse_gemv returns each x_c times 1 plus exact zeros."""
+    bits = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    finite = (bits & 0x7F80) != 0x7F80
+    bits = bits[finite]
+    ref = torch.from_numpy(bits.view(np.int16).copy()).view(torch.bfloat16).float().double().numpy()
+    n = 256
+    eye = np.zeros((n, n), np.uint16)
+    eye[np.arange(n), np.arange(n)] = 0x3F80  # bf16 1.0
+    pad = (-len(bits)) % n
+    xb = np.concatenate([bits, np.zeros(pad, np.uint16)]).reshape(-1, n)
+    got = np.concatenate([oracle.xsparse_gemv(xb[i:i + 1], eye, 0.0)[0][0] for i in range(xb.shape[0])])[:len(bits)]
+    assert np.array_equal(got, ref)  # -0 == +0; every other value bit-exact
+    assert np.array_equal(np.signbit(got[ref != 0]), np.signbit(ref[ref != 0]))
+    # the same widening seen through Eq. 3: the r-th smallest |a| is returned exactly as torch widens it
+    a = bits[np.random.default_rng(0).permutation(len(bits))[:5001]]
+    at = np.abs(torch.from_numpy(a.view(np.int16).copy()).view(torch.bfloat16).float().double().numpy())
+    for k in (0.1, 0.5, 0.9):
+        r = oracle.rank(k, len(a))
+        assert oracle.calibrate_sort(a, k).t == np.sort(at)[r - 1]
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_openmp_timing_build_is_bit_identical(dtype):
+    """The all-core timing build (same source, -fopenmp) returns exactly the serial checker's bits."""
+    x, Wg, Wu, Wd = _case(136, 417, 3, dtype, seed=4)
+    for mode, t in ((oracle.SPARSE, 0.05), (oracle.MASKED, 0.05), (oracle.DENSE, 0.0)):
+        a = oracle.mlp(x, Wg, Wu, Wd, t=t, mode=mode)
+        b = oracle.mlp(x, Wg, Wu, Wd, t=t, mode=mode, all_cores=True)
+        for u, v in zip(a, b):
+            assert np.array_equal(u, v)
