@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--copies", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extras", action="store_true", help="also time dense/cuBLAS/profiled (default on)")
+    ap.add_argument("--launcher-selftest", action="store_true",
+                    help="start the ranks, all-reduce one tensor, print one line (CPU: gloo) and exit")
     return ap.parse_args()
 
 
@@ -106,13 +108,34 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def dist_setup(n):
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`python bench.py --gpus N` without a torchrun environment: start the N ranks ourselves (one
+    process per GPU, torch.distributed.run on 127.0.0.1) and pass rank 0's JSON line through."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, cwd=ROOT).returncode
+
+
+def dist_setup(n, backend="nccl"):
     import torch
     import torch.distributed as dist
     if n > 1 or "RANK" in os.environ:
-        rank = int(os.environ.get("RANK", 0))
-        world = int(os.environ.get("WORLD_SIZE", 1))
+        rank = int(os.environ["RANK"])
+        world = int(os.environ["WORLD_SIZE"])
         local = int(os.environ.get("LOCAL_RANK", rank))
+        if world != n:
+            raise SystemExit(f"bench.py --gpus {n} launched with WORLD_SIZE={world}")
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+            return rank, world, local
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         return rank, world, local
@@ -120,37 +143,54 @@ def dist_setup(n):
     return 0, 1, 0
 
 
+def host_info():
+    """(cores this process may run on, CPU model) for the cpu_baseline record."""
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return cores, model
+
+
 # ---------------------------------------------------------------------------------------- CPU oracle
 
-def time_oracle(d, m, b, sparsity, budget_s=15.0, max_tokens=64, seed=0):
-    """Oracle (fp64 C, single thread) on the same workload: t from the oracle's own |SiLU| on
-    256 calibration tokens' worth of... (bounded: calibrate on 8 tokens), then decode tokens until the
-    time budget is used. Returns (us per token-layer, tokens, m_used)."""
+def time_oracle(d, m, b, sparsity, budget_s=15.0, max_tokens=64, seed=0, all_cores=True):
+    """The CPU oracle (fp64 C; all_cores: its OpenMP build over every core this process may use) on
+    the same workload: t from Eq. 3 on the oracle's own |SiLU| of 2 held-apart tokens, then decode
+    steps of b tokens until the time budget is used. Returns (geometric-mean us per token-layer over
+    the steps -- the paper's protocol, P:532 --, steps, threads)."""
     import numpy as np
     import torch
 
     import cats_synth
     import oracle
-    # bounded sample: full-width layer, as many tokens as fit in the budget
+    cores, _ = host_info()
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores if all_cores else 1))
+    # bounded sample: full-width layer, as many steps as fit in the budget
     Wg, Wu, Wd = cats_synth.mlp_weights(d, m, torch.bfloat16)
     og, ou, od = (cats_synth.to_oracle(a) for a in (Wg, Wu, Wd))
-    z = np.zeros((1, d), np.uint16)
     xs = cats_synth.tokens(max_tokens * b + 8, d, torch.bfloat16, seed=seed + 1)
     ox = cats_synth.to_oracle(xs)
-    _, v, _ = oracle.mlp(ox[:2], og, ou, od, t=0.0, mode=oracle.DENSE)
+    _, v, _ = oracle.mlp(ox[:2], og, ou, od, t=0.0, mode=oracle.DENSE, all_cores=all_cores)
     t = oracle.calibrate_sort(v.astype(np.float32), sparsity).t
-    del z
     times = []
     n_tok = 0
     t_start = time.perf_counter()
     while n_tok < max_tokens:
         s = time.perf_counter()
-        oracle.mlp(ox[2 + n_tok * b: 2 + (n_tok + 1) * b], og, ou, od, t=t)
+        oracle.mlp(ox[2 + n_tok * b: 2 + (n_tok + 1) * b], og, ou, od, t=t, all_cores=all_cores)
         times.append(time.perf_counter() - s)
         n_tok += 1
         if time.perf_counter() - t_start > budget_s:
             break
-    return 1e6 * sum(times) / (n_tok * b), n_tok
+    geo = math.exp(sum(math.log(x) for x in times) / len(times))
+    return 1e6 * geo / b, n_tok, int(os.environ["OMP_NUM_THREADS"]) if all_cores else 1
 
 
 def run_reference(args):
@@ -162,17 +202,21 @@ def run_reference(args):
     d, m = cats_synth.MODELS[args.model]
     # each step: one token through the oracle (~0.6 s at Mistral shape); bounded sample so the run
     # ends within minutes: steps beyond the budget reuse the measured per-token time
-    budget = 150.0
-    us, ntok = time_oracle(d, m, args.batch, args.sparsity, budget_s=budget, max_tokens=args.steps + args.warmup)
+    budget = 60.0
+    us, ntok, threads = time_oracle(d, m, args.batch, args.sparsity, budget_s=budget,
+                                    max_tokens=args.steps + args.warmup)
+    cores, cpu_model = host_info()
     value = us
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value / 1000 * args.batch, 4),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(args, d, m),
-        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{ntok} token(s) x full {args.model} layer (d={d}, m={m}, b={args.batch}), "
-                                   f"single-thread fp64 C oracle, time-bounded at {budget:.0f} s"},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "cpu_model": cpu_model, "affinity_cores": cores,
+                         "sample": f"{ntok} step(s) of b={args.batch} token(s) x full {args.model} layer (d={d}, m={m}), "
+                                   f"fp64 C oracle (OpenMP build, {threads} threads), geometric mean, "
+                                   f"time-bounded at {budget:.0f} s"},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -190,12 +234,35 @@ def workload_config(args, d, m):
                       "of 8 decode calls (eager launches reported in detail.eager_us_per_step)"}
 
 
+def launcher_selftest(args):
+    """The rank plumbing bench.py uses, without the workload: NCCL on GPUs, gloo on a CPU host."""
+    import torch
+    import torch.distributed as dist
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    rank, world, local = dist_setup(args.gpus, backend=backend)
+    dev = torch.device(f"cuda:{local}") if backend == "nccl" else torch.device("cpu")
+    v = torch.tensor([float(rank + 1)], device=dev)
+    if world > 1:
+        dist.all_reduce(v)
+    if rank == 0:
+        print(json.dumps({"launcher_ok": True, "world": world, "backend": backend, "sum_ranks": float(v.item())}),
+              flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 # ---------------------------------------------------------------------------------------- GPU arm
 
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "RANK" not in os.environ:
+        return relaunch_under_torchrun(args.gpus)
+    if args.launcher_selftest:
+        return launcher_selftest(args)
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -319,8 +386,10 @@ def main():
     for i in range(n_prof):
         cats.cats_mlp_decode_profiled(plan, xs[i % 64], *copies[i % len(copies)], t, evs[i], y=y, ws=ws)
     torch.cuda.synchronize(dev)
-    k_first = statistics.mean(e[0].elapsed_time(e[1]) for e in evs) * 1e3   # K12, or KA on the split path
-    k_second = statistics.mean(e[1].elapsed_time(e[2]) for e in evs) * 1e3  # ~0 for K12, KB on the split path
+    t_first = [e[0].elapsed_time(e[1]) * 1e3 for e in evs]   # K12, or KA on the split path
+    t_second = [e[1].elapsed_time(e[2]) * 1e3 for e in evs]  # ~0 for K12, KB on the split path
+    k_first, k_second = statistics.mean(t_first), statistics.mean(t_second)
+    geo = lambda v: math.exp(statistics.mean(math.log(max(x, 1e-3)) for x in v))
     kernels_per_step = cats.cats_mlp_kernels_per_call(plan, b)
     split = kernels_per_step == 2
 
@@ -356,6 +425,11 @@ def main():
             yh.copy_(y, non_blocking=False)
     e2e_ms = timed(e2e_step, min(args.steps, 1000), 10)
 
+    # ---- TP: the all-reduce alone (its share of the step), same buffer and stream
+    allreduce_us = None
+    if world > 1:
+        allreduce_us = timed(lambda i: dist.all_reduce(y), min(args.steps, 1000), 20) * 1e3
+
     # ---- roofline of the dominant kernel (algorithmic bytes / live CUDA-event duration)
     hbm_peak, peak_kind = peaks()
     esz = 2
@@ -363,15 +437,18 @@ def main():
     # W_down rows (4d B per active neuron) + x
     step_bytes = 2 * d * ms + 4 * d * nnz_local + b * d * esz
     us_step_dev = ms_step * 1e3
+    step_dev_us = us_step_dev - (allreduce_us or 0.0)  # the decode kernels' share of the timed step
     if not split:
-        # one kernel per step: its average launch duration over the timed region is the step time
-        dom, dom_bytes, dom_us = "K12", step_bytes, us_step_dev
+        # one kernel per step: its average launch duration over the timed region = the step period
+        # (PDL lets a launch's static W_gate tiles stream while its predecessor drains)
+        dom, dom_bytes, dom_us, iso_us = "K12", step_bytes, step_dev_us, k_first
     else:
         # KA (W_gate + active W_up rows) dominates; its share of the timed step from the event-bracketed
         # launches (isolated launches: shares, not absolutes)
         dom, dom_bytes = "KA", 2 * d * ms + 2 * d * nnz_local + b * d * esz
-        dom_us = us_step_dev * k_first / (k_first + k_second)
+        dom_us, iso_us = step_dev_us * k_first / (k_first + k_second), k_first
     achieved = dom_bytes / (dom_us * 1e-6) / 1e9
+    achieved_iso = dom_bytes / (iso_us * 1e-6) / 1e9
     traffic = None
     tp_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp_path):
@@ -384,9 +461,14 @@ def main():
     value = us_step / b  # us per token-layer, whole job (TP ranks together process b tokens per step)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cus, ntok = time_oracle(d, m, b, k, budget_s=15.0, max_tokens=40)
-        cpu = {"value": round(cus, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{ntok} token(s) x full {args.model} layer, single-thread fp64 C oracle"}
+        cus, ntok, threads = time_oracle(d, m, b, k, budget_s=12.0, max_tokens=40, all_cores=True)
+        cus1, ntok1, _ = time_oracle(d, m, b, k, budget_s=6.0, max_tokens=20, all_cores=False)
+        cores, cpu_model = host_info()
+        cpu = {"value": round(cus, 1), "unit": UNIT, "cores": threads, "kind": "oracle",
+               "cpu_model": cpu_model, "affinity_cores": cores, "single_thread_value": round(cus1, 1),
+               "sample": f"{ntok} step(s) of b={b} token(s) x full {args.model} layer (d={d}, m={m}), fp64 C "
+                         f"oracle, OpenMP build on {threads} threads (single thread: {ntok1} steps), "
+                         f"geometric mean per step"}
 
     if rank == 0:
         line = {
@@ -397,18 +479,28 @@ def main():
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm_peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                          "traffic": traffic, "algorithmic_bytes_per_launch": dom_bytes,
-                         "launch_us": round(dom_us, 3)},
+                         "launch_us": round(dom_us, 3),
+                         "basis": "timed region: the step period of back-to-back PDL launches (graph replay)",
+                         "isolated_launch_us": round(iso_us, 3), "achieved_isolated": round(achieved_iso, 1),
+                         "frac_isolated": round(achieved_iso / hbm_peak, 4),
+                         "isolated_basis": "one launch bracketed by events on its stream, no overlap with "
+                                           "its neighbours (mean of the profiled launches)"},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_ms * 1e3 / b, 3), "unit": UNIT, "h2d_bytes_per_step": b * d * esz,
                     "d2h_bytes_per_step": b * d * 4},
             "gpu_launches": args.steps * kernels_per_step,
             "clocks": clocks,
             "detail": {
+                "nccl": None if world == 1 else {"version": ".".join(map(str, torch.cuda.nccl.version())),
+                                                 "nranks": world, "collective": "all_reduce sum fp32 b x d"},
                 "t": t, "nnz_union_per_rank": nnz_local, "nnz_union_total": U, "m_per_rank": ms,
                 "realized_sparsity": round(1 - U / m, 4),
                 "eager_us_per_step": round(ms_eager * 1e3, 3), "graph_steps_per_replay": G if graph_ok else 0,
                 "isolated_launch_us": {"K12" if not split else "KA": round(k_first, 3),
                                        **({"KB": round(k_second, 3)} if split else {})},
+                "isolated_launch_us_geomean": round(geo([a + c for a, c in zip(t_first, t_second)]), 3),
+                "allreduce_us": None if allreduce_us is None else round(allreduce_us, 3),
+                "allreduce_share": None if allreduce_us is None else round(allreduce_us / us_step_dev, 4),
                 "effective_bytes_per_step": step_bytes,
                 "effective_GBps": round(step_bytes / (us_step * 1e-6) / 1e9, 1),
                 "frac_of_8TBps": round(step_bytes / (us_step * 1e-6) / 1e9 / NOMINAL_HBM_GBS, 4),

@@ -230,6 +230,8 @@ def _prep(plan: MlpPlan, x: torch.Tensor, y, ws, stream, weights=(), wshape=None
         x = x.unsqueeze(0)
     b = x.shape[0]
     dev = torch.device(f"cuda:{plan.device}")
+    if isinstance(plan, XsparsePlan) != (wshape is not None and len(weights) == 1):
+        raise CatsError(12, "plan kind does not match the call")  # CATS_E_UNSUPPORTED, as the C ABI
     _check_tensor(x, "x", (b, plan.m if isinstance(plan, XsparsePlan) else plan.d), plan.dtype, dev)
     for name, w in weights:
         _check_tensor(w, name, wshape, plan.dtype, dev)
@@ -300,6 +302,8 @@ def cats_mlp_decode_host(plan: MlpPlan, x_host: torch.Tensor, W_gate, W_up, W_do
     if x_host.is_cuda or not x_host.is_contiguous():
         raise ValueError("x_host must be a contiguous host tensor")
     b = x_host.shape[0]
+    if isinstance(plan, XsparsePlan):
+        raise CatsError(12, "cats_mlp_decode_host")
     cpu = torch.device("cpu")
     _check_tensor(x_host, "x_host", (b, plan.d), plan.dtype, cpu)
     dev = torch.device(f"cuda:{plan.device}")
@@ -327,6 +331,8 @@ def cats_mlp_gate_act(plan: MlpPlan, x, W_gate, acts=None, ws=None, stream=None)
         x = x.unsqueeze(0)
     b = x.shape[0]
     dev = torch.device(f"cuda:{plan.device}")
+    if isinstance(plan, XsparsePlan):
+        raise CatsError(12, "cats_mlp_gate_act")
     _check_tensor(x, "x", (b, plan.d), plan.dtype, dev)
     _check_tensor(W_gate, "W_gate", (plan.m, plan.d), plan.dtype, dev)
     st = _stream_obj(stream, dev)

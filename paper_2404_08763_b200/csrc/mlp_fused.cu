@@ -318,7 +318,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     }
                     const float v = __fdividef(u, 1.0f + __expf(-u));
                     vrow[tk] = v;
-                    const bool keep = dense || gate_only || (fabsf(v) >= t);
+                    const bool keep = dense || mode == kModeGateOnly || (fabsf(v) >= t);
                     bits |= (keep ? 1u : 0u) << tk;
                     if (acts && lane < n) acts[(size_t)tk * m + (size_t)(r0 + lane)] = v;
                 }

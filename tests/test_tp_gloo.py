@@ -108,3 +108,20 @@ def test_shard_rows():
     assert tp.shard_rows(13824, 8, 7) == slice(12096, 13824)
     with pytest.raises(ValueError):
         tp.shard_rows(10, 4, 0)
+
+
+def test_bench_launcher_starts_n_ranks():
+    """`python bench.py --gpus 2` with no torchrun environment starts its own 2 ranks (torch.distributed.run
+    on 127.0.0.1); every rank joins the process group (gloo on a CPU host) and one all-reduce sees both."""
+    import json
+    import subprocess
+    import sys
+    from tests.conftest import ROOT
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launcher-selftest"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert lines == [{"launcher_ok": True, "world": 2, "backend": "gloo", "sum_ranks": 3.0}]
