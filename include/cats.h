@@ -212,6 +212,9 @@ typedef struct {
     int32_t min_tiles;       /* K12 grid <= ntiles / min_tiles (>= 1) */
     int32_t eager;           /* K12 fills every ring stage with claimed tiles at start (0 / 1) */
     int32_t l2_prefetch;     /* K12 static tiles per CTA prefetched into L2 before griddepcontrol.wait (>= 0) */
+    int32_t tail_rows;       /* K12 tail tiles: rows per tile for the last tail_tiles x grid tiles (0 = uniform;
+                                2 .. NR-1) -- finer work units where the dynamic schedule ends */
+    int32_t tail_tiles;      /* K12 tail tiles per CTA (>= 0) */
     int32_t xs_cols;         /* App. B XS: columns per CTA (0 = auto) */
     int32_t xs_ranges;       /* App. B XS: cluster size R (0 = auto, else 1..8) */
     int32_t xs_mma;          /* App. B XS: 1 = tensor cores where the slab allows (default), 0 = FFMA2 only */

@@ -317,7 +317,8 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
     if (o.compaction < CATS_COMPACT_BALLOT || o.compaction > CATS_COMPACT_ATOMIC) return CATS_E_UNSUPPORTED;
     if (o.lazy_tail < 0 || o.min_tiles < 1 || o.l2_prefetch < 0 || o.max_stages < 0 || o.max_stages == 1 ||
         (o.rows_per_tile != 0 && o.rows_per_tile != 2 && o.rows_per_tile != 4 && o.rows_per_tile != 6) ||
-        o.xs_cols < 0 || o.xs_ranges < 0 || o.xs_ranges > 8)
+        o.xs_cols < 0 || o.xs_ranges < 0 || o.xs_ranges > 8 || o.tail_rows < 0 || o.tail_rows == 1 ||
+        o.tail_rows > 6 || o.tail_tiles < 0)
         return CATS_E_SHAPE;
     if (d <= 0 || m <= 0) return CATS_E_SHAPE;
     if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
@@ -342,6 +343,8 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.nchunks = d * esize / 16;
         p.compaction = kind == 0 ? o.compaction : CATS_COMPACT_BALLOT;
         p.nr_force = o.rows_per_tile;
+        p.tail_rows = o.tail_rows;
+        p.tail_tiles = o.tail_tiles;
         p.trace = o.trace != 0;
         p.kind = kind;
         p.g1 = 0;
@@ -710,7 +713,9 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
             *nnz_union = k;
             return CATS_OK;
         }
-        const int tr = k12_rows_per_tile(p, b), ntiles = k12_ntiles(p, b);
+        // per-tile segments: K12's geometry (tail tiles) when K12 ran, uniform tiles on the split path
+        const bool k12_ran = p.compaction != CATS_COMPACT_BALLOT || !(b >= p.split_min_b && split_supported(p, b));
+        const int ntiles = k12_ran ? k12_ntiles_geo(p, b) : k12_ntiles(p, b);
         std::vector<int32_t> idx(p.m), cnt(ntiles);
         std::vector<uint8_t> tm(p.m);
         cudaError_t e = cudaSetDevice(p.device);
@@ -722,8 +727,10 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
         uint32_t k = 0;
         if (nnz_per_token) std::fill(nnz_per_token, nnz_per_token + b, 0u);
         for (int c = 0; c < ntiles; ++c) {
-            const int64_t r0 = (int64_t)c * tr;
-            const int64_t R = std::min<int64_t>(tr, p.m - r0);
+            const int64_t r0 = k12_ran ? k12_tile_r0(p, b, c) : (int64_t)c * k12_rows_per_tile(p, b);
+            const int64_t r1 = k12_ran ? (c + 1 < ntiles ? k12_tile_r0(p, b, c + 1) : p.m)
+                                       : (int64_t)(c + 1) * k12_rows_per_tile(p, b);
+            const int64_t R = std::min<int64_t>(r1, p.m) - r0;
             if (cnt[c] < 0 || cnt[c] > R) return CATS_E_SHAPE;
             for (int i = 0; i < cnt[c]; ++i) {
                 idx_host[k] = idx[r0 + i];

@@ -75,7 +75,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
              int d, int m, int stages, float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask,
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
              unsigned long long *__restrict__ yacc, float *__restrict__ y, unsigned int *__restrict__ sched,
-             int32_t *__restrict__ gidx, float *__restrict__ gval,
+             int32_t *__restrict__ gidx, float *__restrict__ gval, int t1, int ns,
              int lazy_tail, int eager, int l2pf, unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
@@ -93,7 +93,11 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     const int nch = d * (int)sizeof(T) / 16;
     const uint32_t row_bytes = (uint32_t)d * (uint32_t)sizeof(T);
     const uint32_t stage_bytes = (uint32_t)NR * row_bytes;
-    const int ntiles = (m + NR - 1) / NR;
+    // tile geometry: t1 tiles of NR rows, then (tail) tiles of ns <= NR rows -- finer work units for the
+    // last tiles the dynamic scheduler hands out (k12_t1 / k12_tail_rows; ns == NR: uniform)
+    const int ntiles = t1 + max(0, (m - t1 * NR + ns - 1) / ns);
+    auto tile_r0 = [t1, ns](int tile) { return tile < t1 ? tile * NR : t1 * NR + (tile - t1) * ns; };
+    auto tile_rows = [t1, ns, m](int tile, int r0) { return min(tile < t1 ? NR : ns, m - r0); };
     const bool list_mode = mode == kModeAtomicList;  // App. D Alg. 1, launch 2: work units = chunks of idcs
     const bool has_y = mode != kModeGateOnly && mode != kModeAtomicGate;
 
@@ -216,8 +220,8 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     tile = __shfl_sync(0xffffffffu, tile, 0) + dyn_base;
                 }
                 if (tile < (unsigned)ntiles) {  // GATE job: a new tile of W_gate rows
-                    const int r0 = (int)tile * NR;
-                    const int nr = min(NR, m - r0);
+                    const int r0 = tile_r0((int)tile);
+                    const int nr = tile_rows((int)tile, r0);
                     if (from_static) {
                         ++snext;
                     } else if (lane == 0) {
@@ -257,15 +261,15 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             // before the PDL predecessor has finished; everything it writes (tile counter, y
             // accumulator, x, index lists) is touched only after griddepcontrol.wait below.
             for (int s = batch > stages ? stages : batch; s < batch; ++s) {  // the rest of the static tiles -> L2
-                const int r0 = (int)(sbase + s) * NR;
+                const int r0 = tile_r0((int)(sbase + s));
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Wg + (size_t)r0 * d),
-                             "r"((uint32_t)min(NR, m - r0) * row_bytes)
+                             "r"((uint32_t)tile_rows((int)(sbase + s), r0) * row_bytes)
                              : "memory");
             }
             for (int s = 0; s < min(batch, stages); ++s) {
                 const unsigned int tile = sbase + s;  // grid * batch <= ntiles
-                const int r0 = (int)tile * NR;
-                const int nr = min(NR, m - r0);
+                const int r0 = tile_r0((int)tile);
+                const int nr = tile_rows((int)tile, r0);
                 desc[s].type = kJobGate;
                 desc[s].tile = (int)tile;
                 desc[s].n = nr;
@@ -305,7 +309,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             if (desc[rs].type == kJobGate) {
                 // u (fixed-order sum over the 16 consumer warps) -> v = SiLU(u) (Eq. 2) ->
                 // keep = |v| >= t (Eq. 4, ties kept) -> ballot compaction of the tile
-                const int tile = desc[rs].tile, n = desc[rs].n, r0 = tile * NR;
+                const int tile = desc[rs].tile, n = desc[rs].n, r0 = tile_r0(tile);
                 const float *rb = red + (size_t)rs * NW * NPMAX;
                 uint32_t bits = 0;
                 float vrow[B];
@@ -665,7 +669,8 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
         reinterpret_cast<uint8_t *>(w + p.off_tokmask), reinterpret_cast<float *>(w + p.off_vals),
         reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<unsigned long long *>(w + p.off_ypart), y,
         reinterpret_cast<unsigned int *>(w + p.off_sched), reinterpret_cast<int32_t *>(w + p.off_gidx),
-        reinterpret_cast<float *>(w + p.off_gval), p.lazy_tail * k12_grid(p, B), p.k12_eager, p.k12_l2pf,
+        reinterpret_cast<float *>(w + p.off_gval), k12_t1(p, B), k12_tail_rows(p, B), p.lazy_tail * k12_grid(p, B),
+        p.k12_eager, p.k12_l2pf,
         p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
