@@ -131,14 +131,16 @@ typedef struct {
 #define CATS_CALIB_NONFINITE 3 /* NaN / Inf: nonzero iff any was seen (the bf16 pass flags once per
                                   thread instead of counting every value; ABOVE is exact only when 0) */
 #define CATS_CALIB_NCOUNTS 4
+#define CATS_CALIB_COUNTS_LEN 8 /* length of counts_dev: [0, 4) the counts above, [4, 8) scratch of a
+                                   pass (zero on entry; every pass leaves it zero again) */
 
 /* Initial window for n values: the whole finite key range, coarse bins; strided sampling when n
  * is large (the sample only steers the window; it never decides t). Host-only. */
 cats_status_t cats_calib_window_init(uint64_t n, cats_dtype_t dt, cats_calib_window_t *w);
 
 /* Device pass: hist_dev[0..w->nbins) += histogram of keys in the window, counts_dev[0..4) +=
- * the CATS_CALIB_* counts, over acts (or its sample). Caller zeroes both buffers first (or keeps
- * accumulating chunks / ranks). Asynchronous. Errors: CATS_E_NULL, CATS_E_DTYPE, CATS_E_ALIGN,
+ * the CATS_CALIB_* counts, over acts (or its sample). counts_dev holds CATS_CALIB_COUNTS_LEN
+ * uint64. Caller zeroes both buffers first (or keeps accumulating chunks / ranks). Asynchronous. Errors: CATS_E_NULL, CATS_E_DTYPE, CATS_E_ALIGN,
  * CATS_E_SHAPE (bad window), CATS_E_CUDA. */
 cats_status_t cats_calib_hist(const void *acts, uint64_t n, cats_dtype_t dt, const cats_calib_window_t *w,
                               uint64_t *hist_dev, uint64_t *counts_dev, cats_stream_t s);

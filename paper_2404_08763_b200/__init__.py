@@ -132,7 +132,10 @@ def cats_calib_window_init(n: int, dtype: torch.dtype) -> CalibWindow:
 
 def cats_calib_hist(acts: torch.Tensor, window: CalibWindow, hist_dev: torch.Tensor, counts_dev: torch.Tensor,
                     stream=None):
-    """hist_dev (uint64/int64 [>= nbins]) and counts_dev ([4]) are accumulated into (+=)."""
+    """hist_dev (uint64/int64 [>= nbins]) and counts_dev ([CATS_CALIB_COUNTS_LEN = 8]: 4 counts + pass
+    scratch) are accumulated into (+=)."""
+    if counts_dev.numel() < 8 or hist_dev.numel() < window.nbins:
+        raise ValueError("counts_dev needs 8 entries (CATS_CALIB_COUNTS_LEN), hist_dev window.nbins")
     rc = _lib.load().cats_calib_hist(_dev_ptr(acts, "acts"), acts.numel(), _dt(acts), ctypes.byref(window),
                                      _dev_ptr(hist_dev, "hist"), _dev_ptr(counts_dev, "counts"),
                                      _stream(stream, acts.device))

@@ -35,7 +35,7 @@ constexpr uint32_t kKeyMaxF32 = 0x7f7fffffu;    // largest finite |fp32| key
 constexpr uint32_t kFullPassBins = 4096;        // shared-memory bins of a full-data pass
 constexpr size_t kCalibHistOff = 0;
 constexpr size_t kCalibCountOff = (size_t)CATS_CALIB_MAX_BINS * 8;
-constexpr size_t kCalibWsBytes = kCalibCountOff + 64;
+constexpr size_t kCalibWsBytes = kCalibCountOff + CATS_CALIB_COUNTS_LEN * 8;
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -253,7 +253,7 @@ extern "C" cats_status_t cats_calibrate_threshold(const void *acts, uint64_t n, 
         int done = 0;
         for (int it = 0; it < 32 && !done; ++it) {
             cudaError_t e = cudaMemsetAsync(hist, 0, (size_t)w.nbins * 8, st);
-            if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, CATS_CALIB_NCOUNTS * 8, st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, CATS_CALIB_COUNTS_LEN * 8, st);
             if (e == cudaSuccess) e = launch_calib_hist(acts, n, dt, w, hist, cnt, st);
             if (e == cudaSuccess) e = cudaMemcpyAsync(h_hist.data(), hist, (size_t)w.nbins * 8, cudaMemcpyDeviceToHost, st);
             if (e == cudaSuccess) e = cudaMemcpyAsync(h_cnt, cnt, sizeof h_cnt, cudaMemcpyDeviceToHost, st);

@@ -159,6 +159,182 @@ calib_hist_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint32_t 
     if (threadIdx.x < 4 && scount[threadIdx.x]) atomicAdd(&counts[threadIdx.x], scount[threadIdx.x]);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Full-pass kernel: the data streams through a shared-memory ring fed by the TMA bulk-copy engine
+// (cp.async.bulk + mbarrier), so the HBM stream never waits for the key arithmetic and the
+// arithmetic never waits for HBM (the register-load loop above keeps 8 loads per thread in flight
+// only between its compute phases). One producer warp claims 32 KB chunks from a global counter
+// (dynamic: SMs with more bandwidth take more chunks) and keeps kCalStages of them in flight;
+// 16 consumer warps classify the keys from shared memory. Bytes beyond the last whole chunk (and a
+// sub-16-byte tail) are classified by CTA 0 straight from global memory.
+constexpr int kCalStageBytes = 32 * 1024;
+constexpr int kCalMaxStages = 6;
+constexpr int kCalConsumerWarps = 16;
+constexpr int kCalTmaThreads = (kCalConsumerWarps + 1) * 32;
+
+template <typename K>
+__global__ void __launch_bounds__(kCalTmaThreads, 1)
+calib_hist_tma_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint32_t hi, uint32_t shift,
+                      uint32_t nbins, int kCalStages, unsigned long long *__restrict__ hist,
+                      unsigned long long *__restrict__ counts) {
+    using KT = KeyTraits<K>;
+    constexpr int E = KT::kPerVec;
+    constexpr int NC = kCalConsumerWarps * 32;
+    constexpr int VPT = kCalStageBytes / 16 / NC;  // 16-byte vectors per consumer thread per stage
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char *ring = smem;
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)kCalStages * kCalStageBytes);
+    uint64_t *empty = full + kCalStages;
+    int *chunk_of = reinterpret_cast<int *>(empty + kCalStages);  // [kCalStages] chunk id per stage (-1 = end)
+    uint32_t *sh = reinterpret_cast<uint32_t *>(chunk_of + kCalStages);  // [nbins]
+    __shared__ unsigned long long scount[4];
+    __shared__ unsigned int s_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint32_t i = tid; i < nbins; i += blockDim.x) sh[i] = 0u;
+    if (tid < 4) scount[tid] = 0ull;
+    if (tid == 0) {
+        for (int s = 0; s < kCalStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kCalConsumerWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint64_t nbytes = n * sizeof(K);
+    const uint64_t nchunks = nbytes / kCalStageBytes;
+    unsigned int *ctr = reinterpret_cast<unsigned int *>(counts + 4);  // [0] chunk counter, [2] exit tickets
+
+    uint32_t below = 0, nonfin = 0, inwin = 0, seen = 0;
+    if (warp == kCalConsumerWarps) {
+        // ---------------- producer: claim chunks, keep kCalStages bulk copies in flight ----------------
+        if (lane == 0) {
+            const uint64_t policy = l2_evict_first_policy();
+            for (int j = 0;; ++j) {
+                const int s = j % kCalStages;
+                if (j >= kCalStages) mbar_wait(&empty[s], (uint32_t)((j / kCalStages) - 1) & 1u);
+                const unsigned int c = atomicAdd(ctr, 1u);
+                if ((uint64_t)c >= nchunks) {
+                    chunk_of[s] = -1;
+                    mbar_arrive_expect_tx(&full[s], 0u);  // END
+                    break;
+                }
+                chunk_of[s] = (int)c;
+                mbar_arrive_expect_tx(&full[s], (uint32_t)kCalStageBytes);
+                bulk_g2s(ring + (size_t)s * kCalStageBytes, reinterpret_cast<const unsigned char *>(acts) +
+                         (size_t)c * kCalStageBytes, (uint32_t)kCalStageBytes, &full[s], policy);
+            }
+        }
+    } else {
+        // ---------------- consumers ----------------
+        uint32_t cur_bin = 0xffffffffu, cur_cnt = 0;
+        const uint32_t span = hi - lo;
+        auto classify_in = [&](uint32_t key) {
+            ++inwin;
+            const uint32_t bin = (key - lo) >> shift;
+            if (bin == cur_bin) {
+                ++cur_cnt;
+            } else {
+                if (cur_cnt) atomicAdd(&sh[cur_bin], cur_cnt);
+                cur_bin = bin;
+                cur_cnt = 1;
+            }
+        };
+        auto classify = [&](uint32_t key) {
+            below += key < lo ? 1u : 0u;
+            nonfin += key >= KT::kInf ? 1u : 0u;
+            if (key - lo <= span) classify_in(key);
+        };
+        uint32_t nge2 = 0, kmax2 = 0, seen_main = 0;
+        const uint32_t lo2 = lo * 0x10001u;
+        const uint32_t hi2x = (min(hi, KT::kMask) * 0x10001u) | 0x80008000u;
+        for (int j = 0;; ++j) {
+            const int s = j % kCalStages;
+            mbar_wait(&full[s], (uint32_t)(j / kCalStages) & 1u);
+            if (chunk_of[s] < 0) break;
+            const uint32_t sb = smem_u32(ring + (size_t)s * kCalStageBytes);
+            uint4 r[VPT];
+#pragma unroll
+            for (int u = 0; u < VPT; ++u) r[u] = lds128(sb + (uint32_t)((u * NC + tid) * 16));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // the stage is in registers: let the producer refill it
+            if constexpr (sizeof(K) == 2) {
+                // two keys per 32-bit word, SIMD within the register (see calib_hist_kernel)
+                uint32_t hit = 0;  // words with an in-window key, handled after the SIMD sweep
+#pragma unroll
+                for (int u = 0; u < VPT; ++u) {
+                    const uint32_t wv[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t gl = ((wv[q] | 0x80008000u) - lo2) & 0x80008000u;
+                        nge2 += __popc(gl);
+                        const uint32_t k2 = wv[q] & 0x7fff7fffu;
+                        kmax2 = __vmaxu2(kmax2, k2);
+                        hit |= ((hi2x - k2) & gl) ? (1u << (u * 4 + q)) : 0u;
+                    }
+                }
+                while (hit) {  // rare: keys inside the (sample-aimed) window
+                    const int wq = __ffs(hit) - 1;
+                    hit &= hit - 1;
+                    uint32_t w = 0;
+#pragma unroll
+                    for (int u = 0; u < VPT; ++u) {
+                        if ((wq >> 2) == u) {
+                            const int q = wq & 3;
+                            w = q == 0 ? r[u].x : q == 1 ? r[u].y : q == 2 ? r[u].z : r[u].w;
+                        }
+                    }
+                    const uint32_t gl = ((w | 0x80008000u) - lo2) & 0x80008000u;
+                    const uint32_t k2 = w & 0x7fff7fffu;
+                    const uint32_t iw = (hi2x - k2) & gl;
+                    if (iw & 0x8000u) classify_in(k2 & 0xffffu);
+                    if (iw & 0x80000000u) classify_in(k2 >> 16);
+                }
+                seen_main += VPT * E;
+            } else {
+#pragma unroll
+                for (int u = 0; u < VPT; ++u)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) classify(KT::key(r[u], e));
+                seen += VPT * E;
+            }
+        }
+        if constexpr (sizeof(K) == 2) {
+            below += seen_main - nge2;
+            nonfin += ((kmax2 & 0xffffu) >= KT::kInf || (kmax2 >> 16) >= KT::kInf) ? 1u : 0u;
+            seen += seen_main;
+        }
+        // bytes past the last whole chunk: CTA 0's consumers, from global memory
+        if (blockIdx.x == 0) {
+            const uint64_t e0 = nchunks * (kCalStageBytes / sizeof(K));
+            for (uint64_t i = e0 + tid; i < n; i += NC) {
+                classify((uint32_t)acts[i] & KT::kMask);
+                ++seen;
+            }
+        }
+        if (cur_cnt) atomicAdd(&sh[cur_bin], cur_cnt);
+    }
+    const uint32_t above = seen - below - inwin - nonfin;
+    const unsigned long long c4[4] = {below, inwin, above, nonfin};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        unsigned long long v = c4[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && v) atomicAdd(&scount[q], v);
+    }
+    __syncthreads();
+    for (uint32_t b = tid; b < nbins; b += blockDim.x)
+        if (sh[b]) atomicAdd(&hist[b], (unsigned long long)sh[b]);
+    if (tid < 4 && scount[tid]) atomicAdd(&counts[tid], scount[tid]);
+    // the last CTA re-arms the pass scratch (chunk counter, tickets) for the next pass
+    if (tid == 0) s_last = atomicAdd(ctr + 4, 1u) == gridDim.x - 1 ? 1u : 0u;
+    __syncthreads();
+    if (s_last && tid == 0) {
+        ctr[0] = 0u;
+        ctr[4] = 0u;
+    }
+}
+
 cudaError_t launch_calib_hist(const void *acts, uint64_t n, cats_dtype_t dt, const cats_calib_window_t &w,
                               uint64_t *hist, uint64_t *counts, cudaStream_t s) {
     int dev = 0, nsm = 148;
@@ -174,6 +350,25 @@ cudaError_t launch_calib_hist(const void *acts, uint64_t n, cats_dtype_t dt, con
     const int grid = (int)std::min<uint64_t>(want, (uint64_t)nsm * blocks_per_sm);
     auto *h = reinterpret_cast<unsigned long long *>(hist);
     auto *c = reinterpret_cast<unsigned long long *>(counts);
+    const int tstages = (int)std::min<size_t>(kCalMaxStages, (220 * 1024 - (size_t)w.nbins * 4) / (kCalStageBytes + 20));
+    if (!w.sample_stride && tstages >= 2 && (uint64_t)n * (dt == CATS_BF16 ? 2 : 4) >= (uint64_t)kCalStageBytes * nsm) {
+        // full pass over a large buffer: the TMA-ring kernel, one CTA per SM
+        const size_t tsmem = (size_t)tstages * (kCalStageBytes + 16 + 4) + (size_t)w.nbins * 4;
+        if (dt == CATS_BF16) {
+            auto kern = calib_hist_tma_kernel<uint16_t>;
+            cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), tsmem);
+            if (e != cudaSuccess) return e;
+            kern<<<nsm, kCalTmaThreads, tsmem, s>>>(static_cast<const uint16_t *>(acts), n, w.lo, w.hi, w.shift,
+                                                     w.nbins, tstages, h, c);
+        } else {
+            auto kern = calib_hist_tma_kernel<uint32_t>;
+            cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), tsmem);
+            if (e != cudaSuccess) return e;
+            kern<<<nsm, kCalTmaThreads, tsmem, s>>>(static_cast<const uint32_t *>(acts), n, w.lo, w.hi, w.shift,
+                                                     w.nbins, tstages, h, c);
+        }
+        return cudaGetLastError();
+    }
     if (dt == CATS_BF16) {
         auto kern = calib_hist_kernel<uint16_t>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -49,7 +49,7 @@ def calibrate_threshold(acts: torch.Tensor, k: float, group=None, hist_fn=None, 
     w = cats_calib_window_init(n, acts.dtype)
     dev = acts.device if hist_fn is None else torch.device("cpu")
     hist = torch.zeros(32768, dtype=torch.int64, device=dev)
-    counts = torch.zeros(4, dtype=torch.int64, device=dev)
+    counts = torch.zeros(8, dtype=torch.int64, device=dev)  # CATS_CALIB_COUNTS_LEN (4 counts + pass scratch)
     for _ in range(max_steps):
         hist.zero_()
         counts.zero_()
@@ -58,12 +58,12 @@ def calibrate_threshold(acts: torch.Tensor, k: float, group=None, hist_fn=None, 
         else:
             h, c = hist_fn(acts, w)
             hist[: w.nbins] += torch.from_numpy(h.astype(np.int64))
-            counts += torch.from_numpy(c.astype(np.int64))
+            counts[:4] += torch.from_numpy(c.astype(np.int64))
         if group is not None:
             dist.all_reduce(hist, group=group)
             dist.all_reduce(counts, group=group)
         done, tb, _, _ = cats_calib_step(hist[: w.nbins].cpu().numpy().view(np.uint64),
-                                         counts.cpu().numpy().view(np.uint64), n, acts.dtype, k, w)
+                                         counts[:4].cpu().numpy().view(np.uint64), n, acts.dtype, k, w)
         if done:
             return _bits_to_float(tb, acts.dtype)
     raise RuntimeError("sharded calibration did not converge")

@@ -70,6 +70,21 @@ for _ in range(3):
     e1.record()
     torch.cuda.synchronize()
     best.append(1e3 * e0.elapsed_time(e1) / (a.reps * copies))
+# isolated launches: one call bracketed by events, nothing overlapping it
+iso = []
+for i in range(60):
+    W = Ws[i % copies]
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    torch.cuda.synchronize()
+    e0.record()
+    if a.dense:
+        cats.cats_mlp_dense(plan, x, *W, y=y, ws=ws)
+    else:
+        cats.cats_mlp_decode(plan, x, *W, t, y=y, ws=ws)
+    e1.record()
+    torch.cuda.synchronize()
+    if i >= 10:
+        iso.append(1e3 * e0.elapsed_time(e1))
 cats.cats_mlp_decode(plan, x, *W0, t, y=y, ws=ws)
 idx, tm, per = cats.cats_mlp_last_active(plan, ws, a.batch)
 U = len(idx)
@@ -77,5 +92,6 @@ eff = 2 * (d * m + 2 * d * U) if not a.dense else 2 * 3 * d * m
 us = min(best)
 print(json.dumps(dict(tag=a.tag, model=a.model, d=d, m=m, b=a.batch, k=a.k, dense=a.dense, copies=copies,
                       us=round(us, 3), us_runs=[round(v, 3) for v in best], union=U,
+                      iso_us=round(sum(iso) / len(iso), 3),
                       eff_GBps=round(eff / (us * 1e-6) / 1e9, 1), grid=plan.info["grid"],
                       opts=opts)), flush=True)

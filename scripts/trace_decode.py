@@ -22,14 +22,16 @@ ap.add_argument("--k", type=float, default=0.5)
 ap.add_argument("--dense", action="store_true")
 ap.add_argument("--json")
 ap.add_argument("--m", type=int, default=0, help="override m (e.g. a TP shard)")
+ap.add_argument("--opt", action="append", default=[], help="plan option key=value, repeatable")
 a = ap.parse_args()
+opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt}
 d, m = cats_synth.MODELS[a.model]
 if a.m:
     m = a.m
 dev = torch.device("cuda:0")
 W = [w.to(dev) for w in cats_synth.mlp_weights(d, m, torch.bfloat16)]
 copies = [W] + [[w.clone() for w in W] for _ in range(3)]
-plan = cats.MlpPlan(d, m, max_batch=8, trace=1)
+plan = cats.MlpPlan(d, m, max_batch=8, trace=1, **opts)
 ws = plan.workspace()
 off, nbytes = ctypes.c_size_t(), ctypes.c_size_t()
 plan._lib.cats_mlp_trace_info(plan.handle, ctypes.byref(off), ctypes.byref(nbytes))
