@@ -187,7 +187,8 @@ cats_status_t cats_mlp_plan_create(int d, int m, int max_batch, cats_dtype_t w_d
  * explicit field here, fixed at plan creation. cats_mlp_plan_create(...) == _ex(..., NULL). */
 typedef enum {
     CATS_PATH_AUTO = 0,   /* K12 at b = 1; KA + KB at b >= 2 where their shared memory fits */
-    CATS_PATH_FUSED = 1   /* K12 (the single fused kernel) at every batch size */
+    CATS_PATH_FUSED = 1,  /* K12 (the single fused kernel) at every batch size */
+    CATS_PATH_SPLIT = 2   /* KA + KB wherever they fit, b = 1 included (small tensor-parallel shards) */
 } cats_path_t;
 
 /* How the active set reaches the sparse up / down projection (App. D; the ablation
@@ -330,6 +331,36 @@ cats_status_t cats_xsparse_plan_create_ex(int d_in, int d_out, int max_batch, ca
  *         CATS_E_THRESHOLD (t < 0, NaN or Inf), CATS_E_CUDA. */
 cats_status_t cats_xsparse_gemv(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_in_major,
                                 float t, float *y, void *ws, size_t ws_bytes, cats_stream_t s);
+
+/* ---- Tensor parallelism: one-shot cross-rank reduction over NVLink peer memory ------
+ * Each of the P ranks (one process per GPU) holds its m / P neuron block; its cats_mlp_decode returns a
+ * partial y_p and y = sum_p y_p (the exchange step; masking needs none: t is layer-global, Eq. 5 is per
+ * neuron). Instead of an NCCL all-reduce, every rank allocates one SYMMETRIC buffer of
+ * cats_tp_buffer_bytes (device memory, zero-initialised once), exports it with cats_ipc_handle_get, opens
+ * every peer's with cats_ipc_handle_open (CUDA IPC over NVLink / NVSwitch) and builds a comm; then
+ * cats_tp_allreduce is ONE launch that pushes this rank's partial into every rank's buffer, flags it, waits
+ * for every rank's flags and sums the P partials in fixed rank order 0..P-1: bit-identical y on every rank.
+ * Epochs live on the device (graph-capturable); two parity slots make back-to-back calls safe.
+ * Requirements: P <= 8; n (floats per call) a multiple of 4 and <= n_max; every rank calls with the same
+ * n in the same order; buffers 16-byte aligned. Errors: CATS_E_NULL, CATS_E_SHAPE, CATS_E_ALIGN, CATS_E_CUDA. */
+#define CATS_IPC_HANDLE_BYTES 64
+typedef struct cats_tp_comm cats_tp_comm_t;
+cats_status_t cats_tp_buffer_bytes(int world, uint64_t n_max, size_t *bytes);
+cats_status_t cats_ipc_handle_get(const void *dev_ptr, uint8_t *handle_out /* [CATS_IPC_HANDLE_BYTES] */);
+cats_status_t cats_ipc_handle_open(const uint8_t *handle, int device, void **dev_ptr_out);
+cats_status_t cats_ipc_handle_close(void *dev_ptr);
+/* bufs[r] = rank r's symmetric buffer as mapped in this process (bufs[rank] = the local allocation). Host-only. */
+cats_status_t cats_tp_comm_create(int rank, int world, uint64_t n_max, void *const *bufs, int device,
+                                  cats_tp_comm_t **out);
+void cats_tp_comm_destroy(cats_tp_comm_t *comm);
+/* y[n] = sum over ranks (order 0..P-1) of every rank's x[n] (fp32, device). Asynchronous on s (programmatic
+ * dependent launch: it may start while the decode that writes x drains). x and y may alias. */
+cats_status_t cats_tp_allreduce(const cats_tp_comm_t *comm, const float *x, float *y, uint64_t n, cats_stream_t s);
+/* The same step for `world` ranks emulated on ONE device (testing without P GPUs): comms[r] built with
+ * rank r over buffers on this device, x[r] / y[r] the ranks' partials / outputs; one cooperative launch runs
+ * every rank's CTAs (they wait on one another's flags, so they must be co-resident). */
+cats_status_t cats_tp_allreduce_emulated(cats_tp_comm_t *const *comms, int world, const float *const *x,
+                                         float *const *y, uint64_t n, cats_stream_t s);
 
 /* Diagnostics. When the plan was created with options.trace = 1, the kernels
  * record %globaltimer stamps (ns) per CTA into a trace area of the workspace:

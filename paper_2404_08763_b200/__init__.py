@@ -14,14 +14,14 @@ import torch
 
 from . import _lib
 from ._lib import (CATS_BF16, CATS_COMPACT_ATOMIC, CATS_COMPACT_BALLOT, CATS_COMPACT_PREDICATED, CATS_F32,
-                   CATS_PATH_AUTO, CATS_PATH_FUSED, CalibInfo, CalibWindow, PlanInfo, PlanOptions)
+                   CATS_PATH_AUTO, CATS_PATH_FUSED, CATS_PATH_SPLIT, CalibInfo, CalibWindow, PlanInfo, PlanOptions)
 
 __all__ = [
     "CatsError", "MlpPlan", "cats_calib_rank", "cats_calibrate_workspace_bytes", "cats_calibrate_threshold",
     "cats_calib_window_init", "cats_calib_hist", "cats_calib_step", "cats_mlp_decode", "cats_mlp_dense",
     "cats_mlp_decode_profiled",
     "cats_mlp_decode_host", "cats_mlp_gate_act", "cats_mlp_last_active", "cats_mlp_kernels_per_call", "library_path",
-    "XsparsePlan", "cats_xsparse_gemv", "plan_options", "CATS_PATH_AUTO", "CATS_PATH_FUSED", "CATS_COMPACT_BALLOT",
+    "XsparsePlan", "cats_xsparse_gemv", "plan_options", "CATS_PATH_AUTO", "CATS_PATH_FUSED", "CATS_PATH_SPLIT", "CATS_COMPACT_BALLOT",
     "CATS_COMPACT_PREDICATED", "CATS_COMPACT_ATOMIC",
 ]
 

@@ -36,7 +36,7 @@ class PlanOptions(ctypes.Structure):
                 ("xs_mma", ctypes.c_int32), ("xs_no_shrink", ctypes.c_int32)]
 
 
-CATS_PATH_AUTO, CATS_PATH_FUSED = 0, 1
+CATS_PATH_AUTO, CATS_PATH_FUSED, CATS_PATH_SPLIT = 0, 1, 2
 CATS_COMPACT_BALLOT, CATS_COMPACT_PREDICATED, CATS_COMPACT_ATOMIC = 0, 1, 2
 
 
@@ -80,6 +80,14 @@ _SIGS = {
     "cats_mlp_kernels_per_call": (I, [P, I, P]),
     "cats_xsparse_plan_create": (I, [I, I, I, I, I, I, P]),
     "cats_xsparse_gemv": (I, [P, P, I, P, F, P, P, SZ, P]),
+    "cats_tp_buffer_bytes": (I, [I, U64, P]),
+    "cats_ipc_handle_get": (I, [P, P]),
+    "cats_ipc_handle_open": (I, [P, I, P]),
+    "cats_ipc_handle_close": (I, [P]),
+    "cats_tp_comm_create": (I, [I, I, U64, P, I, P]),
+    "cats_tp_comm_destroy": (None, [P]),
+    "cats_tp_allreduce": (I, [P, P, P, U64, P]),
+    "cats_tp_allreduce_emulated": (I, [P, I, P, P, U64, P]),
 }
 
 

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libcats.so")
-SOURCES = ["api.cu", "mlp_fused.cu", "mlp_split.cu", "xsparse.cu", "calib.cu"]
+SOURCES = ["api.cu", "mlp_fused.cu", "mlp_split.cu", "xsparse.cu", "calib.cu", "tp_comm.cu"]
 HEADERS = ["cats_device.cuh", "cats_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

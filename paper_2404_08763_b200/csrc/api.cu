@@ -313,7 +313,7 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         if (opt_in->size != sizeof(cats_mlp_plan_options_t)) return CATS_E_SHAPE;
         o = *opt_in;
     }
-    if (o.path != CATS_PATH_AUTO && o.path != CATS_PATH_FUSED) return CATS_E_UNSUPPORTED;
+    if (o.path < CATS_PATH_AUTO || o.path > CATS_PATH_SPLIT) return CATS_E_UNSUPPORTED;
     if (o.compaction < CATS_COMPACT_BALLOT || o.compaction > CATS_COMPACT_ATOMIC) return CATS_E_UNSUPPORTED;
     if (o.lazy_tail < 0 || o.min_tiles < 1 || o.l2_prefetch < 0 || o.max_stages < 0 || o.max_stages == 1 ||
         (o.rows_per_tile != 0 && o.rows_per_tile != 2 && o.rows_per_tile != 4 && o.rows_per_tile != 6) ||
@@ -429,9 +429,10 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.off_ystage = off;  off = align_up(off + (size_t)max_batch * d * 4, 256);
         // split path (b >= 2): x1 per compact position and the KB range partials
         // non-default compaction modes (the App. D ablation) run K12-based kernels at every batch size
-        p.split_min_b = (o.path == CATS_PATH_FUSED || p.compaction != CATS_COMPACT_BALLOT) ? CATS_MAX_BATCH + 1 : 2;
+        p.split_min_b = (o.path == CATS_PATH_FUSED || p.compaction != CATS_COMPACT_BALLOT) ? CATS_MAX_BATCH + 1
+                        : o.path == CATS_PATH_SPLIT ? 1 : 2;
         size_t part_bytes = 0, x1_bytes = 0;
-        for (int b = 2; b <= max_batch; ++b) {
+        for (int b = p.split_min_b; b <= max_batch; ++b) {
             if (!split_supported(p, b)) continue;
             part_bytes = std::max(part_bytes, (size_t)split_ranges(p, b) * b * d * 4);
             x1_bytes = std::max(x1_bytes, (size_t)k12_ntiles(p, b) * k12_rows_per_tile(p, b) * b * 4);

@@ -169,6 +169,7 @@ calib_hist_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint32_t 
 // sub-16-byte tail) are classified by CTA 0 straight from global memory.
 constexpr int kCalStageBytes = 32 * 1024;
 constexpr int kCalMaxStages = 6;
+constexpr int kCalClaim = 4;  // chunks per claim
 constexpr int kCalConsumerWarps = 16;
 constexpr int kCalTmaThreads = (kCalConsumerWarps + 1) * 32;
 
@@ -208,11 +209,21 @@ calib_hist_tma_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint3
     if (warp == kCalConsumerWarps) {
         // ---------------- producer: claim chunks, keep kCalStages bulk copies in flight ----------------
         if (lane == 0) {
+            // chunks are claimed kCalClaim at a time, the next group's atomic in flight while the current
+            // group streams (a blocking claim per chunk would put an L2 atomic round trip on every 32 KB)
             const uint64_t policy = l2_evict_first_policy();
+            unsigned int grp = atomicAdd(ctr, (unsigned)kCalClaim);
+            unsigned int nxt = atomicAdd(ctr, (unsigned)kCalClaim);
+            int in_grp = 0;
             for (int j = 0;; ++j) {
                 const int s = j % kCalStages;
                 if (j >= kCalStages) mbar_wait(&empty[s], (uint32_t)((j / kCalStages) - 1) & 1u);
-                const unsigned int c = atomicAdd(ctr, 1u);
+                if (in_grp == kCalClaim) {
+                    grp = nxt;
+                    in_grp = 0;
+                    nxt = atomicAdd(ctr, (unsigned)kCalClaim);
+                }
+                const unsigned int c = grp + (unsigned)in_grp++;
                 if ((uint64_t)c >= nchunks) {
                     chunk_of[s] = -1;
                     mbar_arrive_expect_tx(&full[s], 0u);  // END

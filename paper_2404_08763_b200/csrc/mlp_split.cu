@@ -869,7 +869,7 @@ bool kb_supported(const PlanData &p, int b) {  // KB alone fits this shape and b
 bool split_supported(const PlanData &p, int b) {
     // KB's phase 2 holds up to kKbReducers CTAs (one per SM) waiting for the rest: more SMs than that
     if (p.num_sms <= kKbReducers) return false;
-    if (b < 2 || b > 8 || !kb_supported(p, b)) return false;
+    if (b < 1 || b > 8 || !kb_supported(p, b)) return false;
     const int sa = split_ka_stages(p, b);
     return sa >= 2 && split_ka_smem(p, b, sa) <= kSmemBudget;  // >= 2 stages per group
 }
@@ -954,8 +954,13 @@ static cudaError_t launch_split_b(const PlanData &p, const void *x, const void *
         e = k12_rows_per_tile(p, B) == 4 ? launch_ka<T, B, 4, 1>(p, x, Wg, Wu, t, mode, ws, s)
                                          : launch_ka<T, B, 2, 1>(p, x, Wg, Wu, t, mode, ws, s);
     } else {
-        e = k12_rows_per_tile(p, B) == 4 ? launch_ka<T, B, 4, 0>(p, x, Wg, Wu, t, mode, ws, s)
-                                         : launch_ka<T, B, 2, 0>(p, x, Wg, Wu, t, mode, ws, s);
+        const int nr = k12_rows_per_tile(p, B);
+        if constexpr (B == 1) {  // b = 1 on large layers tiles by 6 rows (the split path at b = 1: options)
+            if (nr == 6) e = launch_ka<T, B, 6, 0>(p, x, Wg, Wu, t, mode, ws, s);
+        }
+        if (nr != 6) e = nr == 4 ? launch_ka<T, B, 4, 0>(p, x, Wg, Wu, t, mode, ws, s)
+                                 : launch_ka<T, B, 2, 0>(p, x, Wg, Wu, t, mode, ws, s);
+        else if (B != 1) e = cudaErrorInvalidValue;
     }
     if (e != cudaSuccess) return e;
     if (ev_mid) {
@@ -970,6 +975,7 @@ static cudaError_t launch_split_dt(const PlanData &p, const void *x, int b, cons
                                    const void *Wd, float t, int mode, float *y, void *ws, cudaStream_t s,
                                    cudaEvent_t ev) {
     switch (b) {
+        case 1: return launch_split_b<T, 1>(p, x, Wg, Wu, Wd, t, mode, y, ws, s, ev);
         case 2: return launch_split_b<T, 2>(p, x, Wg, Wu, Wd, t, mode, y, ws, s, ev);
         case 3: return launch_split_b<T, 3>(p, x, Wg, Wu, Wd, t, mode, y, ws, s, ev);
         case 4: return launch_split_b<T, 4>(p, x, Wg, Wu, Wd, t, mode, y, ws, s, ev);

@@ -1,0 +1,239 @@
+// tp_comm.cu -- one-shot cross-rank reduction of the tensor-parallel partials over NVLink peer memory
+// (DESIGN.md §7).
+//
+// Tensor parallelism splits the intermediate dimension m into P contiguous neuron blocks; every rank's
+// decode yields a partial y_p (b x d fp32) and y = sum_p y_p is the layer output (the one exchange step
+// of the path; the threshold t is layer-global, so the masks need no communication -- Eq. 5 is per
+// neuron). The paper measures one GPU and motivates removing synchronisation overhead
+// (App. D); this is the B200 design of that exchange:
+//
+//   * every rank owns a symmetric buffer (same layout on all ranks, mapped into every peer's address
+//     space with CUDA IPC over NVLink): a header of per-CTA epoch counters and flags[src][cta], then two
+//     parity slots of world x n floats;
+//   * ONE launch per call: CTA c takes slice c of the n values, pushes this rank's slice into slot
+//     [epoch & 1][rank] of EVERY rank's buffer (16-byte stores over NVLink, self included), publishes
+//     flags[rank][c] = epoch in every peer (st.release.sys after a system-scope fence), waits until
+//     all world flags of its slice carry the epoch, and sums the slots in fixed rank order 0..P-1 --
+//     the same additions in the same order on every rank, so y is bit-identical across ranks;
+//   * epochs are per CTA and live on the device (CUDA-graph safe); two parity slots make a call's pushes
+//     land in the slot no rank can still be reading (a rank pushes call e+1 only after its call e saw
+//     every rank's call-e data, i.e. after every rank finished call e-1).
+//
+// On one device (this pool) the P ranks are emulated as ONE cooperative launch over all ranks' data
+// (blocks of virtual rank r = blockIdx.x / C), so the flag waits are between co-resident CTAs.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+
+#include "cats_device.cuh"
+#include "cats_internal.h"
+
+namespace cats {
+
+constexpr int kTpMaxWorld = 8;
+constexpr int kTpThreads = 256;
+constexpr int kTpMaxCtas = 64;
+constexpr size_t kTpHeaderBytes = (size_t)(1 + kTpMaxWorld) * kTpMaxCtas * 4;  // ep[C] + flags[W][C], u32
+
+struct TpLaunch {
+    int world, ctas, nlocal, rank0;       // nlocal ranks handled by this launch: rank0 .. rank0 + nlocal - 1
+    unsigned long long n, slot_floats;    // values per call, floats per (parity, rank) slot
+    unsigned char *bufs[kTpMaxWorld][kTpMaxWorld];  // [local rank][peer]: peer's symmetric buffer as mapped here
+    const float *x[kTpMaxWorld];          // [local rank] partial
+    float *y[kTpMaxWorld];                // [local rank] output
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned int *p, unsigned int v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kTpThreads) tp_allreduce_kernel(const __grid_constant__ TpLaunch L) {
+    const int lr = blockIdx.x / L.ctas, c = blockIdx.x % L.ctas;  // local rank, slice
+    const int me = L.rank0 + lr, W = L.world;
+    unsigned char *const *bufs = L.bufs[lr];
+    unsigned int *own_hdr = reinterpret_cast<unsigned int *>(bufs[me]);
+    // slice of this CTA (16-byte aligned boundaries: n is a multiple of 4)
+    const unsigned long long n4 = L.n / 4;
+    const unsigned long long s0 = n4 * c / L.ctas, s1 = n4 * (c + 1) / L.ctas;
+    __shared__ unsigned int s_ep;
+    pdl_launch_dependents();  // the next layer's decode may start streaming its static W_gate tiles
+    pdl_wait_primary();       // x (and this CTA's epoch word) may come from the kernels launched before us
+    if (threadIdx.x == 0) s_ep = own_hdr[c] + 1u;  // this CTA's epoch (only CTA c of this rank writes ep[c])
+    __syncthreads();
+    const unsigned int ep = s_ep;
+    const size_t slot_off = kTpHeaderBytes + (size_t)(ep & 1u) * W * L.slot_floats * 4;
+    // push: this rank's slice into slot [ep & 1][me] of every rank (NVLink stores; self is local)
+    const float4 *x4 = reinterpret_cast<const float4 *>(L.x[lr]);
+    for (int r = 0; r < W; ++r) {
+        float4 *dst = reinterpret_cast<float4 *>(bufs[r] + slot_off + (size_t)me * L.slot_floats * 4);
+        for (unsigned long long i = s0 + threadIdx.x; i < s1; i += blockDim.x) dst[i] = __ldcg(x4 + i);
+    }
+    __syncthreads();
+    if (threadIdx.x < W) {
+        __threadfence_system();  // the slice stores (every thread's, ordered by the barrier) before the flag
+        unsigned int *hdr = reinterpret_cast<unsigned int *>(bufs[threadIdx.x]);
+        st_release_sys(hdr + (size_t)(1 + me) * kTpMaxCtas + c, ep);
+    }
+    // wait for every rank's slice c of this epoch
+    if (threadIdx.x < W) {
+        const unsigned int *f = own_hdr + (size_t)(1 + threadIdx.x) * kTpMaxCtas + c;
+        while ((int)(ld_acquire_sys(f) - ep) < 0) {
+        }
+    }
+    __syncthreads();
+    // y = sum over ranks in fixed order 0..W-1 (identical on every rank)
+    const float4 *slots = reinterpret_cast<const float4 *>(bufs[me] + slot_off);
+    float4 *y4 = reinterpret_cast<float4 *>(L.y[lr]);
+    const unsigned long long stride4 = L.slot_floats / 4;
+    for (unsigned long long i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+        float4 a = __ldcv(slots + i);
+        for (int r = 1; r < W; ++r) {
+            const float4 v = __ldcv(slots + (size_t)r * stride4 + i);
+            a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+        }
+        y4[i] = a;
+    }
+    if (threadIdx.x == 0) own_hdr[c] = ep;
+}
+
+}  // namespace cats
+
+using namespace cats;
+
+struct cats_tp_comm {
+    int rank, world, device, ctas;
+    uint64_t n_max;
+    unsigned char *bufs[kTpMaxWorld];  // every rank's symmetric buffer as mapped in this process
+};
+
+namespace {
+inline cats_status_t cuda_status_tp(cudaError_t e) {
+    if (e == cudaSuccess) return CATS_OK;
+    set_last_cuda_error(e);
+    return CATS_E_CUDA;
+}
+size_t tp_buffer_bytes(int world, uint64_t n) { return kTpHeaderBytes + 2 * (size_t)world * ((n + 3) / 4 * 4) * 4; }
+int tp_ctas(uint64_t n) {  // ~1 KB of the call's values per CTA and slice, at most kTpMaxCtas
+    const uint64_t c = (n + 255) / 256;
+    return (int)(c < 1 ? 1 : c > (uint64_t)kTpMaxCtas ? kTpMaxCtas : c);
+}
+}  // namespace
+
+extern "C" cats_status_t cats_tp_buffer_bytes(int world, uint64_t n_max, size_t *bytes) {
+    if (!bytes) return CATS_E_NULL;
+    if (world < 1 || world > kTpMaxWorld || n_max == 0 || n_max % 4) return CATS_E_SHAPE;
+    *bytes = tp_buffer_bytes(world, n_max);
+    return CATS_OK;
+}
+
+extern "C" cats_status_t cats_ipc_handle_get(const void *dev_ptr, uint8_t *handle_out) {
+    if (!dev_ptr || !handle_out) return CATS_E_NULL;
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(dev_ptr));
+    if (e != cudaSuccess) return cuda_status_tp(e);
+    static_assert(sizeof(h) == CATS_IPC_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+    std::memcpy(handle_out, &h, sizeof h);
+    return CATS_OK;
+}
+
+extern "C" cats_status_t cats_ipc_handle_open(const uint8_t *handle, int device, void **dev_ptr_out) {
+    if (!handle || !dev_ptr_out) return CATS_E_NULL;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+    return cuda_status_tp(e);
+}
+
+extern "C" cats_status_t cats_ipc_handle_close(void *dev_ptr) {
+    if (!dev_ptr) return CATS_E_NULL;
+    return cuda_status_tp(cudaIpcCloseMemHandle(dev_ptr));
+}
+
+extern "C" cats_status_t cats_tp_comm_create(int rank, int world, uint64_t n_max, void *const *bufs, int device,
+                                             cats_tp_comm_t **out) {
+    if (!bufs || !out) return CATS_E_NULL;
+    if (world < 1 || world > kTpMaxWorld || rank < 0 || rank >= world || n_max == 0 || n_max % 4) return CATS_E_SHAPE;
+    for (int r = 0; r < world; ++r) {
+        if (!bufs[r]) return CATS_E_NULL;
+        if (reinterpret_cast<uintptr_t>(bufs[r]) & 15u) return CATS_E_ALIGN;
+    }
+    cats_tp_comm *c = new (std::nothrow) cats_tp_comm;
+    if (!c) return CATS_E_CUDA;
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    c->n_max = n_max;
+    c->ctas = tp_ctas(n_max);
+    for (int r = 0; r < kTpMaxWorld; ++r) c->bufs[r] = r < world ? static_cast<unsigned char *>(bufs[r]) : nullptr;
+    *out = c;
+    return CATS_OK;
+}
+
+extern "C" void cats_tp_comm_destroy(cats_tp_comm_t *comm) { delete comm; }
+
+namespace {
+cats_status_t tp_launch(cats_tp_comm_t *const *comms, int nlocal, const float *const *x, float *const *y, uint64_t n,
+                        cudaStream_t s, bool cooperative) {
+    const cats_tp_comm *c0 = comms[0];
+    if (n == 0 || n % 4 || n > c0->n_max) return CATS_E_SHAPE;
+    TpLaunch L{};
+    L.world = c0->world;
+    L.ctas = c0->ctas;
+    L.nlocal = nlocal;
+    L.rank0 = c0->rank;
+    L.n = n;
+    L.slot_floats = (c0->n_max + 3) / 4 * 4;
+    for (int l = 0; l < nlocal; ++l) {
+        const cats_tp_comm *c = comms[l];
+        if (!c || !x[l] || !y[l]) return CATS_E_NULL;
+        if (c->world != c0->world || c->n_max != c0->n_max || c->rank != c0->rank + l) return CATS_E_SHAPE;
+        if ((reinterpret_cast<uintptr_t>(x[l]) | reinterpret_cast<uintptr_t>(y[l])) & 15u) return CATS_E_ALIGN;
+        for (int r = 0; r < c->world; ++r) L.bufs[l][r] = c->bufs[r];
+        L.x[l] = x[l];
+        L.y[l] = y[l];
+    }
+    cudaError_t e = cudaSetDevice(c0->device);
+    if (e != cudaSuccess) return cuda_status_tp(e);
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nlocal * c0->ctas));
+    cfg.blockDim = dim3(kTpThreads);
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cooperative) {  // emulated ranks wait on one another: co-residency guaranteed (or the launch fails)
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+    } else {            // one rank: start while the decode drains (programmatic dependent launch)
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+    }
+    e = cudaLaunchKernelEx(&cfg, tp_allreduce_kernel, L);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return cuda_status_tp(e);
+}
+}  // namespace
+
+extern "C" cats_status_t cats_tp_allreduce(const cats_tp_comm_t *comm, const float *x, float *y, uint64_t n,
+                                           cats_stream_t s) {
+    if (!comm || !x || !y) return CATS_E_NULL;
+    cats_tp_comm_t *c = const_cast<cats_tp_comm_t *>(comm);
+    return tp_launch(&c, 1, &x, &y, n, static_cast<cudaStream_t>(s), false);
+}
+
+extern "C" cats_status_t cats_tp_allreduce_emulated(cats_tp_comm_t *const *comms, int world, const float *const *x,
+                                                    float *const *y, uint64_t n, cats_stream_t s) {
+    if (!comms || !x || !y) return CATS_E_NULL;
+    if (world < 1 || world > kTpMaxWorld) return CATS_E_SHAPE;
+    for (int r = 0; r < world; ++r)
+        if (!comms[r]) return CATS_E_NULL;
+    if (comms[0]->rank != 0 || comms[0]->world != world) return CATS_E_SHAPE;
+    return tp_launch(comms, world, x, y, n, static_cast<cudaStream_t>(s), true);
+}

@@ -69,12 +69,124 @@ def calibrate_threshold(acts: torch.Tensor, k: float, group=None, hist_fn=None, 
     raise RuntimeError("sharded calibration did not converge")
 
 
-def tp_decode(plan, x, W_gate_shard, W_up_shard, W_down_shard, t: float, y=None, ws=None, group=None, stream=None):
-    """y = sum over ranks of the rank-local CATS-MLP partials (one NCCL all-reduce)."""
+class TpComm:
+    """The fused one-shot cross-rank reduction (cats_tp_allreduce) for one process group:
+    every rank allocates its symmetric buffer, exports it with CUDA IPC, and opens every peer's (the
+    handles travel through torch.distributed, the plumbing; the reduction itself is one library kernel
+    that writes and reads peer memory over NVLink)."""
+
+    def __init__(self, n_max: int, group=None, device=None):
+        import ctypes
+        from . import _lib
+        self._lib = _lib.load()
+        self.rank = dist.get_rank(group) if group is not None else 0
+        self.world = dist.get_world_size(group) if group is not None else 1
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.n_max = int(n_max)
+        nb = ctypes.c_size_t()
+        _chk(self._lib.cats_tp_buffer_bytes(self.world, self.n_max, ctypes.byref(nb)), "cats_tp_buffer_bytes")
+        self.buf = torch.zeros(nb.value, dtype=torch.uint8, device=f"cuda:{self.device}")
+        torch.cuda.synchronize(self.device)
+        h = (ctypes.c_uint8 * 64)()
+        _chk(self._lib.cats_ipc_handle_get(self.buf.data_ptr(), h), "cats_ipc_handle_get")
+        handles = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(handles, bytes(h), group=group)
+        else:
+            handles = [bytes(h)]
+        self._opened = []
+        ptrs = (ctypes.c_void_p * self.world)()
+        for r, hb in enumerate(handles):
+            if r == self.rank:
+                ptrs[r] = self.buf.data_ptr()
+                continue
+            p = ctypes.c_void_p()
+            _chk(self._lib.cats_ipc_handle_open((ctypes.c_uint8 * 64).from_buffer_copy(hb), self.device,
+                                                ctypes.byref(p)), "cats_ipc_handle_open")
+            self._opened.append(p)
+            ptrs[r] = p.value
+        self._h = ctypes.c_void_p()
+        _chk(self._lib.cats_tp_comm_create(self.rank, self.world, self.n_max, ptrs, self.device, ctypes.byref(self._h)),
+             "cats_tp_comm_create")
+        if self.world > 1:
+            dist.barrier(group=group)
+
+    def allreduce(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """y = sum over ranks of x (fp32, fixed rank order, identical on every rank); x and y may alias."""
+        y = x if y is None else y
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        _chk(self._lib.cats_tp_allreduce(self._h, x.data_ptr(), y.data_ptr(), x.numel(), st.cuda_stream),
+             "cats_tp_allreduce")
+        return y
+
+    def __del__(self):
+        lib = getattr(self, "_lib", None)
+        if lib is None:
+            return
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.cats_tp_comm_destroy(h)
+        for p in getattr(self, "_opened", []):
+            lib.cats_ipc_handle_close(p)
+
+
+def _chk(rc, where):
+    if rc != 0:
+        from . import CatsError
+        raise CatsError(rc, where)
+
+
+def tp_decode(plan, x, W_gate_shard, W_up_shard, W_down_shard, t: float, y=None, ws=None, group=None, stream=None,
+              comm: TpComm | None = None):
+    """y = sum over ranks of the rank-local CATS-MLP partials: the fused one-shot reduction (comm) or one
+    NCCL all-reduce (group)."""
     y = cats_mlp_decode(plan, x, W_gate_shard, W_up_shard, W_down_shard, t, y=y, ws=ws, stream=stream)
-    if group is not None and dist.get_world_size(group) > 1:
+    if comm is not None and comm.world > 1:
+        comm.allreduce(y, stream=stream)
+    elif group is not None and dist.get_world_size(group) > 1:
         dist.all_reduce(y, group=group)
     return y
 
 
-__all__ = ["shard_rows", "calibrate_threshold", "tp_decode", "CATS_BF16"]
+
+
+
+class EmulatedTpComms:
+    """P ranks of the fused reduction emulated on ONE device (cats_tp_allreduce_emulated): P symmetric
+    buffers on this GPU and P comms over them; allreduce(xs, ys) runs every rank's step in one cooperative
+    launch. For testing the exchange protocol where fewer GPUs than ranks are available."""
+
+    def __init__(self, world: int, n_max: int, device=None):
+        import ctypes
+        from . import _lib
+        self._lib = _lib.load()
+        self.world, self.n_max = int(world), int(n_max)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        nb = ctypes.c_size_t()
+        _chk(self._lib.cats_tp_buffer_bytes(self.world, self.n_max, ctypes.byref(nb)), "cats_tp_buffer_bytes")
+        self.bufs = [torch.zeros(nb.value, dtype=torch.uint8, device=f"cuda:{self.device}") for _ in range(world)]
+        ptrs = (ctypes.c_void_p * world)(*[b.data_ptr() for b in self.bufs])
+        self._h = []
+        for r in range(world):
+            h = ctypes.c_void_p()
+            _chk(self._lib.cats_tp_comm_create(r, world, self.n_max, ptrs, self.device, ctypes.byref(h)),
+                 "cats_tp_comm_create")
+            self._h.append(h)
+
+    def allreduce(self, xs, ys=None, stream=None):
+        import ctypes
+        ys = xs if ys is None else ys
+        n = xs[0].numel()
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        H = (ctypes.c_void_p * self.world)(*[h.value for h in self._h])
+        X = (ctypes.c_void_p * self.world)(*[x.data_ptr() for x in xs])
+        Y = (ctypes.c_void_p * self.world)(*[y.data_ptr() for y in ys])
+        _chk(self._lib.cats_tp_allreduce_emulated(H, self.world, X, Y, n, st.cuda_stream), "cats_tp_allreduce_emulated")
+        return ys
+
+    def __del__(self):
+        lib = getattr(self, "_lib", None)
+        for h in getattr(self, "_h", []):
+            if lib is not None and h.value:
+                lib.cats_tp_comm_destroy(h)
+__all__ = ["shard_rows", "calibrate_threshold", "tp_decode", "TpComm", "EmulatedTpComms", "CATS_BF16"]

@@ -279,8 +279,10 @@ def test_plan_options():
     assert [cats.cats_mlp_kernels_per_call(pred, b) for b in range(1, 9)] == [1] * 8
     atom = cats.MlpPlan(4096, 11008, max_batch=8, num_sms=148, compaction=cats.CATS_COMPACT_ATOMIC)
     assert [cats.cats_mlp_kernels_per_call(atom, b) for b in range(1, 9)] == [2] * 8  # gate + list kernel
-    assert atom.workspace_bytes >= auto.workspace_bytes + 11008 * 4 * 9  # the global idcs list (ids + v)
+    assert atom.workspace_bytes >= fused.workspace_bytes + 11008 * 4 * 9  # the global idcs list (ids + v)
     assert cats.MlpPlan(5120, 13824, num_sms=148, rows_per_tile=2).info["rows_per_tile"] == 2
+    split1 = cats.MlpPlan(5120, 1728, max_batch=8, num_sms=148, path=cats.CATS_PATH_SPLIT)
+    assert cats.cats_mlp_kernels_per_call(split1, 1) == 2  # KA + KB at b = 1 (small TP shards)
     # KB's last-64 reduction needs more than 64 SMs: smaller devices take K12 at every batch size
     small = cats.MlpPlan(4096, 11008, max_batch=8, num_sms=64)
     assert [cats.cats_mlp_kernels_per_call(small, b) for b in range(1, 9)] == [1] * 8
@@ -312,3 +314,19 @@ def test_binding_checks_shapes_before_the_abi():
         cats.cats_mlp_decode_host(p, torch.zeros(2, 255, dtype=torch.bfloat16), w, w, w, 0.1)
     with pytest.raises(TypeError):
         cats.cats_mlp_decode_host(p, torch.zeros(2, 256, dtype=torch.float32), w, w, w, 0.1)
+
+
+def test_tp_comm_validation_without_gpu():
+    """The fused TP reduction's host side (cats_tp_*): buffer sizing and argument checks, no device needed."""
+    nb = ctypes.c_size_t()
+    assert lib.cats_tp_buffer_bytes(4, 5120, ctypes.byref(nb)) == 0
+    assert nb.value >= 2 * 4 * 5120 * 4
+    for w, n in [(0, 5120), (9, 5120), (4, 0), (4, 5122)]:
+        assert lib.cats_status_string(lib.cats_tp_buffer_bytes(w, n, ctypes.byref(nb))).decode() == "CATS_E_SHAPE"
+    ptrs = (ctypes.c_void_p * 2)(FAKE, FAKE + 4096)
+    h = ctypes.c_void_p()
+    assert lib.cats_tp_comm_create(1, 2, 5120, ptrs, 0, ctypes.byref(h)) == 0
+    lib.cats_tp_comm_destroy(h)
+    assert lib.cats_status_string(lib.cats_tp_comm_create(2, 2, 5120, ptrs, 0, ctypes.byref(h))).decode() == "CATS_E_SHAPE"
+    bad = (ctypes.c_void_p * 2)(FAKE, FAKE + 4)
+    assert lib.cats_status_string(lib.cats_tp_comm_create(0, 2, 5120, bad, 0, ctypes.byref(h))).decode() == "CATS_E_ALIGN"
