@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--copies", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extras", action="store_true", help="also time dense/cuBLAS/profiled (default on)")
+    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "fused"],
+                    help="N > 1: NCCL all-reduce, or the library's one-shot NVLink reduction (cats_tp_allreduce)")
     ap.add_argument("--launcher-selftest", action="store_true",
                     help="start the ranks, all-reduce one tensor, print one line (CPU: gloo) and exit")
     return ap.parse_args()
@@ -298,12 +300,19 @@ def main():
 
     xs = cats_synth.tokens(64 * b, d, torch.bfloat16, seed=1).to(dev).view(64, b, d)
     y = torch.empty((b, d), dtype=torch.float32, device=dev)
+    comm = tpmod.TpComm(b * d, group=dist.group.WORLD) if world > 1 and args.allreduce == "fused" else None
+
+    def reduce_y(st):
+        if world > 1:
+            if comm is not None:
+                comm.allreduce(y, stream=st)
+            else:
+                dist.all_reduce(y)
 
     def step(i, st=stream):
         W = copies[i % len(copies)]
         cats.cats_mlp_decode(plan, xs[i % 64], W[0], W[1], W[2], t, y=y, ws=ws, stream=st)
-        if world > 1:
-            dist.all_reduce(y)
+        reduce_y(st)
 
     # CUDA graph of G consecutive steps (the library calls are stream-ordered, allocation- and
     # sync-free, so they capture as-is); replayed K/G times in the timed region
@@ -397,8 +406,7 @@ def main():
     def dense_step(i):
         W = copies[i % len(copies)]
         cats.cats_mlp_dense(plan, xs[i % 64], W[0], W[1], W[2], y=y, ws=ws, stream=stream)
-        if world > 1:
-            dist.all_reduce(y)
+        reduce_y(stream)
     dense_ms = timed(dense_step, min(args.steps, 1000), 20)
 
     def cublas_step(i):
@@ -421,14 +429,14 @@ def main():
         else:
             xd = xh[i % 64].to(dev, non_blocking=True)
             cats.cats_mlp_decode(plan, xd, W[0], W[1], W[2], t, y=y, ws=ws, stream=stream)
-            dist.all_reduce(y)
+            reduce_y(stream)
             yh.copy_(y, non_blocking=False)
     e2e_ms = timed(e2e_step, min(args.steps, 1000), 10)
 
     # ---- TP: the all-reduce alone (its share of the step), same buffer and stream
     allreduce_us = None
     if world > 1:
-        allreduce_us = timed(lambda i: dist.all_reduce(y), min(args.steps, 1000), 20) * 1e3
+        allreduce_us = timed(lambda i: reduce_y(stream), min(args.steps, 1000), 20) * 1e3
 
     # ---- roofline of the dominant kernel (algorithmic bytes / live CUDA-event duration)
     hbm_peak, peak_kind = peaks()
@@ -491,6 +499,7 @@ def main():
             "gpu_launches": args.steps * kernels_per_step,
             "clocks": clocks,
             "detail": {
+                "allreduce": None if world == 1 else args.allreduce,
                 "nccl": None if world == 1 else {"version": ".".join(map(str, torch.cuda.nccl.version())),
                                                  "nranks": world, "collective": "all_reduce sum fp32 b x d"},
                 "t": t, "nnz_union_per_rank": nnz_local, "nnz_union_total": U, "m_per_rank": ms,

@@ -133,8 +133,9 @@ extern "C" cats_status_t cats_calib_window_init(uint64_t n, cats_dtype_t dt, cat
     if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
     make_window(0, key_max(dt), CATS_CALIB_MAX_BINS, w);
     const uint64_t nvec = n / (dt == CATS_BF16 ? 8 : 4);
-    // sample ~2^17 vectors (~1M bf16 values) when the data is large; odd stride against aliasing
-    w->sample_stride = nvec > (1ull << 21) ? ((nvec >> 17) | 1ull) : 0ull;
+    // sample ~2^20 vectors (~8M bf16 values) when the data is large; odd stride against aliasing. The
+    // sample's 6-sigma margin is then ~0.1% of the mass: the full pass's window holds a key or two
+    w->sample_stride = nvec > (1ull << 24) ? ((nvec >> 20) | 1ull) : 0ull;
     return CATS_OK;
 }
 
@@ -429,8 +430,11 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.off_ystage = off;  off = align_up(off + (size_t)max_batch * d * 4, 256);
         // split path (b >= 2): x1 per compact position and the KB range partials
         // non-default compaction modes (the App. D ablation) run K12-based kernels at every batch size
+        // AUTO: K12 at b = 1 while a consumer thread holds <= 2 chunks of a row (d <= 4096 bf16); wider rows
+        // (Llama2-13B, d = 5120: K12 needs 3 chunks per thread and 4-row tiles) take KA + KB from b = 1
+        // (measured, 13B b = 1: 51.9 vs 57.6 us unsharded, 17.4 vs 19.1 us at the TP8 shard)
         p.split_min_b = (o.path == CATS_PATH_FUSED || p.compaction != CATS_COMPACT_BALLOT) ? CATS_MAX_BATCH + 1
-                        : o.path == CATS_PATH_SPLIT ? 1 : 2;
+                        : (o.path == CATS_PATH_SPLIT || (esize == 2 && k12_cpt(p, 1) >= 3)) ? 1 : 2;
         size_t part_bytes = 0, x1_bytes = 0;
         for (int b = p.split_min_b; b <= max_batch; ++b) {
             if (!split_supported(p, b)) continue;

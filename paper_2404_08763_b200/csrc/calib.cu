@@ -170,7 +170,8 @@ calib_hist_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint32_t 
 constexpr int kCalStageBytes = 32 * 1024;
 constexpr int kCalMaxStages = 6;
 constexpr int kCalClaim = 4;  // chunks per claim
-constexpr int kCalConsumerWarps = 16;
+constexpr int kCalConsumerWarps = 32;
+constexpr int kCalRegBins = 8;  // windows of <= 8 bins are counted in registers
 constexpr int kCalTmaThreads = (kCalConsumerWarps + 1) * 32;
 
 template <typename K>
@@ -237,12 +238,22 @@ calib_hist_tma_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint3
         }
     } else {
         // ---------------- consumers ----------------
+        // in-window keys: a window of <= kCalRegBins bins (the usual case: the sample pass aims it at a
+        // key or two) is counted in registers (unrolled compare-adds, no shared atomics on a hot bin);
+        // wider windows go to the shared-memory histogram with a run-length cache
+        const bool regbins = nbins <= (uint32_t)kCalRegBins;
+        uint32_t rc[kCalRegBins];
+#pragma unroll
+        for (int j = 0; j < kCalRegBins; ++j) rc[j] = 0u;
         uint32_t cur_bin = 0xffffffffu, cur_cnt = 0;
         const uint32_t span = hi - lo;
         auto classify_in = [&](uint32_t key) {
             ++inwin;
             const uint32_t bin = (key - lo) >> shift;
-            if (bin == cur_bin) {
+            if (regbins) {
+#pragma unroll
+                for (int j = 0; j < kCalRegBins; ++j) rc[j] += bin == (uint32_t)j ? 1u : 0u;
+            } else if (bin == cur_bin) {
                 ++cur_cnt;
             } else {
                 if (cur_cnt) atomicAdd(&sh[cur_bin], cur_cnt);
@@ -266,11 +277,9 @@ calib_hist_tma_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint3
             uint4 r[VPT];
 #pragma unroll
             for (int u = 0; u < VPT; ++u) r[u] = lds128(sb + (uint32_t)((u * NC + tid) * 16));
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);  // the stage is in registers: let the producer refill it
             if constexpr (sizeof(K) == 2) {
                 // two keys per 32-bit word, SIMD within the register (see calib_hist_kernel)
-                uint32_t hit = 0;  // words with an in-window key, handled after the SIMD sweep
+                uint32_t hit = 0;  // words holding an in-window key: handled after the sweep, from smem
 #pragma unroll
                 for (int u = 0; u < VPT; ++u) {
                     const uint32_t wv[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
@@ -283,17 +292,12 @@ calib_hist_tma_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint3
                         hit |= ((hi2x - k2) & gl) ? (1u << (u * 4 + q)) : 0u;
                     }
                 }
-                while (hit) {  // rare: keys inside the (sample-aimed) window
+                while (hit) {  // rare: re-read the word from the (still owned) stage
                     const int wq = __ffs(hit) - 1;
                     hit &= hit - 1;
-                    uint32_t w = 0;
-#pragma unroll
-                    for (int u = 0; u < VPT; ++u) {
-                        if ((wq >> 2) == u) {
-                            const int q = wq & 3;
-                            w = q == 0 ? r[u].x : q == 1 ? r[u].y : q == 2 ? r[u].z : r[u].w;
-                        }
-                    }
+                    uint32_t w;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w)
+                                 : "r"(sb + (uint32_t)(((wq >> 2) * NC + tid) * 16 + (wq & 3) * 4)));
                     const uint32_t gl = ((w | 0x80008000u) - lo2) & 0x80008000u;
                     const uint32_t k2 = w & 0x7fff7fffu;
                     const uint32_t iw = (hi2x - k2) & gl;
@@ -308,6 +312,8 @@ calib_hist_tma_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint3
                     for (int e = 0; e < E; ++e) classify(KT::key(r[u], e));
                 seen += VPT * E;
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // stage consumed: the producer may refill it
         }
         if constexpr (sizeof(K) == 2) {
             below += seen_main - nge2;
@@ -323,6 +329,15 @@ calib_hist_tma_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint3
             }
         }
         if (cur_cnt) atomicAdd(&sh[cur_bin], cur_cnt);
+        if (regbins) {
+#pragma unroll
+            for (int j = 0; j < kCalRegBins; ++j) {
+                uint32_t v = rc[j];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0 && v) atomicAdd(&sh[j], v);
+            }
+        }
     }
     const uint32_t above = seen - below - inwin - nonfin;
     const unsigned long long c4[4] = {below, inwin, above, nonfin};
