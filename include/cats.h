@@ -365,9 +365,10 @@ cats_status_t cats_tp_allreduce_emulated(cats_tp_comm_t *const *comms, int world
 /* Diagnostics. When the plan was created with options.trace = 1, the kernels
  * record %globaltimer stamps (ns) per CTA into a trace area of the workspace:
  * uint64 trace[3][512 CTAs][8 slots] at byte `offset` (bytes = 0 when tracing is off).
- * [0] K12 / KA slots: 0 start, 1 ring primed, 2 jobs done, 3 exit, 4 K12 partial reduced;
- * [1] KB slots: 0 start, 1 list ready, 2 jobs done, 3 barrier passed, 4 exit, 5 masks read,
- *     6 prefix done;
+ * [0] K12 / KA slots: 0 start, 1 ring primed, 2 jobs done, 3 exit, 4 K12 partial reduced, 5 all consumer
+ *     warps done, 6 partial staged (bulk reduce issued), 7 bulk reduce complete;
+ * [1] KB slots: 0 start, 1 list ready, 2 jobs done, 3 reducer released (last-64 reducers only), 4 exit,
+ *     5 masks read, 6 prefix done;
  * [2] per-CTA producer/consumer statistics (see scripts/trace_decode.py). */
 cats_status_t cats_mlp_trace_info(const cats_mlp_plan_t *plan, size_t *offset, size_t *bytes);
 

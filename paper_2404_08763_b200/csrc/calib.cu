@@ -170,12 +170,12 @@ calib_hist_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint32_t 
 constexpr int kCalStageBytes = 32 * 1024;
 constexpr int kCalMaxStages = 6;
 constexpr int kCalClaim = 4;  // chunks per claim
-constexpr int kCalConsumerWarps = 32;
+constexpr int kCalConsumerWarps = 16;
 constexpr int kCalRegBins = 8;  // windows of <= 8 bins are counted in registers
 constexpr int kCalTmaThreads = (kCalConsumerWarps + 1) * 32;
 
 template <typename K>
-__global__ void __launch_bounds__(kCalTmaThreads, 1)
+__global__ void __launch_bounds__(kCalTmaThreads, 2)
 calib_hist_tma_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint32_t hi, uint32_t shift,
                       uint32_t nbins, int kCalStages, unsigned long long *__restrict__ hist,
                       unsigned long long *__restrict__ counts) {
@@ -376,21 +376,24 @@ cudaError_t launch_calib_hist(const void *acts, uint64_t n, cats_dtype_t dt, con
     const int grid = (int)std::min<uint64_t>(want, (uint64_t)nsm * blocks_per_sm);
     auto *h = reinterpret_cast<unsigned long long *>(hist);
     auto *c = reinterpret_cast<unsigned long long *>(counts);
-    const int tstages = (int)std::min<size_t>(kCalMaxStages, (220 * 1024 - (size_t)w.nbins * 4) / (kCalStageBytes + 20));
+    // two CTAs per SM (two producers, 2 x 16 consumer warps), each with a ring of 32 KB stages
+    const size_t bins_smem = w.nbins <= (uint32_t)kCalRegBins ? 64 : (size_t)w.nbins * 4;
+    const int tstages = (int)std::min<size_t>(kCalMaxStages, (110 * 1024 - bins_smem) / (kCalStageBytes + 20));
     if (!w.sample_stride && tstages >= 2 && (uint64_t)n * (dt == CATS_BF16 ? 2 : 4) >= (uint64_t)kCalStageBytes * nsm) {
         // full pass over a large buffer: the TMA-ring kernel, one CTA per SM
         const size_t tsmem = (size_t)tstages * (kCalStageBytes + 16 + 4) + (size_t)w.nbins * 4;
+        const int tgrid = 2 * nsm;
         if (dt == CATS_BF16) {
             auto kern = calib_hist_tma_kernel<uint16_t>;
             cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), tsmem);
             if (e != cudaSuccess) return e;
-            kern<<<nsm, kCalTmaThreads, tsmem, s>>>(static_cast<const uint16_t *>(acts), n, w.lo, w.hi, w.shift,
+            kern<<<tgrid, kCalTmaThreads, tsmem, s>>>(static_cast<const uint16_t *>(acts), n, w.lo, w.hi, w.shift,
                                                      w.nbins, tstages, h, c);
         } else {
             auto kern = calib_hist_tma_kernel<uint32_t>;
             cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), tsmem);
             if (e != cudaSuccess) return e;
-            kern<<<nsm, kCalTmaThreads, tsmem, s>>>(static_cast<const uint32_t *>(acts), n, w.lo, w.hi, w.shift,
+            kern<<<tgrid, kCalTmaThreads, tsmem, s>>>(static_cast<const uint32_t *>(acts), n, w.lo, w.hi, w.shift,
                                                      w.nbins, tstages, h, c);
         }
         return cudaGetLastError();

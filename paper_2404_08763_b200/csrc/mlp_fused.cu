@@ -559,6 +559,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         __shared__ unsigned int s_last;
         if (has_y) {
             consumer_barrier<NC>();  // every consumer warp is past its last job: the ring is idle
+            trace_stamp(trace, 0, 5);
             unsigned long long *sbuf = reinterpret_cast<unsigned long long *>(ring);
             const int tpc = min(B, (int)(((size_t)stages * stage_bytes) / ((size_t)d * 8)));  // tokens per chunk
             for (int t0 = 0; t0 < B; t0 += tpc) {
@@ -583,8 +584,10 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk engine
                 consumer_barrier<NC>();
                 if (tid == 0) {
+                    trace_stamp(trace, 0, 6);
                     bulk_reduce_add_u64(yacc + (size_t)t0 * d, sbuf, (uint32_t)((size_t)tn * d * 8));
                     bulk_commit_and_wait_all();
+                    trace_stamp(trace, 0, 7);
                 }
                 consumer_barrier<NC>();  // sbuf reusable
             }
