@@ -318,8 +318,8 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
     if (o.compaction < CATS_COMPACT_BALLOT || o.compaction > CATS_COMPACT_ATOMIC) return CATS_E_UNSUPPORTED;
     if (o.lazy_tail < 0 || o.min_tiles < 1 || o.l2_prefetch < 0 || o.max_stages < 0 || o.max_stages == 1 ||
         (o.rows_per_tile != 0 && o.rows_per_tile != 2 && o.rows_per_tile != 4 && o.rows_per_tile != 6) ||
-        o.xs_cols < 0 || o.xs_ranges < 0 || o.xs_ranges > 8 || o.tail_rows < 0 || o.tail_rows == 1 ||
-        o.tail_rows > 6 || o.tail_tiles < 0)
+        o.xs_cols < 0 || o.xs_ranges < 0 || o.xs_ranges > 8 || o.tail_rows < 0 ||
+        o.tail_rows > 6 || o.tail_tiles < 0 || o.tail_fused < 0 || o.tail_fused > 1)
         return CATS_E_SHAPE;
     if (d <= 0 || m <= 0) return CATS_E_SHAPE;
     if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
@@ -346,6 +346,7 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.nr_force = o.rows_per_tile;
         p.tail_rows = o.tail_rows;
         p.tail_tiles = o.tail_tiles;
+        p.tail_fused = o.tail_fused;
         p.trace = o.trace != 0;
         p.kind = kind;
         p.g1 = 0;
@@ -424,7 +425,7 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.off_idx = off;     off = align_up(off + (size_t)m * 4, 256);
         p.off_tokmask = off; off = align_up(off + (size_t)m, 256);
         p.off_vals = off;    off = align_up(off + (size_t)m * max_batch * 4, 256);
-        p.off_cnt = off;     off = align_up(off + (size_t)((m + 1) / 2) * 4, 256);
+        p.off_cnt = off;     off = align_up(off + (size_t)m * 4, 256);  // per-tile counts (tail tiles may be 1 row)
         p.off_ypart = off;   off = align_up(off + (size_t)max_batch * d * 8, 256);  // int64 y accumulator
         p.off_xstage = off;  off = align_up(off + (size_t)max_batch * d * esize, 256);
         p.off_ystage = off;  off = align_up(off + (size_t)max_batch * d * 4, 256);

@@ -378,7 +378,9 @@ cudaError_t launch_calib_hist(const void *acts, uint64_t n, cats_dtype_t dt, con
     auto *c = reinterpret_cast<unsigned long long *>(counts);
     // two CTAs per SM (two producers, 2 x 16 consumer warps), each with a ring of 32 KB stages
     const size_t bins_smem = w.nbins <= (uint32_t)kCalRegBins ? 64 : (size_t)w.nbins * 4;
-    const int tstages = (int)std::min<size_t>(kCalMaxStages, (110 * 1024 - bins_smem) / (kCalStageBytes + 20));
+    const size_t tbudget = 110 * 1024;
+    const int tstages = bins_smem >= tbudget ? 0
+                      : (int)std::min<size_t>(kCalMaxStages, (tbudget - bins_smem) / (kCalStageBytes + 20));
     if (!w.sample_stride && tstages >= 2 && (uint64_t)n * (dt == CATS_BF16 ? 2 : 4) >= (uint64_t)kCalStageBytes * nsm) {
         // full pass over a large buffer: the TMA-ring kernel, one CTA per SM
         const size_t tsmem = (size_t)tstages * (kCalStageBytes + 16 + 4) + (size_t)w.nbins * 4;

@@ -53,6 +53,7 @@ struct PlanData {
     int compaction;     // cats_compaction_t (options.compaction)
     int tail_rows;      // K12 tail tiles: rows per tail tile (options.tail_rows; 0 = uniform tiles)
     int tail_tiles;     // K12 tail tiles per CTA (options.tail_tiles)
+    int tail_fused;     // K12 tail tiles as fused gate+up+down jobs (options.tail_fused)
     int kind;           // 0 = gated-MLP plan, 1 = App. B input-sparse projection plan (d = d_out, m = d_in)
     struct XsCfg {            // kind 1 (xsparse.cu), per batch size b = 1..8:
         int cols, q, r;       //   columns per CTA, column parts, cluster size (ranges of the kept list)
@@ -91,7 +92,7 @@ inline int k12_grid(const PlanData &p, int b) {  // >= k12_min_tiles tiles per C
 // k12_tail_rows (k12_ntiles stays the uniform count, used for grid sizing and by KA / KB).
 inline int k12_tail_rows(const PlanData &p, int b) {
     const int nr = k12_rows_per_tile(p, b);
-    return (p.tail_rows >= 2 && p.tail_rows < nr && p.tail_tiles > 0) ? p.tail_rows : nr;
+    return (p.tail_rows >= 1 && p.tail_rows < nr && p.tail_tiles > 0) ? p.tail_rows : nr;
 }
 inline int k12_t1(const PlanData &p, int b) {
     const int nr = k12_rows_per_tile(p, b), ns = k12_tail_rows(p, b);

@@ -45,7 +45,11 @@
 
 namespace cats {
 
-enum : int { kJobEnd = 0, kJobGate = 1, kJobUD = 2 };
+enum : int { kJobEnd = 0, kJobGate = 1, kJobUD = 2, kJobGUD = 3 };
+// kJobGUD (tail tiles, options.tail_fused): one stage carries a tail tile's W_gate, W_up and W_down rows
+// ([NG rows of each], NG = NR / 3); the consumers compute u -> v -> keep themselves and finish the
+// tile in the same job -- the mask -> UD-load round trip (two loaded HBM latencies in a row at the end
+// of the schedule) becomes one, for the price of reading the tail tiles' inactive W_up / W_down rows.
 
 
 
@@ -75,7 +79,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
              int d, int m, int stages, float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask,
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
              unsigned long long *__restrict__ yacc, float *__restrict__ y, unsigned int *__restrict__ sched,
-             int32_t *__restrict__ gidx, float *__restrict__ gval, int t1, int ns,
+             int32_t *__restrict__ gidx, float *__restrict__ gval, int t1, int ns, int tail_fused,
              int lazy_tail, int eager, int l2pf, unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
@@ -100,6 +104,8 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     auto tile_rows = [t1, ns, m](int tile, int r0) { return min(tile < t1 ? NR : ns, m - r0); };
     const bool list_mode = mode == kModeAtomicList;  // App. D Alg. 1, launch 2: work units = chunks of idcs
     const bool has_y = mode != kModeGateOnly && mode != kModeAtomicGate;
+    constexpr int NG = NR / 3 > 0 ? NR / 3 : 1;  // rows of a fused tail tile (GUD job)
+    const bool gud_tail = tail_fused && NR >= 3 && ns <= NG && (mode == kModeCats || mode == kModeDense);
 
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char *ring = smem;                                                           // [stages][stage_bytes]
@@ -228,14 +234,27 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                         t_res = kNoTile;
                         claim_tile_async(t_res, sched, tile + (unsigned)lazy_tail < (unsigned)ntl);
                     }
-                    if (lane == 0) {
-                        D.type = kJobGate;
-                        D.tile = (int)tile;
-                        D.n = nr;
-                        mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
-                        bulk_g2s(dst, Wg + (size_t)r0 * d, (uint32_t)nr * row_bytes, &full[s], policy);
+                    if (gud_tail && (int)tile >= t1) {  // fused tail tile: W_gate, W_up, W_down rows at once
+                        if (lane == 0) {
+                            D.type = kJobGUD;
+                            D.tile = (int)tile;
+                            D.n = nr;
+                            mbar_arrive_expect_tx(&full[s], 3u * (uint32_t)nr * row_bytes);
+                        }
+                        __syncwarp();
+                        if (lane < 3)
+                            bulk_g2s(dst + (size_t)lane * nr * row_bytes, (lane == 0 ? Wg : lane == 1 ? Wu : Wd) + (size_t)r0 * d,
+                                     (uint32_t)nr * row_bytes, &full[s], policy);
+                    } else {
+                        if (lane == 0) {
+                            D.type = kJobGate;
+                            D.tile = (int)tile;
+                            D.n = nr;
+                            mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
+                            bulk_g2s(dst, Wg + (size_t)r0 * d, (uint32_t)nr * row_bytes, &full[s], policy);
+                        }
+                        ++gates_inflight;
                     }
-                    ++gates_inflight;
                     if (trace) t_last_gate = gtimer();
                 } else {
                     if (lane == 0) t_res = tile - dyn_base;  // past the end: keep it, no further claims
@@ -461,6 +480,113 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);  // stage read + partials written -> producer
+            } else if (type == kJobGUD) {
+                ++n_ud;
+                const int tile = desc[s].tile, r0 = tile_r0(tile);
+                constexpr int NPGU = NG * B;
+                constexpr int PPR = 32 / NW;
+                uint4 wg[NG][CPT], wu[NG][CPT], wd[NG][CPT];
+#pragma unroll
+                for (int i = 0; i < NG; ++i)
+#pragma unroll
+                    for (int k = 0; k < CPT; ++k) {
+                        const int ch = tid + k * NC;
+                        const bool ok = i < n && ch < nch;
+                        const uint32_t off = (uint32_t)i * row_bytes + (uint32_t)ch * 16u;
+                        wg[i][k] = ok ? lds128(sbase + off) : make_uint4(0u, 0u, 0u, 0u);
+                        wu[i][k] = ok ? lds128(sbase + (uint32_t)n * row_bytes + off) : make_uint4(0u, 0u, 0u, 0u);
+                        wd[i][k] = ok ? lds128(sbase + 2u * (uint32_t)n * row_bytes + off) : make_uint4(0u, 0u, 0u, 0u);
+                    }
+                // u = x W_gate[:, j] and up = x W_up[:, j]: per-thread partials -> warp sums -> red
+                float pg[NG][B], pu[NG][B];
+#pragma unroll
+                for (int i = 0; i < NG; ++i)
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) {
+                        pg[i][tk] = 0.f;
+                        pu[i][tk] = 0.f;
+#pragma unroll
+                        for (int k = 0; k < CPT; ++k) {
+                            pg[i][tk] = dot16<T>(wg[i][k], xr[tk][k], pg[i][tk]);
+                            pu[i][tk] = dot16<T>(wu[i][k], xr[tk][k], pu[i][tk]);
+                        }
+                    }
+#pragma unroll
+                for (int i = 0; i < NG; ++i)
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) {
+                        const float vg = warp_allreduce_sum(pg[i][tk]);
+                        const float vu = warp_allreduce_sum(pu[i][tk]);
+                        if (lane == 0) {
+                            rb[warp * NPMAX + i * B + tk] = vg;
+                            rb[warp * NPMAX + NPGU + i * B + tk] = vu;
+                        }
+                    }
+                consumer_barrier<NC>();
+                // cross-warp sums (fixed tree, identical in every warp) of the 2 NG B pairs
+                float sg[2 * NPGU];
+#pragma unroll
+                for (int c = 0; c < (2 * NPGU + PPR - 1) / PPR; ++c) {
+                    const int pp = c * PPR + lane / NW;
+                    float v = (pp < 2 * NPGU) ? rb[(lane % NW) * NPMAX + pp] : 0.f;
+#pragma unroll
+                    for (int o = NW / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+#pragma unroll
+                    for (int q = 0; q < PPR; ++q)
+                        if (c * PPR + q < 2 * NPGU) sg[c * PPR + q] = __shfl_sync(0xffffffffu, v, q * NW);
+                }
+                consumer_barrier<NC>();  // every warp has read red[s]
+                if (lane == 0) mbar_arrive(&empty[s]);  // stage, descriptor and red[s] released
+                // v = SiLU(u) (Eq. 2), keep = |v| >= t (Eq. 4), x1 = up * v (Optimization 1), pre-scaled 2^8
+                float x1[NG][B];
+                uint32_t bits[NG];
+#pragma unroll
+                for (int i = 0; i < NG; ++i) {
+                    bits[i] = 0u;
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk) {
+                        const float u = sg[i * B + tk];
+                        const float v = __fdividef(u, 1.0f + __expf(-u));
+                        const bool keep = i < n && (mode == kModeDense || fabsf(v) >= t);
+                        bits[i] |= (keep ? 1u : 0u) << tk;
+                        x1[i][tk] = keep ? (sg[NPGU + i * B + tk] * v) * kFixPre : 0.f;
+                    }
+                }
+                if (warp == 0) {  // bookkeeping of the tile: ascending active rows at [r0, r0 + cnt)
+                    int rank = 0;
+#pragma unroll
+                    for (int i = 0; i < NG; ++i) {
+                        if (lane == 0 && bits[i]) {
+                            const int pos = r0 + rank;
+                            idx[pos] = r0 + i;
+                            tokmask[pos] = (uint8_t)bits[i];
+#pragma unroll
+                            for (int tk = 0; tk < B; ++tk) {
+                                const float u = sg[i * B + tk];
+                                const float v = __fdividef(u, 1.0f + __expf(-u));
+                                vals[(size_t)pos * B + tk] = ((bits[i] >> tk) & 1u) ? v : 0.0f;
+                            }
+                        }
+                        rank += bits[i] ? 1 : 0;
+                    }
+                    if (lane == 0) cnt[tile] = rank;
+                }
+                // ---- down: y_job[c] = sum_i x1_i W_down[i][c] (fp32, fixed order) -> fixed point ----
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    float wf[NG][VEC];
+#pragma unroll
+                    for (int i = 0; i < NG; ++i) unpack16(wd[i][k], wf[i]);
+#pragma unroll
+                    for (int tk = 0; tk < B; ++tk)
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            float yj = 0.f;
+#pragma unroll
+                            for (int i = 0; i < NG; ++i) yj = fmaf(x1[i][tk], wf[i][e], yj);
+                            fix_acc(yhi[tk][k][e], ylo[tk][k][e], yj);
+                        }
+                }
             } else {  // kJobUD
                 ++n_ud;
                 float vj[NU][B];  // descriptor -> registers before releasing the stage
@@ -672,7 +798,8 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
         reinterpret_cast<uint8_t *>(w + p.off_tokmask), reinterpret_cast<float *>(w + p.off_vals),
         reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<unsigned long long *>(w + p.off_ypart), y,
         reinterpret_cast<unsigned int *>(w + p.off_sched), reinterpret_cast<int32_t *>(w + p.off_gidx),
-        reinterpret_cast<float *>(w + p.off_gval), k12_t1(p, B), k12_tail_rows(p, B), p.lazy_tail * k12_grid(p, B),
+        reinterpret_cast<float *>(w + p.off_gval), k12_t1(p, B), k12_tail_rows(p, B), p.tail_fused,
+        p.lazy_tail * k12_grid(p, B),
         p.k12_eager, p.k12_l2pf,
         p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
     if (e != cudaSuccess) return e;
