@@ -699,11 +699,22 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                         if (ch < nch) {
                             ulonglong2 *dst =
                                 reinterpret_cast<ulonglong2 *>(sbuf + (size_t)(tk - t0) * d + (size_t)ch * VEC);
+                            ulonglong2 qv[VEC / 2];
 #pragma unroll
                             for (int q = 0; q < VEC / 2; ++q)
-                                dst[q] = make_ulonglong2(
+                                qv[q] = make_ulonglong2(
                                     (unsigned long long)fix_value(yhi[tk][k][2 * q], ylo[tk][k][2 * q]),
                                     (unsigned long long)fix_value(yhi[tk][k][2 * q + 1], ylo[tk][k][2 * q + 1]));
+                            // a thread's 16-byte pieces in lane-rotated order: the 32 lanes' stores of one
+                            // instruction then spread over all banks (4 wavefronts instead of 16 at VEC = 8)
+#pragma unroll
+                            for (int q2 = 0; q2 < VEC / 2; ++q2) {
+                                const int q = (q2 + lane) & (VEC / 2 - 1);
+                                ulonglong2 v = qv[0];
+#pragma unroll
+                                for (int j = 1; j < VEC / 2; ++j) v = q == j ? qv[j] : v;
+                                dst[q] = v;
+                            }
                         }
                     }
                 }
