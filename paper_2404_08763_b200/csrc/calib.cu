@@ -58,6 +58,7 @@ calib_hist_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint32_t 
     auto classify_in = [&](uint32_t key) {  // key known to lie in [lo, hi]
         ++inwin;
         const uint32_t bin = (key - lo) >> shift;
+        CATS_DCHECK(bin < nbins);
         if (bin == cur_bin) {
             ++cur_cnt;
         } else {
@@ -250,6 +251,7 @@ calib_hist_tma_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint3
         auto classify_in = [&](uint32_t key) {
             ++inwin;
             const uint32_t bin = (key - lo) >> shift;
+            CATS_DCHECK(bin < nbins);
             if (regbins) {
 #pragma unroll
                 for (int j = 0; j < kCalRegBins; ++j) rc[j] += bin == (uint32_t)j ? 1u : 0u;

@@ -12,6 +12,24 @@
 #error "libcats is written for sm_100a (B200) only"
 #endif
 
+// Debug build (python -m paper_2404_08763_b200.build --debug -> libcats_debug.so): device-side bounds and
+// invariant checks that trap on failure -- the pool's stand-in for compute-sanitizer, which is closed here.
+#ifdef CATS_DEBUG_CHECKS
+#include <cstdio>
+#define CATS_DCHECK(cond)                                                                                   \
+    do {                                                                                                    \
+        if (!(cond)) {                                                                                      \
+            printf("CATS_DCHECK failed %s:%d: %s (block %d, thread %d)\n", __FILE__, __LINE__, #cond,       \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                      \
+            __trap();                                                                                       \
+        }                                                                                                   \
+    } while (0)
+#else
+#define CATS_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 namespace cats {
 
 using bf16_bits = uint16_t;  // bfloat16 stored as its bit pattern

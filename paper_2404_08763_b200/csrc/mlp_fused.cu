@@ -172,9 +172,11 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     mbar_arrive_expect_tx(&full[s], nrows * row_bytes);
                 }
                 __syncwarp();
+                CATS_DCHECK(q_tail - q_head <= QCAP);
                 if (has) {  // one bulk copy per lane: row (lane & 1) of neuron lane >> 1
                     const int i = lane >> 1;
                     const size_t j = (size_t)Q.id[i];
+                    CATS_DCHECK(j < (size_t)m && (size_t)(lane + 1) * row_bytes <= stage_bytes);
                     bulk_g2s(dst + (size_t)lane * row_bytes, ((lane & 1) ? Wd : Wu) + j * d, row_bytes, &full[s],
                              policy);
                 }
@@ -190,6 +192,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     }
                     const int base = (int)tile * NU;
                     const int qn = min(NU, (int)sched_list_n - base);
+                    CATS_DCHECK(qn >= 1 && sched_list_n <= (unsigned)m);
                     if (lane < qn) {
                         D.id[lane] = __ldcg(gidx + base + lane);
 #pragma unroll
@@ -228,6 +231,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 if (tile < (unsigned)ntiles) {  // GATE job: a new tile of W_gate rows
                     const int r0 = tile_r0((int)tile);
                     const int nr = tile_rows((int)tile, r0);
+                    CATS_DCHECK(r0 >= 0 && nr >= 1 && r0 + nr <= m && (uint32_t)nr * row_bytes <= stage_bytes);
                     if (from_static) {
                         ++snext;
                     } else if (lane == 0) {
@@ -367,12 +371,14 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 }
                 if (act) {
                     const int pos = r0 + rank;
+                    CATS_DCHECK(pos < m && rank < n);
                     idx[pos] = r0 + lane;
                     tokmask[pos] = (uint8_t)bits;
 #pragma unroll
                     for (int tk = 0; tk < B; ++tk) vals[(size_t)pos * B + tk] = ((bits >> tk) & 1u) ? vrow[tk] : 0.0f;
                     if (mode == kModeAtomicGate) {  // App. D Alg. 1 line 4: append (j, v_j) to the global idcs
                         const unsigned int ap = atomicAdd(&sched[3], 1u);
+                        CATS_DCHECK(ap < (unsigned)m);
                         gidx[ap] = r0 + lane;
 #pragma unroll
                         for (int tk = 0; tk < B; ++tk) gval[(size_t)ap * B + tk] = ((bits >> tk) & 1u) ? vrow[tk] : 0.0f;

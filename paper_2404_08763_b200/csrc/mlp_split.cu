@@ -573,6 +573,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     const long long U = pre[ntiles];
     auto wcum = [R](long long r) { return r * (4LL * R + 1) - r * (r - 1) / 2; };  // sum_{i<r} (4R - i)
     const int lo = (int)(U * wcum(rr) / wcum(R)), hi = (int)(U * wcum(rr + 1) / wcum(R)), len = hi - lo;
+    CATS_DCHECK(rr < R && 0 <= lo && lo <= hi && hi <= U && len <= maxr);
 
     // ---- this range's neurons: compact rank g -> (tile, k) by binary search; neuron = k-th set row ----
     for (int i = tid; i < len; i += nth) {
@@ -587,6 +588,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
         for (int j = 0; j < k; ++j) msk &= msk - 1u;  // drop the k lowest set rows
         lj[i] = a * nr_tile + (__ffs(msk) - 1);
         lpos[i] = a * nr_tile + k;
+        CATS_DCHECK(msk != 0u && k < nr_tile);
     }
     __syncthreads();
     trace_stamp(trace, 1, 1);

@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(kTpThreads) tp_allreduce_kernel(const __grid_c
     // slice of this CTA (16-byte aligned boundaries: n is a multiple of 4)
     const unsigned long long n4 = L.n / 4;
     const unsigned long long s0 = n4 * c / L.ctas, s1 = n4 * (c + 1) / L.ctas;
+    CATS_DCHECK(lr < L.nlocal && me < W && s1 <= n4 && L.n <= L.slot_floats);
     __shared__ unsigned int s_ep;
     pdl_launch_dependents();  // the next layer's decode may start streaming its static W_gate tiles
     pdl_wait_primary();       // x (and this CTA's epoch word) may come from the kernels launched before us

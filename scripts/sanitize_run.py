@@ -1,12 +1,17 @@
-"""Small-shape workload for compute-sanitizer (memcheck / racecheck / synccheck): every kernel family once.
+"""Small-shape workload touching every kernel family once, for checking runs: compute-sanitizer where the
+pool allows it (closed on this pool), and the debug library's device-side bounds checks:
 
-    compute-sanitizer --tool memcheck python scripts/sanitize_run.py
+    python -m paper_2404_08763_b200.build --debug && python scripts/sanitize_run.py --debug
 """
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+
+if "--debug" in sys.argv:  # load libcats_debug.so (CATS_DCHECK compiled in) instead of libcats.so
+    from paper_2404_08763_b200 import _lib
+    _lib.LIB_PATH = _lib.LIB_PATH.replace("libcats.so", "libcats_debug.so")
 
 import cats_synth
 import paper_2404_08763_b200 as cats
@@ -52,3 +57,4 @@ for _ in range(3):
     em.allreduce([torch.randn(2048, device=dev) for _ in range(4)])
 torch.cuda.synchronize()
 print("tp ok", flush=True)
+print("library:", cats.library_path(), flush=True)
