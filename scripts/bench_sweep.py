@@ -27,6 +27,7 @@ import paper_2404_08763_b200 as cats
 ap = argparse.ArgumentParser()
 ap.add_argument("--quick", action="store_true")
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--only", default="", help="comma-separated config prefixes to run (C0,C1,C2,N3,C3)")
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 torch.cuda.set_device(dev)
@@ -63,6 +64,10 @@ def calibrate(plan, ws, Wg, d, k, dtype, ntok=256, seed=0, heavy=False):
 
 def emit(**kw):
     print(json.dumps(kw), flush=True)
+
+
+def want(name):
+    return not a.only or any(name.startswith(p) for p in a.only.split(","))
 
 
 _STACKS = {}
@@ -132,30 +137,39 @@ def run_layers(name, d, m, layers, copies, b, k, heavy, dtype=torch.bfloat16, de
 
 
 def run_chained(name, d, m, layers, b, k, heavy=False, dtype=torch.bfloat16):
-    """N3 decode-loop proxy with real layer-to-layer dynamics: layer l's output feeds layer l + 1 through a
-    residual connection, x_{l+1} = bf16(x_l + y_l) (torch's in-place add: plumbing between the layers), and
-    each layer's t is calibrated on 256 calibration tokens that went through the same chain. Timed as one
-    CUDA graph of the whole stack (decode + residual add per layer) / layers."""
+    """N3 decode-loop proxy with real layer-to-layer dynamics: layer l's output feeds layer l + 1 the way a
+    pre-norm transformer block does, h_l = RMSNorm(x_l) (unit gain), x_{l+1} = bf16(x_l + MLP_l(h_l)) (torch
+    ops between the layers: plumbing, not the hot path; attention is not modelled), and each layer's t is
+    calibrated on 256 calibration tokens that went through the same chain. Timed as one CUDA graph of the
+    whole stack (norm + decode + residual add per layer) / layers."""
     plan = cats.MlpPlan(d, m, max_batch=8, dtype=dtype)
     ws = plan.workspace()
     Ws = weights(d, m, layers, 1, heavy, dtype)
+    def rmsnorm(v, out):
+        vf = v.float()
+        out.copy_(vf * torch.rsqrt(vf.pow(2).mean(-1, keepdim=True) + 1e-6))
+
     xc = cats_synth.tokens(256, d, dtype, seed=100, heavy=heavy).to(dev)
+    hc = torch.empty_like(xc)
     yc = torch.empty(8, d, device=dev)
     ts = []
     for l in range(layers):
-        acts = torch.cat([cats.cats_mlp_gate_act(plan, xc[i:i + 8], Ws[l][0], ws=ws) for i in range(0, 256, 8)])
+        rmsnorm(xc, hc)
+        acts = torch.cat([cats.cats_mlp_gate_act(plan, hc[i:i + 8], Ws[l][0], ws=ws) for i in range(0, 256, 8)])
         ts.append(cats.cats_calibrate_threshold(acts, k)[0] if k > 0 else 0.0)
         for i in range(0, 256, 8):
-            cats.cats_mlp_decode(plan, xc[i:i + 8], *Ws[l], ts[l], y=yc, ws=ws)
+            cats.cats_mlp_decode(plan, hc[i:i + 8], *Ws[l], ts[l], y=yc, ws=ws)
             xc[i:i + 8].add_(yc)
     x0 = cats_synth.tokens(b, d, dtype, seed=1, heavy=heavy).to(dev)
     x = x0.clone()
+    h = torch.empty_like(x)
     y = torch.empty(b, d, device=dev)
 
     def fn():
         x.copy_(x0)
         for W, t in zip(Ws[:layers], ts):
-            cats.cats_mlp_decode(plan, x, W[0], W[1], W[2], t, y=y, ws=ws)
+            rmsnorm(x, h)
+            cats.cats_mlp_decode(plan, h, W[0], W[1], W[2], t, y=y, ws=ws)
             x.add_(y)
 
     us = graph_time(fn, a.reps) / layers
@@ -163,7 +177,8 @@ def run_chained(name, d, m, layers, b, k, heavy=False, dtype=torch.bfloat16):
     x.copy_(x0)
     unions, spars = [], []
     for W, t in zip(Ws[:layers], ts):
-        cats.cats_mlp_decode(plan, x, W[0], W[1], W[2], t, y=y, ws=ws)
+        rmsnorm(x, h)
+        cats.cats_mlp_decode(plan, h, W[0], W[1], W[2], t, y=y, ws=ws)
         idx, tm, per = cats.cats_mlp_last_active(plan, ws, b)
         unions.append(len(idx) / m)
         spars.append(1 - float(per.mean()) / m)
@@ -175,18 +190,20 @@ def run_chained(name, d, m, layers, b, k, heavy=False, dtype=torch.bfloat16):
          t_first=ts[0], t_last=ts[-1])
 
 
-run_layers("C0-toy", 64, 176, 1, 1, 1, 0.5, False, dtype=torch.float32, dense_too=True)
-run_layers("C1-mistral-7b", 4096, 14336, 1, 4, 1, 0.5, False, dense_too=True)
+if want("C0"):
+    run_layers("C0-toy", 64, 176, 1, 1, 1, 0.5, False, dtype=torch.float32, dense_too=True)
+if want("C1"):
+    run_layers("C1-mistral-7b", 4096, 14336, 1, 4, 1, 0.5, False, dense_too=True)
 bs = [1, 8] if a.quick else [1, 2, 4, 8]
 ks = [0.5, 0.9] if a.quick else [0.5, 0.7, 0.9]
-for heavy in ([False] if a.quick else [False, True]):
+for heavy in ([False] if a.quick else [False, True]) if want("C2") else []:
     for k in ks:
         for b in bs:
             run_layers("C2-llama2-7b-32L", 4096, 11008, 32, 1, b, k, heavy, dense_too=(k == 0.5 and not heavy))
-for b in ([1] if a.quick else [1, 8]):
+for b in ([1] if a.quick else [1, 8]) if want("N3") else []:
     for k in ([0.5] if a.quick else [0.5, 0.7, 0.9]):
         run_chained("N3-llama2-7b-32L-chained", 4096, 11008, 32, b, k)
-for P in [1, 2, 4, 8]:
+for P in [1, 2, 4, 8] if want("C3") else []:
     for b in (1, 8):
         run_layers(f"C3-llama2-13b-TP{P}-shard", 5120, 13824 // P, 1, 4 * P if P > 1 else 4, b, 0.5, False,
                    dense_too=True, optimal=(b == 1))
