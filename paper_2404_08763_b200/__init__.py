@@ -217,11 +217,15 @@ class XsparsePlan(MlpPlan):
 
 
 def _check_tensor(t: torch.Tensor, name: str, shape, dtype, device):
-    if tuple(t.shape) != tuple(shape):
+    # cheap checks first (this runs on every call: ~1 us per tensor matters for the e2e path)
+    if t.shape != shape:
         raise ValueError(f"{name}: shape {tuple(t.shape)} != {tuple(shape)}")
-    if t.dtype != dtype:
+    if t.dtype is not dtype:
         raise TypeError(f"{name}: dtype {t.dtype} != {dtype}")
-    if t.device != device:
+    if device.type == "cpu":
+        if t.is_cuda:
+            raise ValueError(f"{name}: on {t.device}, expected cpu")
+    elif not t.is_cuda or t.get_device() != device.index:
         raise ValueError(f"{name}: on {t.device}, expected {device}")
 
 

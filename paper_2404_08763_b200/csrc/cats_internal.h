@@ -66,9 +66,16 @@ struct PlanData {
     size_t off_gidx, off_gval;  // App. D Alg. 1 mode: the global idcs list (ids, v per token), arbitrary order
 };
 
+int split_ka_stages_nr(const PlanData &p, int b, int nr);  // mlp_split.cu
+
 // K12 tile height NR (W_gate rows per GATE job; a UD job carries NR/2 neurons = the same bytes).
+// The split path (KA, KB) shares the tile geometry at b >= 2.
 inline int k12_rows_per_tile(const PlanData &p, int b) {
     if (p.nr_force == 2 || p.nr_force == 4 || (p.nr_force == 6 && b == 1)) return p.nr_force;  // options
+    // b >= 2: 2-row tiles where x [b][d] staged in KA's shared memory leaves < 2 stages of 4-row tiles per
+    // job stream (Llama2-13B d = 5120 from b = 6) -- otherwise the planner would fall back to K12, whose
+    // x and y partials do not fit in registers there (measured 3.5 ms per step at b = 8)
+    if (b >= 2 && split_ka_stages_nr(p, b, 4) < 2) return 2;
     // 4-row tiles whenever two 4-row stages fit (measured at d = 5120, b = 1: 4 rows x 2 stages beats
     // 2 rows x 5 stages, 55.6 vs 60.6 us; per-job costs are per row pair)
     const size_t row = (size_t)p.d * p.esize;

@@ -816,6 +816,19 @@ int split_ka_ks(const PlanData &p, int b) { return (p.esize == 2 && b >= kSplitM
 // KA shared memory: x [b][d] (FHFMA path only), then per group (kSplitAGroups): the ring of padded
 // rows, 2 mbarriers, a descriptor and the warp partial sums per stage, and the FIFO. `stages` counts
 // stages per group.
+static size_t split_ka_per_stage_nr(const PlanData &p, int b, int nr) {
+    const size_t desc = (3 + 2 * (size_t)nr + (size_t)nr * b) * 4;  // sizeof(SplitDesc<nr, b>)
+    return (size_t)nr * ((size_t)p.d * p.esize + 16) + 16 + desc +
+           (size_t)(kSplitAWarps / kSplitAGroups) * pow2_ceil(nr * b) * 4;
+}
+// KA ring stages per group with tiles of nr rows (used by k12_rows_per_tile to pick nr at b >= 2)
+int split_ka_stages_nr(const PlanData &p, int b, int nr) {
+    const size_t ent = (2 + (size_t)b) * 4;
+    const size_t xs = (size_t)b * ((size_t)p.d * p.esize + ((p.esize == 2 && b >= kSplitMmaMinB) ? 16 : 0));
+    const size_t fixed = xs + kSplitAGroups * kSplitFifo * ent;
+    if (fixed >= kSmemBudget) return 0;
+    return (int)std::min<size_t>((kSmemBudget - fixed) / (kSplitAGroups * split_ka_per_stage_nr(p, b, nr)), kMaxStages);
+}
 static size_t split_ka_per_stage(const PlanData &p, int b) {
     const int nr = k12_rows_per_tile(p, b);
     const size_t desc = (3 + 2 * (size_t)nr + (size_t)nr * b) * 4;  // sizeof(SplitDesc<nr, b>)

@@ -173,6 +173,14 @@ def run_chained(name, d, m, layers, b, k, heavy=False, dtype=torch.bfloat16):
             x.add_(y)
 
     us = graph_time(fn, a.reps) / layers
+
+    def fn_plumbing():  # the same graph without the decodes: norm + residual add only
+        x.copy_(x0)
+        for _ in range(layers):
+            rmsnorm(x, h)
+            x.add_(y)
+
+    us_plumb = graph_time(fn_plumbing, a.reps) / layers
     # realised activity per layer along the chain (eager pass)
     x.copy_(x0)
     unions, spars = [], []
@@ -185,6 +193,7 @@ def run_chained(name, d, m, layers, b, k, heavy=False, dtype=torch.bfloat16):
         x.add_(y)
     emit(config=name, d=d, m=m, b=b, k=k, heavy=heavy, layers=layers, chained=True,
          us_per_token_layer=round(us / b, 3), us_per_step=round(us, 3),
+         us_plumbing_per_layer=round(us_plumb, 3), us_decode_per_token_layer=round((us - us_plumb) / b, 3),
          union_frac_mean=round(sum(unions) / layers, 4), union_frac_min=round(min(unions), 4),
          union_frac_max=round(max(unions), 4), per_token_sparsity_mean=round(sum(spars) / layers, 4),
          t_first=ts[0], t_last=ts[-1])

@@ -64,6 +64,8 @@ def test_plan_without_gpu():
     assert toy.info["grid"] == 176 // 4 // 2         # small layers: >= 2 tiles per CTA
     small = cats.MlpPlan(64, 5, max_batch=8, dtype=torch.float32, num_sms=148)
     assert small.info["grid"] == 1                  # 2 tiles (m = 5): one CTA
+    p13 = cats.MlpPlan(5120, 13824, max_batch=8, num_sms=148)   # Llama2-13B: KA + KB at every batch size
+    assert [cats.cats_mlp_kernels_per_call(p13, b) for b in range(1, 9)] == [2] * 8
     for b in range(1, 9):                            # every batch size fits the shared-memory budget
         i = cats.MlpPlan(5120, 13824, max_batch=b, num_sms=148).info
         per_sm = 2 if b == 1 else 1

@@ -152,8 +152,8 @@ def test_parity_every_planned_batch(model, b):
     d, m = cats_synth.MODELS[model]
     k = {2: 0.5, 3: 0.7, 4: 0.5, 5: 0.9, 6: 0.7, 7: 0.5, 8: 0.5}[b]
     res, _ = run_parity(d, m, b, torch.bfloat16, k, seed=50 + b, heavy=(b % 2 == 1))
-    # the split path KA + KB wherever its shared memory fits (Llama2-13B d = 5120 from b = 6: K12)
-    assert res["kernels"] == (1 if (d == 5120 and b >= 6) else 2)
+    # the split path KA + KB (Llama2-13B d = 5120 from b = 6: 2-row tiles so that KA's ring fits)
+    assert res["kernels"] == 2
 
 
 @pytest.mark.parametrize("model,b", [("mistral-7b", 2), ("llama2-7b", 5), ("llama2-13b", 8)])
@@ -170,8 +170,8 @@ def test_parity_llama13b_tp_shard(P, b):
     """BASELINE config 3: the per-GPU shard m / P of Llama2-13B (the decode of one rank, b = 1 and 8)."""
     d, m = cats_synth.MODELS["llama2-13b"]
     res, _ = run_parity(d, m // P, b, torch.bfloat16, 0.5, seed=70 + P)
-    # d = 5120: KA + KB from b = 1 (planner, DESIGN.md §5.2); b = 8: K12 (KA + KB shared memory does not fit)
-    assert res["kernels"] == (2 if b == 1 else 1)
+    # d = 5120: KA + KB from b = 1 (planner, DESIGN.md §5.2); b = 8 with 2-row tiles
+    assert res["kernels"] == 2
 
 
 @pytest.mark.parametrize("comp", ["predicated", "atomic"])
