@@ -319,7 +319,8 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
     if (o.lazy_tail < 0 || o.min_tiles < 1 || o.l2_prefetch < 0 || o.max_stages < 0 || o.max_stages == 1 ||
         (o.rows_per_tile != 0 && o.rows_per_tile != 2 && o.rows_per_tile != 4 && o.rows_per_tile != 6) ||
         o.xs_cols < 0 || o.xs_ranges < 0 || o.xs_ranges > 8 || o.tail_rows < 0 ||
-        o.tail_rows > 6 || o.tail_tiles < 0 || o.tail_fused < 0 || o.tail_fused > 1)
+        o.tail_rows > 6 || o.tail_tiles < 0 || o.tail_fused < 0 || o.tail_fused > 1 || o.ud_pool < 0 ||
+        o.ud_pool > 1)
         return CATS_E_SHAPE;
     if (d <= 0 || m <= 0) return CATS_E_SHAPE;
     if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
@@ -347,6 +348,7 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.tail_rows = o.tail_rows;
         p.tail_tiles = o.tail_tiles;
         p.tail_fused = o.tail_fused;
+        p.ud_pool = o.ud_pool;
         p.trace = o.trace != 0;
         p.kind = kind;
         p.g1 = 0;
@@ -448,6 +450,13 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         const bool atomic_list = p.compaction == CATS_COMPACT_ATOMIC;  // App. D Alg. 1: global idcs list
         p.off_gidx = off;    off = align_up(off + (atomic_list ? (size_t)m * 4 : 0), 256);
         p.off_gval = off;    off = align_up(off + (atomic_list ? (size_t)m * max_batch * 4 : 0), 256);
+        size_t pool_bytes = 0;  // K12 UD pool: 2 slots per tile, (1 + NU + NU b) epoch-tagged words per slot
+        if (p.ud_pool)
+            for (int b = 1; b <= max_batch; ++b) {
+                const size_t nu = (size_t)k12_rows_per_tile(p, b) / 2;
+                pool_bytes = std::max(pool_bytes, (size_t)2 * k12_ntiles_geo(p, b) * (1 + nu + nu * b) * 8);
+            }
+        p.off_pool = off;    off = align_up(off + pool_bytes, 256);
         p.k12_min_tiles = o.min_tiles;
         p.k12_l2pf = o.l2_prefetch;  // measured: prefetching only slows the drain (default 0)
         p.k12_eager = o.eager;
@@ -560,6 +569,9 @@ extern "C" cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, vo
                             static_cast<cudaStream_t>(s));
     if (e == cudaSuccess)
         e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_tmask, 0, (size_t)((plan->p.m + 1) / 2) * 4,
+                            static_cast<cudaStream_t>(s));
+    if (e == cudaSuccess && plan->p.ud_pool)  // pool words carry epochs: zero = never published
+        e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_pool, 0, plan->p.off_trace - plan->p.off_pool,
                             static_cast<cudaStream_t>(s));
     return cuda_status(e);
 }

@@ -80,6 +80,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
              unsigned long long *__restrict__ yacc, float *__restrict__ y, unsigned int *__restrict__ sched,
              int32_t *__restrict__ gidx, float *__restrict__ gval, int t1, int ns, int tail_fused,
+             unsigned long long *__restrict__ pool, int ud_pool,
              int lazy_tail, int eager, int l2pf, unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
@@ -105,6 +106,13 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     const bool list_mode = mode == kModeAtomicList;  // App. D Alg. 1, launch 2: work units = chunks of idcs
     const bool has_y = mode != kModeGateOnly && mode != kModeAtomicGate;
     constexpr int NG = NR / 3 > 0 ? NR / 3 : 1;  // rows of a fused tail tile (GUD job)
+    // UD pool (options.ud_pool): every CTA first streams GATE tiles; each retired tile publishes its <= 2 UD
+    // jobs into fixed slots 2 tile + h of a grid-wide pool (epoch-tagged 8-byte words: no fences); once the
+    // tiles are exhausted, CTAs claim pool slots in order from a counter -- the up/down work of the whole
+    // layer is balanced dynamically across the grid and no CTA ends on its own last tile's dependency chain
+    constexpr int PW = 1 + NU + NU * B;          // pool words per slot: (n), (id_i), (v_i,tk), each with the epoch
+    static_assert(PW <= 32, "one pool word per lane");
+    const bool pooled = ud_pool && (mode == kModeCats || mode == kModeDense);
     const bool gud_tail = tail_fused && NR >= 3 && ns <= NG && (mode == kModeCats || mode == kModeDense);
 
     extern __shared__ __align__(128) unsigned char smem[];
@@ -140,6 +148,9 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         // drain (balanced tail), and small layers spread over all CTAs.
         unsigned int t_res = kNoTile;  // raw counter value; tile id = dyn_base + counter
         unsigned int sched_list_n = 0; // list mode: length of the global idcs list
+        unsigned int pool_slot = kNoTile;  // pool mode: the next claimed slot (lane 0; async claim)
+        unsigned int pool_ep = 0;          // pool mode: this call's epoch (sched[7] + 1)
+        bool gates_exhausted = false;
         // static first tiles per CTA: `stages` of them go straight into the ring, up to l2pf more are
         // prefetched into L2 (cp.async.bulk.prefetch) -- both before griddepcontrol.wait, so they use
         // the HBM time while the previous kernel drains -- and taken in order before any claim
@@ -157,11 +168,65 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         unsigned long long p_wait = 0, p_busy = 0, p_issue = 0, t_last_gate = 0;  // diagnostics (CATS_TRACE)
 
         // issue job `prod` into its stage; returns false if nothing can be issued yet
+        // pool mode, after the GATE tiles are exhausted: the next claimed pool slot as a UD job.
+        // 1 = issued, 0 = nothing issuable yet (slot not published), 2 = END issued
+        auto issue_pool = [&](Desc &D, unsigned char *dst, int s) -> int {
+            for (;;) {
+                unsigned int slot = pool_slot;
+                if (lane == 0 && slot == kNoTile) slot = atomicAdd(&sched[4], 1u);
+                slot = __shfl_sync(0xffffffffu, slot, 0);
+                if (lane == 0) pool_slot = slot;
+                if (slot >= 2u * (unsigned)ntiles) {  // every slot claimed: end once no GATE job can publish
+                    if (gates_inflight != 0) return 0;
+                    if (lane == 0) {
+                        D.type = kJobEnd;
+                        D.n = 0;
+                        mbar_arrive_expect_tx(&full[s], 0u);
+                    }
+                    ended = true;
+                    return 2;
+                }
+                unsigned long long w = 0ull;
+                if (lane < PW)
+                    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(pool + (size_t)slot * PW + lane) : "memory");
+                // word 0 (the slot's neuron count) first, then the words of its qn neurons; all epoch-tagged
+                const bool fresh0 = __shfl_sync(0xffffffffu, (unsigned int)(w >> 32), 0) == pool_ep;
+                const int qn = (int)__shfl_sync(0xffffffffu, (unsigned int)w, 0);
+                const int wi = lane - 1 - NU;  // v word index (neuron wi / B, token wi % B)
+                const bool used = (lane >= 1 && lane <= NU) ? lane - 1 < qn : (lane > NU && lane < PW) ? wi / B < qn : false;
+                const bool fresh = !used || (unsigned int)(w >> 32) == pool_ep;
+                if (!fresh0 || !__all_sync(0xffffffffu, fresh)) return 0;  // not published yet: retry later
+                if (lane == 0) {
+                    pool_slot = kNoTile;
+                    claim_tile_async(pool_slot, sched + 4, true);  // the next slot, claimed ahead
+                }
+                if (qn == 0) continue;  // an empty slot (tile with <= NU active neurons): take the next
+                if (lane >= 1 && lane <= NU) D.id[lane - 1] = used ? (int)(unsigned int)w : 0;
+                if (lane > NU && lane < PW) D.v[wi / B][wi % B] = used ? __uint_as_float((unsigned int)w) : 0.0f;
+                __syncwarp();
+                if (lane == 0) {
+                    D.type = kJobUD;
+                    D.tile = (int)(slot >> 1);
+                    D.n = qn;
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)qn * 2u * row_bytes);
+                }
+                __syncwarp();
+                if (lane < 2 * qn) {
+                    const size_t j = (size_t)D.id[lane >> 1];
+                    CATS_DCHECK(j < (size_t)m);
+                    bulk_g2s(dst + (size_t)lane * row_bytes, ((lane & 1) ? Wd : Wu) + j * d, row_bytes, &full[s], policy);
+                }
+                return 1;
+            }
+        };
+
         auto issue_job = [&]() -> bool {
             const int s = ps;
             Desc &D = desc[s];
             unsigned char *dst = ring + (size_t)s * stage_bytes;
-            if (q_head != q_tail) {  // UD job: W_up and W_down rows of <= NU active neurons
+            if (pooled && gates_exhausted) {
+                if (issue_pool(D, dst, s) == 0) return false;
+            } else if (q_head != q_tail) {  // UD job: W_up and W_down rows of <= NU active neurons
                 const Desc &Q = queue[q_head % QCAP];
                 const int qn = Q.n;
                 // a negative id marks a row whose load Mask predicates off (Alg. 2 mode): no copy, read as 0
@@ -262,6 +327,14 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     if (trace) t_last_gate = gtimer();
                 } else {
                     if (lane == 0) t_res = tile - dyn_base;  // past the end: keep it, no further claims
+                    if (pooled) {  // GATE tiles exhausted: from now on, UD jobs from the pool
+                        gates_exhausted = true;
+                        if (issue_pool(D, dst, s) == 0) return false;
+                        __syncwarp();
+                        ++prod;
+                        if (++ps == stages) ps = 0;
+                        return true;
+                    }
                     if (gates_inflight != 0) return false;  // an in-flight GATE job may add UD work
                     // no tiles left and nothing in flight can create UD work: end the ring
                     if (lane == 0) {
@@ -310,6 +383,11 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             ntl = (int)((sched_list_n + NU - 1) / NU);
         }
         if (lane == 0) claim_tile_async(t_res, sched, dyn_base + (unsigned)lazy_tail < (unsigned)ntl);
+        if (pooled) {
+            unsigned int e = 0;
+            if (lane == 0) e = *reinterpret_cast<volatile unsigned int *>(sched + 7) + 1u;
+            pool_ep = __shfl_sync(0xffffffffu, e, 0);
+        }
         prod = __shfl_sync(0xffffffffu, prod, 0);
         ps = prod % stages;
         gates_inflight = prod;
@@ -324,6 +402,10 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         int rs = 0;                  // = retire % stages
         uint32_t rphase = 0;         // = (retire / stages) & 1
         while (!ended) {
+            if (retire == prod) {  // nothing in flight (pool mode, waiting for a slot to be published): poll
+                if (!issue_job()) __nanosleep(64);
+                continue;
+            }
             // ---- retire job `retire` in order ----
             const unsigned long long tw0 = trace ? gtimer() : 0ull;
             mbar_wait(&empty[rs], rphase);
@@ -383,7 +465,19 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
 #pragma unroll
                         for (int tk = 0; tk < B; ++tk) gval[(size_t)ap * B + tk] = ((bits >> tk) & 1u) ? vrow[tk] : 0.0f;
                     }
-                    if (!gate_only && !predicated) {  // queue the tile's active neurons, NU per UD job, ascending
+                    if (pooled) {  // publish into slot 2 tile + rank / NU: (id, v) words tagged with the epoch
+                        unsigned long long *ps_ = pool + ((size_t)2 * tile + rank / NU) * PW;
+                        const int i = rank % NU;
+                        const unsigned long long ept = (unsigned long long)pool_ep << 32;
+                        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(ps_ + 1 + i),
+                                     "l"(ept | (unsigned int)(r0 + lane)) : "memory");
+#pragma unroll
+                        for (int tk = 0; tk < B; ++tk) {
+                            const float vv = ((bits >> tk) & 1u) ? vrow[tk] : 0.0f;
+                            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(ps_ + 1 + NU + i * B + tk),
+                                         "l"(ept | __float_as_uint(vv)) : "memory");
+                        }
+                    } else if (!gate_only && !predicated) {  // queue the tile's active neurons, NU per UD job, ascending
                         Desc &Q = queue[(q_tail + rank / NU) % QCAP];
                         const int i = rank % NU;
                         Q.id[i] = r0 + lane;
@@ -397,6 +491,11 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     }
                 }
                 if (lane == 0) cnt[tile] = nact;
+                if (pooled && lane < 2) {  // the slots' neuron counts (0 for an empty slot), published last
+                    const int qn = min(NU, max(0, nact - lane * NU));
+                    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(pool + ((size_t)2 * tile + lane) * PW),
+                                 "l"(((unsigned long long)pool_ep << 32) | (unsigned int)qn) : "memory");
+                }
                 if (predicated) q_tail += (n + NU - 1) / NU;
                 else if (!gate_only) q_tail += (nact + NU - 1) / NU;
                 --gates_inflight;
@@ -424,6 +523,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     } else {
         // ===================================== CONSUMER WARPS ====================================
         pdl_wait_primary();     // x (and the accumulators) may come from the PDL predecessor
+        const unsigned int pool_ep_c = pooled ? *reinterpret_cast<volatile unsigned int *>(sched + 7) + 1u : 0u;
         uint4 xr[B][CPT];  // x, own chunks, packed (bf16 pairs or fp32), 0 past the row end
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
@@ -770,6 +870,10 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 sched[0] = 0u;
                 sched[1] = 0u;
                 if (list_mode) sched[3] = 0u;  // the idcs list was consumed: re-arm the append counter
+                if (pooled) {
+                    sched[4] = 0u;             // pool claims
+                    sched[7] = pool_ep_c;      // the pool's epoch: the next call publishes with epoch + 1
+                }
             }
         }
         trace_stamp(trace, 0, 3);
@@ -816,6 +920,7 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
         reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<unsigned long long *>(w + p.off_ypart), y,
         reinterpret_cast<unsigned int *>(w + p.off_sched), reinterpret_cast<int32_t *>(w + p.off_gidx),
         reinterpret_cast<float *>(w + p.off_gval), k12_t1(p, B), k12_tail_rows(p, B), p.tail_fused,
+        reinterpret_cast<unsigned long long *>(w + p.off_pool), p.ud_pool,
         p.lazy_tail * k12_grid(p, B),
         p.k12_eager, p.k12_l2pf,
         p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
