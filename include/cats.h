@@ -218,6 +218,8 @@ typedef struct {
     int32_t tail_rows;       /* K12 tail tiles: rows per tile for the last tail_tiles x grid tiles (0 = uniform;
                                 2 .. NR-1) -- finer work units where the dynamic schedule ends */
     int32_t tail_tiles;      /* K12 tail tiles per CTA (>= 0) */
+    int32_t convert_ctas;    /* K12: the last convert_ctas CTAs to finish convert the exact accumulator to fp32 y
+                                (a slice each); 0 or 1 = the last CTA alone */
     int32_t ud_pool;         /* 1: K12 streams every GATE tile first; retired tiles publish their up/down jobs to a
                                 grid-wide pool that all CTAs drain (dynamic balancing of the second half) */
     int32_t tail_fused;      /* 1: a tail tile of tail_rows <= NR / 3 rows is one job that loads its W_gate, W_up and

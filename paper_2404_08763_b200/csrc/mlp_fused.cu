@@ -80,7 +80,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
              unsigned long long *__restrict__ yacc, float *__restrict__ y, unsigned int *__restrict__ sched,
              int32_t *__restrict__ gidx, float *__restrict__ gval, int t1, int ns, int tail_fused,
-             unsigned long long *__restrict__ pool, int ud_pool,
+             unsigned long long *__restrict__ pool, int ud_pool, int convert_ctas,
              int lazy_tail, int eager, int l2pf, unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
@@ -185,6 +185,10 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     }
                     ended = true;
                     return 2;
+                }
+                if (gud_tail && (int)(slot >> 1) >= t1) {  // fused tail tiles publish nothing: skip their slots
+                    if (lane == 0) pool_slot = kNoTile;
+                    continue;
                 }
                 unsigned long long w = 0ull;
                 if (lane < PW)
@@ -497,7 +501,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                                  "l"(((unsigned long long)pool_ep << 32) | (unsigned int)qn) : "memory");
                 }
                 if (predicated) q_tail += (n + NU - 1) / NU;
-                else if (!gate_only) q_tail += (nact + NU - 1) / NU;
+                else if (!gate_only && !pooled) q_tail += (nact + NU - 1) / NU;  // pool mode: published, not queued
                 --gates_inflight;
                 __syncwarp();
             }
@@ -841,34 +845,53 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         }
         consumer_barrier<NC>();
         trace_stamp(trace, 0, 4);  // partial reduced into yacc
-        if (tid == 0) s_last = (atomicAdd(&sched[1], 1u) == gridDim.x - 1) ? 1u : 0u;
+        // The last KC CTAs to arrive convert the accumulator (a 1/KC slice each) once every CTA's partial is
+        // in (KC = options.convert_ctas; 1 = the last CTA alone). A converter only waits for CTAs that
+        // have not arrived; the last converter to pass the wait re-arms the counters.
+        __shared__ unsigned int s_ticket, s_reset;
+        if (tid == 0) s_ticket = atomicAdd(&sched[1], 1u);
         consumer_barrier<NC>();
-        if (s_last) {
+        const int G = (int)gridDim.x;
+        const int KC = min(G, max(1, convert_ctas));
+        const int ri = (int)s_ticket - (G - KC);
+        if (ri >= 0) {
+            if (tid == 0) {
+                if (KC > 1) {
+                    unsigned int seen;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(sched + 1) : "memory");
+                    } while (seen < (unsigned)G);
+                }
+                s_reset = (KC == 1 || atomicAdd(&sched[6], 1u) == (unsigned)KC - 1u) ? 1u : 0u;
+            }
+            consumer_barrier<NC>();
             __threadfence();
             if (has_y) {
                 // 8 independent L2 loads in flight per thread (the accumulator was just written by
                 // the bulk-reduce engine of every SM; a serial loop would pay one L2 trip per step)
                 const int n2 = B * d / 2;
-                for (int c0 = 0; c0 < n2; c0 += 8 * NC) {
+                const int cb = (int)((long long)n2 * ri / KC), ce = (int)((long long)n2 * (ri + 1) / KC);
+                for (int c0 = cb; c0 < ce; c0 += 8 * NC) {
                     longlong2 v[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const int c = c0 + u * NC + tid;
-                        v[u] = c < n2 ? __ldcg(reinterpret_cast<const longlong2 *>(yacc) + c) : make_longlong2(0, 0);
+                        v[u] = c < ce ? __ldcg(reinterpret_cast<const longlong2 *>(yacc) + c) : make_longlong2(0, 0);
                     }
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const int c = c0 + u * NC + tid;
-                        if (c < n2) {
+                        if (c < ce) {
                             reinterpret_cast<float2 *>(y)[c] = make_float2(fix_to_float(v[u].x), fix_to_float(v[u].y));
                             reinterpret_cast<longlong2 *>(yacc)[c] = make_longlong2(0, 0);
                         }
                     }
                 }
             }
-            if (tid == 0) {
+            if (tid == 0 && s_reset) {
                 sched[0] = 0u;
                 sched[1] = 0u;
+                sched[6] = 0u;
                 if (list_mode) sched[3] = 0u;  // the idcs list was consumed: re-arm the append counter
                 if (pooled) {
                     sched[4] = 0u;             // pool claims
@@ -920,7 +943,7 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
         reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<unsigned long long *>(w + p.off_ypart), y,
         reinterpret_cast<unsigned int *>(w + p.off_sched), reinterpret_cast<int32_t *>(w + p.off_gidx),
         reinterpret_cast<float *>(w + p.off_gval), k12_t1(p, B), k12_tail_rows(p, B), p.tail_fused,
-        reinterpret_cast<unsigned long long *>(w + p.off_pool), p.ud_pool,
+        reinterpret_cast<unsigned long long *>(w + p.off_pool), p.ud_pool, mode == kModeGateOnly ? 1 : p.convert_ctas,
         p.lazy_tail * k12_grid(p, B),
         p.k12_eager, p.k12_l2pf,
         p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);

@@ -192,7 +192,8 @@ def test_parity_app_d_ablation_modes(comp, model, b, k):
         assert float((y - y2).norm() / y.norm()) < 1e-6
 
 
-@pytest.mark.parametrize("opts", [{"ud_pool": 1}, {"ud_pool": 1, "tail_rows": 2, "tail_tiles": 2},
+@pytest.mark.parametrize("opts", [{"ud_pool": 1}, {"ud_pool": 1, "tail_rows": 2, "tail_tiles": 2}, {"convert_ctas": 8},
+                                  {"ud_pool": 1, "convert_ctas": 16},
                                   {"tail_rows": 2, "tail_tiles": 1},
                                   {"tail_rows": 2, "tail_tiles": 2, "tail_fused": 1},
                                   {"tail_rows": 1, "tail_tiles": 3, "tail_fused": 1, "rows_per_tile": 4}])
