@@ -451,10 +451,10 @@ def main():
         # (PDL lets a launch's static W_gate tiles stream while its predecessor drains)
         dom, dom_bytes, dom_us, iso_us = "K12", step_bytes, step_dev_us, k_first
     else:
-        # KA (W_gate + active W_up rows) dominates; its share of the timed step from the event-bracketed
-        # launches (isolated launches: shares, not absolutes)
-        dom, dom_bytes = "KA", 2 * d * ms + 2 * d * nnz_local + b * d * esz
-        dom_us, iso_us = step_dev_us * k_first / (k_first + k_second), k_first
+        # two launches per step (KA gate + up, KB down + reduction): the roofline of the pair over the whole
+        # step's algorithmic bytes (the step period / the two isolated launches back to back)
+        dom, dom_bytes = "KA+KB", step_bytes
+        dom_us, iso_us = step_dev_us, k_first + k_second
     achieved = dom_bytes / (dom_us * 1e-6) / 1e9
     achieved_iso = dom_bytes / (iso_us * 1e-6) / 1e9
     traffic = None
