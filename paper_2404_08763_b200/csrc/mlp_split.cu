@@ -497,6 +497,11 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
 
     trace_stamp(trace, 1, 0);
     pdl_launch_dependents();
+    // this CTA's arrival ticket for column part q, taken at start: the atomic's round trip overlaps the
+    // mask reads below (KB starts only after the previous decode's KB completed and re-armed the tickets:
+    // KA waits for it before letting KB launch)
+    unsigned int rr_ticket = 0;
+    if (tid == 0) rr_ticket = atomicAdd(&sched[8 + q], 1u);
     if (tid == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
@@ -567,7 +572,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     // (weights 4R - r : 4R - r ... about +-14%) so that late arrivals finish with the early ones. The
     // boundaries are a fixed function of (U, R) and the partials are summed in range order: which CTA
     // computes which range does not change a bit of y.
-    if (tid == 0) s_rr = (int)atomicAdd(&sched[8 + q], 1u);
+    if (tid == 0) s_rr = (int)rr_ticket;
     __syncthreads();
     const int rr = s_rr;
     const long long U = pre[ntiles];
