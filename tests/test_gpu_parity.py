@@ -72,11 +72,16 @@ def check_y(yg, y_ref):
     return max(errs)
 
 
-def run_parity(d, m, b, dtype, k, seed=0, heavy=False, num_sms=0, check=True, opts=None, wd_scale=1.0):
+def run_parity(d, m, b, dtype, k, seed=0, heavy=False, num_sms=0, check=True, opts=None, wd_scale=1.0,
+               x_scale=1.0, same_tokens=False):
     Wg, Wu, Wd = cats_synth.mlp_weights(d, m, dtype, layer=seed, heavy=heavy)
     if wd_scale != 1.0:  # power of two: exact in bf16 / fp32, scales y exactly (mask unchanged)
         Wd = (Wd.float() * wd_scale).to(dtype)
     x = cats_synth.tokens(b, d, dtype, seed=1 + seed, heavy=heavy)
+    if x_scale != 1.0:   # power of two: exact; moves u = x W_gate into SiLU's saturated / linear regions
+        x = (x.float() * x_scale).to(dtype)
+    if same_tokens:      # b copies of one token: identical per-token masks (union = each token's set)
+        x = x[:1].repeat(b, 1).contiguous()
     ox, og, ou, od = (cats_synth.to_oracle(a) for a in (x, Wg, Wu, Wd))
     # threshold: Eq. 3 on the oracle's |SiLU| of these tokens (any t >= 0 is a valid test point)
     zero = np.zeros((m, d), og.dtype)
@@ -208,6 +213,17 @@ def test_parity_k12_tail_geometry(opts, model, b, k):
     assert res["kernels"] == 1
     assert torch.equal(y, cats.cats_mlp_decode(plan, dx, dg, du, dd, res["t"], ws=ws))
     res_small, _ = run_parity(264, 1000, b, torch.bfloat16, k, seed=86, opts={"path": cats.CATS_PATH_FUSED, **opts})
+
+
+@pytest.mark.parametrize("b", [1, 2, 8])
+@pytest.mark.parametrize("case", ["saturated", "tiny", "same_tokens"])
+def test_parity_extreme_inputs(case, b):
+    """x scaled by 2^6 (|u| up to ~10: SiLU's saturated branches, exp(-u) overflowing to inf for very
+    negative u), by 2^-6 (u ~ 5e-3: SiLU's linear region near 0, t tiny), and b identical tokens."""
+    kw = {"saturated": {"x_scale": 64.0}, "tiny": {"x_scale": 1 / 64}, "same_tokens": {"same_tokens": True}}[case]
+    res, _ = run_parity(1024, 3000, b, torch.bfloat16, 0.7, seed=95, **kw)
+    if case == "same_tokens" and b > 1:
+        assert abs(res["nnz_union"] / 3000 - (1 - res["sparsity"])) < 1e-9  # union = every token's set
 
 
 @pytest.mark.parametrize("b", [1, 4])
