@@ -345,8 +345,9 @@ cats_status_t cats_xsparse_gemv(const cats_mlp_plan_t *plan, const void *x, int 
  * neuron). Instead of an NCCL all-reduce, every rank allocates one SYMMETRIC buffer of
  * cats_tp_buffer_bytes (device memory, zero-initialised once), exports it with cats_ipc_handle_get, opens
  * every peer's with cats_ipc_handle_open (CUDA IPC over NVLink / NVSwitch) and builds a comm; then
- * cats_tp_allreduce is ONE launch that pushes this rank's partial into every rank's buffer, flags it, waits
- * for every rank's flags and sums the P partials in fixed rank order 0..P-1: bit-identical y on every rank.
+ * cats_tp_allreduce is ONE launch that pushes this rank's partial into every rank's buffer (each float in an
+ * 8-byte word with the call's epoch: the data is its own flag), waits until every rank's words of its slice
+ * carry the epoch and sums the P partials in fixed rank order 0..P-1: bit-identical y on every rank.
  * Epochs live on the device (graph-capturable); two parity slots make back-to-back calls safe.
  * Requirements: P <= 8; n (floats per call) a multiple of 4 and <= n_max; every rank calls with the same
  * n in the same order; buffers 16-byte aligned. Errors: CATS_E_NULL, CATS_E_SHAPE, CATS_E_ALIGN, CATS_E_CUDA. */

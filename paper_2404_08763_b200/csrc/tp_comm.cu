@@ -8,13 +8,14 @@
 // (App. D); this is the B200 design of that exchange:
 //
 //   * every rank owns a symmetric buffer (same layout on all ranks, mapped into every peer's address
-//     space with CUDA IPC over NVLink): a header of per-CTA epoch counters and flags[src][cta], then two
-//     parity slots of world x n floats;
-//   * ONE launch per call: CTA c takes slice c of the n values, pushes this rank's slice into slot
-//     [epoch & 1][rank] of EVERY rank's buffer (16-byte stores over NVLink, self included), publishes
-//     flags[rank][c] = epoch in every peer (st.release.sys after a system-scope fence), waits until
-//     all world flags of its slice carry the epoch, and sums the slots in fixed rank order 0..P-1 --
-//     the same additions in the same order on every rank, so y is bit-identical across ranks;
+//     space with CUDA IPC over NVLink): per-CTA epoch counters, then two parity slots of world x n
+//     8-byte words (value, epoch);
+//   * ONE launch per call: CTA c takes slice c of the n values and pushes this rank's slice into slot
+//     [epoch & 1][rank] of EVERY rank's buffer, each float in one 8-byte word with the call's epoch
+//     (16-byte stores over NVLink, self included) -- the data is its own flag (no fences, no flag
+//     round trip); every thread then polls its own words of each rank's row until they carry the epoch
+//     and sums them in fixed rank order 0..P-1 -- the same additions in the same order on every rank,
+//     so y is bit-identical across ranks;
 //   * epochs are per CTA and live on the device (CUDA-graph safe); two parity slots make a call's pushes
 //     land in the slot no rank can still be reading (a rank pushes call e+1 only after its call e saw
 //     every rank's call-e data, i.e. after every rank finished call e-1).
@@ -34,7 +35,7 @@ namespace cats {
 constexpr int kTpMaxWorld = 8;
 constexpr int kTpThreads = 256;
 constexpr int kTpMaxCtas = 64;
-constexpr size_t kTpHeaderBytes = (size_t)(1 + kTpMaxWorld) * kTpMaxCtas * 4;  // ep[C] + flags[W][C], u32
+constexpr size_t kTpHeaderBytes = 256;  // per-CTA epochs ep[kTpMaxCtas], u32
 
 struct TpLaunch {
     int world, ctas, nlocal, rank0;       // nlocal ranks handled by this launch: rank0 .. rank0 + nlocal - 1
@@ -44,15 +45,22 @@ struct TpLaunch {
     float *y[kTpMaxWorld];                // [local rank] output
 };
 
-__device__ __forceinline__ void st_release_sys(unsigned int *p, unsigned int v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+
+__device__ __forceinline__ void st_volatile_v4(uint4 *p, const uint4 &v) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
 }
-__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int *p) {
-    unsigned int v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ uint4 ld_volatile_v4(const uint4 *p) {
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p) : "memory");
     return v;
 }
 
+// Low-latency protocol: every pushed float travels with the call's epoch in the same 8-byte word
+// (value bits, epoch), so a reader accepts a value exactly when its word carries the epoch -- no flags,
+// no fences, no barrier between the push and the wait (each thread waits for its own words only).
+// 8-byte words are written and read whole, so a word is either entirely this call's or stale.
 __global__ void __launch_bounds__(kTpThreads) tp_allreduce_kernel(const __grid_constant__ TpLaunch L) {
     const int lr = blockIdx.x / L.ctas, c = blockIdx.x % L.ctas;  // local rank, slice
     const int me = L.rank0 + lr, W = L.world;
@@ -68,39 +76,44 @@ __global__ void __launch_bounds__(kTpThreads) tp_allreduce_kernel(const __grid_c
     if (threadIdx.x == 0) s_ep = own_hdr[c] + 1u;  // this CTA's epoch (only CTA c of this rank writes ep[c])
     __syncthreads();
     const unsigned int ep = s_ep;
-    const size_t slot_off = kTpHeaderBytes + (size_t)(ep & 1u) * W * L.slot_floats * 4;
+    if (threadIdx.x == 0) own_hdr[c] = ep;
+    // slots: [parity][rank][slot_floats] of (value, epoch) 8-byte words
+    const size_t slot_words = (size_t)L.slot_floats;
+    const size_t slot_off = kTpHeaderBytes + (size_t)(ep & 1u) * W * slot_words * 8;
     // push: this rank's slice into slot [ep & 1][me] of every rank (NVLink stores; self is local)
     const float4 *x4 = reinterpret_cast<const float4 *>(L.x[lr]);
-    for (int r = 0; r < W; ++r) {
-        float4 *dst = reinterpret_cast<float4 *>(bufs[r] + slot_off + (size_t)me * L.slot_floats * 4);
-        for (unsigned long long i = s0 + threadIdx.x; i < s1; i += blockDim.x) dst[i] = __ldcg(x4 + i);
-    }
-    __syncthreads();
-    if (threadIdx.x < W) {
-        __threadfence_system();  // the slice stores (every thread's, ordered by the barrier) before the flag
-        unsigned int *hdr = reinterpret_cast<unsigned int *>(bufs[threadIdx.x]);
-        st_release_sys(hdr + (size_t)(1 + me) * kTpMaxCtas + c, ep);
-    }
-    // wait for every rank's slice c of this epoch
-    if (threadIdx.x < W) {
-        const unsigned int *f = own_hdr + (size_t)(1 + threadIdx.x) * kTpMaxCtas + c;
-        while ((int)(ld_acquire_sys(f) - ep) < 0) {
+    for (unsigned long long i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+        const float4 v = __ldcg(x4 + i);
+        const uint4 lo = make_uint4(__float_as_uint(v.x), ep, __float_as_uint(v.y), ep);
+        const uint4 hi = make_uint4(__float_as_uint(v.z), ep, __float_as_uint(v.w), ep);
+        for (int r = 0; r < W; ++r) {
+            uint4 *dst = reinterpret_cast<uint4 *>(bufs[r] + slot_off + (size_t)me * slot_words * 8) + 2 * i;
+            st_volatile_v4(dst, lo);
+            st_volatile_v4(dst + 1, hi);
         }
     }
-    __syncthreads();
-    // y = sum over ranks in fixed order 0..W-1 (identical on every rank)
-    const float4 *slots = reinterpret_cast<const float4 *>(bufs[me] + slot_off);
+    // y = sum over ranks in fixed order 0..W-1 (identical on every rank), each word once it carries the epoch
+    const uint4 *slots = reinterpret_cast<const uint4 *>(bufs[me] + slot_off);
     float4 *y4 = reinterpret_cast<float4 *>(L.y[lr]);
-    const unsigned long long stride4 = L.slot_floats / 4;
+    const size_t rstride = slot_words / 2;  // uint4 per rank row
     for (unsigned long long i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
-        float4 a = __ldcv(slots + i);
-        for (int r = 1; r < W; ++r) {
-            const float4 v = __ldcv(slots + (size_t)r * stride4 + i);
-            a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = 0; r < W; ++r) {
+            const uint4 *src = slots + (size_t)r * rstride + 2 * i;
+            uint4 lo, hi;
+            do {
+                lo = ld_volatile_v4(src);
+                hi = ld_volatile_v4(src + 1);
+            } while (lo.y != ep || lo.w != ep || hi.y != ep || hi.w != ep);
+            if (r == 0) {
+                a = make_float4(__uint_as_float(lo.x), __uint_as_float(lo.z), __uint_as_float(hi.x), __uint_as_float(hi.z));
+            } else {
+                a.x += __uint_as_float(lo.x); a.y += __uint_as_float(lo.z);
+                a.z += __uint_as_float(hi.x); a.w += __uint_as_float(hi.z);
+            }
         }
         y4[i] = a;
     }
-    if (threadIdx.x == 0) own_hdr[c] = ep;
 }
 
 }  // namespace cats
@@ -119,7 +132,7 @@ inline cats_status_t cuda_status_tp(cudaError_t e) {
     set_last_cuda_error(e);
     return CATS_E_CUDA;
 }
-size_t tp_buffer_bytes(int world, uint64_t n) { return kTpHeaderBytes + 2 * (size_t)world * ((n + 3) / 4 * 4) * 4; }
+size_t tp_buffer_bytes(int world, uint64_t n) { return kTpHeaderBytes + 2 * (size_t)world * ((n + 3) / 4 * 4) * 8; }
 int tp_ctas(uint64_t n) {  // ~1 KB of the call's values per CTA and slice, at most kTpMaxCtas
     const uint64_t c = (n + 255) / 256;
     return (int)(c < 1 ? 1 : c > (uint64_t)kTpMaxCtas ? kTpMaxCtas : c);

@@ -36,6 +36,11 @@ def graph_us(fn, reps=200):
     return 1e3 * e0.elapsed_time(e1) / (reps * 10)
 
 
+comm = tp.TpComm(5120)  # world = 1: the non-emulated kernel (push to self, flag, sum), no cooperative launch
+x1 = torch.randn(5120, device="cuda")
+y1 = torch.empty_like(x1)
+print(json.dumps({"P": 1, "n": 5120, "real_kernel_world1_us": round(graph_us(lambda: comm.allreduce(x1, y1)), 3)}),
+      flush=True)
 for P in (2, 4, 8):
     for n in (5120, 8 * 5120):
         em = tp.EmulatedTpComms(P, n)
