@@ -45,8 +45,9 @@ def parse():
     ap.add_argument("--copies", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extras", action="store_true", help="also time dense/cuBLAS/profiled (default on)")
-    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "fused"],
-                    help="N > 1: NCCL all-reduce, or the library's one-shot NVLink reduction (cats_tp_allreduce)")
+    ap.add_argument("--allreduce", default="fused", choices=["nccl", "fused"],
+                    help="N > 1: the library's one-shot NVLink reduction (cats_tp_allreduce; checked against NCCL "
+                         "at start, NCCL on a mismatch), or NCCL's all-reduce")
     ap.add_argument("--launcher-selftest", action="store_true",
                     help="start the ranks, all-reduce one tensor, print one line (CPU: gloo) and exit")
     return ap.parse_args()
@@ -300,7 +301,26 @@ def main():
 
     xs = cats_synth.tokens(64 * b, d, torch.bfloat16, seed=1).to(dev).view(64, b, d)
     y = torch.empty((b, d), dtype=torch.float32, device=dev)
-    comm = tpmod.TpComm(b * d, group=dist.group.WORLD) if world > 1 and args.allreduce == "fused" else None
+    comm = None
+    allreduce_used = "nccl" if world > 1 else None
+    if world > 1 and args.allreduce == "fused":
+        try:  # the fused reduction, checked once against NCCL on a rank-dependent pattern
+            comm = tpmod.TpComm(b * d, group=dist.group.WORLD)
+            probe = torch.arange(b * d, device=dev, dtype=torch.float32).view(b, d) * (rank + 1) / (b * d)
+            ref = probe.clone()
+            dist.all_reduce(ref)
+            got = comm.allreduce(probe.clone())
+            torch.cuda.synchronize(dev)
+            ok = torch.tensor([1 if torch.allclose(got, ref, rtol=1e-6, atol=1e-6) else 0], device=dev)
+        except Exception as exc:  # pragma: no cover - multi-GPU only
+            print(f"[bench] fused reduction unavailable ({type(exc).__name__}: {exc})", file=sys.stderr, flush=True)
+            ok = torch.tensor([0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item():
+            allreduce_used = "fused"
+        else:
+            comm = None
+            print("[bench] fused reduction check failed on some rank: using NCCL", file=sys.stderr, flush=True)
 
     def reduce_y(st):
         if world > 1:
@@ -499,7 +519,7 @@ def main():
             "gpu_launches": args.steps * kernels_per_step,
             "clocks": clocks,
             "detail": {
-                "allreduce": None if world == 1 else args.allreduce,
+                "allreduce": allreduce_used,
                 "nccl": None if world == 1 else {"version": ".".join(map(str, torch.cuda.nccl.version())),
                                                  "nranks": world, "collective": "all_reduce sum fp32 b x d"},
                 "t": t, "nnz_union_per_rank": nnz_local, "nnz_union_total": U, "m_per_rank": ms,
