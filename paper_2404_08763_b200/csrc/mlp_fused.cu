@@ -165,7 +165,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         int q_head = 0, q_tail = 0;  // pending UD jobs
         int gates_inflight = 0;      // GATE jobs issued, not yet retired
         bool ended = false;
-        unsigned long long p_wait = 0, p_busy = 0, p_issue = 0, t_last_gate = 0;  // diagnostics (CATS_TRACE)
+        unsigned long long p_wait = 0, p_busy = 0, p_issue = 0, t_last_gate = 0;  // diagnostics (options.trace)
 
         // issue job `prod` into its stage; returns false if nothing can be issued yet
         // pool mode, after the GATE tiles are exhausted: the next claimed pool slot as a UD job.

@@ -25,9 +25,9 @@
 //    (prefix-summed in every CTA) is cut into R equal ranges; CTA (r, q) streams the W_down rows of
 //    range r, column part q, accumulates y_r = sum_j x1_j W_down[j] in fp32 in list order (CUDA
 //    cores for b <= 3; for b >= 4 MMA with W_down^T via ldmatrix.trans and x1 as exact bf16 hi + lo),
-//    writes the partial, and after a grid barrier every CTA sums a slice of the R partials in fixed
-//    order r = 0..R-1 into y: the deterministic two-phase split-K reduction of the north star. The
-//    equal ranges balance the data-dependent work exactly.
+//    writes the partial; the last 64 CTAs to finish (no grid barrier) each sum a slice of the R partials in
+//    fixed order r = 0..R-1 into y: the deterministic two-phase split-K reduction of the north star. The
+//    tapered ranges balance the data-dependent work.
 //
 // KA -> KB -> next decode run as programmatic dependent launches: a kernel's CTAs become resident
 // while its predecessor drains and wait (griddepcontrol.wait) only before touching its outputs.
@@ -296,7 +296,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
         int rs = 0;
         uint32_t rphase = 0;
         const int r = lane / B, tk = lane % B;  // this lane's (row, token) pair
-        unsigned long long p_wait = 0;           // diagnostics (CATS_TRACE)
+        unsigned long long p_wait = 0;           // diagnostics (options.trace)
         int n_gate = 0, n_up = 0;
         // retire every job in order; after END (the last job issued, never released by the
         // consumers) is queued, the UP jobs still in flight are retired before the loop exits
