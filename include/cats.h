@@ -354,6 +354,10 @@ cats_status_t cats_xsparse_gemv(const cats_mlp_plan_t *plan, const void *x, int 
 #define CATS_IPC_HANDLE_BYTES 64
 typedef struct cats_tp_comm cats_tp_comm_t;
 cats_status_t cats_tp_buffer_bytes(int world, uint64_t n_max, size_t *bytes);
+/* The symmetric buffer as its own cudaMalloc allocation, zeroed (an IPC handle maps a whole allocation: a
+ * sub-range of a caching allocator's block would open at the block's base in the peers). Blocks. */
+cats_status_t cats_tp_buffer_alloc(size_t bytes, int device, void **dev_ptr_out);
+cats_status_t cats_tp_buffer_free(void *dev_ptr);
 cats_status_t cats_ipc_handle_get(const void *dev_ptr, uint8_t *handle_out /* [CATS_IPC_HANDLE_BYTES] */);
 cats_status_t cats_ipc_handle_open(const uint8_t *handle, int device, void **dev_ptr_out);
 cats_status_t cats_ipc_handle_close(void *dev_ptr);

@@ -82,6 +82,8 @@ _SIGS = {
     "cats_xsparse_plan_create": (I, [I, I, I, I, I, I, P]),
     "cats_xsparse_gemv": (I, [P, P, I, P, F, P, P, SZ, P]),
     "cats_tp_buffer_bytes": (I, [I, U64, P]),
+    "cats_tp_buffer_alloc": (I, [SZ, I, P]),
+    "cats_tp_buffer_free": (I, [P]),
     "cats_ipc_handle_get": (I, [P, P]),
     "cats_ipc_handle_open": (I, [P, I, P]),
     "cats_ipc_handle_close": (I, [P]),

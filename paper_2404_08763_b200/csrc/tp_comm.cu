@@ -146,6 +146,26 @@ extern "C" cats_status_t cats_tp_buffer_bytes(int world, uint64_t n_max, size_t 
     return CATS_OK;
 }
 
+extern "C" cats_status_t cats_tp_buffer_alloc(size_t bytes, int device, void **dev_ptr_out) {
+    if (!dev_ptr_out) return CATS_E_NULL;
+    if (bytes == 0) return CATS_E_SHAPE;
+    void *p = nullptr;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaMalloc(&p, bytes);  // its own allocation: an IPC handle maps exactly it
+    if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);  // epochs start at 0 (blocking)
+    if (e != cudaSuccess) {
+        if (p) cudaFree(p);
+        return cuda_status_tp(e);
+    }
+    *dev_ptr_out = p;
+    return CATS_OK;
+}
+
+extern "C" cats_status_t cats_tp_buffer_free(void *dev_ptr) {
+    if (!dev_ptr) return CATS_E_NULL;
+    return cuda_status_tp(cudaFree(dev_ptr));
+}
+
 extern "C" cats_status_t cats_ipc_handle_get(const void *dev_ptr, uint8_t *handle_out) {
     if (!dev_ptr || !handle_out) return CATS_E_NULL;
     cudaIpcMemHandle_t h;

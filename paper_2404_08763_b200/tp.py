@@ -85,10 +85,12 @@ class TpComm:
         self.n_max = int(n_max)
         nb = ctypes.c_size_t()
         _chk(self._lib.cats_tp_buffer_bytes(self.world, self.n_max, ctypes.byref(nb)), "cats_tp_buffer_bytes")
-        self.buf = torch.zeros(nb.value, dtype=torch.uint8, device=f"cuda:{self.device}")
-        torch.cuda.synchronize(self.device)
+        # the buffer is its own cudaMalloc allocation (not a slice of torch's caching allocator): an IPC
+        # handle maps a whole allocation, so peers open exactly this buffer
+        self._buf = ctypes.c_void_p()
+        _chk(self._lib.cats_tp_buffer_alloc(nb.value, self.device, ctypes.byref(self._buf)), "cats_tp_buffer_alloc")
         h = (ctypes.c_uint8 * 64)()
-        _chk(self._lib.cats_ipc_handle_get(self.buf.data_ptr(), h), "cats_ipc_handle_get")
+        _chk(self._lib.cats_ipc_handle_get(self._buf, h), "cats_ipc_handle_get")
         handles = [None] * self.world
         if self.world > 1:
             dist.all_gather_object(handles, bytes(h), group=group)
@@ -98,7 +100,7 @@ class TpComm:
         ptrs = (ctypes.c_void_p * self.world)()
         for r, hb in enumerate(handles):
             if r == self.rank:
-                ptrs[r] = self.buf.data_ptr()
+                ptrs[r] = self._buf.value
                 continue
             p = ctypes.c_void_p()
             _chk(self._lib.cats_ipc_handle_open((ctypes.c_uint8 * 64).from_buffer_copy(hb), self.device,
@@ -128,6 +130,9 @@ class TpComm:
             lib.cats_tp_comm_destroy(h)
         for p in getattr(self, "_opened", []):
             lib.cats_ipc_handle_close(p)
+        b = getattr(self, "_buf", None)
+        if b is not None and b.value:
+            lib.cats_tp_buffer_free(b)
 
 
 def _chk(rc, where):

@@ -330,5 +330,10 @@ def test_tp_comm_validation_without_gpu():
     assert lib.cats_tp_comm_create(1, 2, 5120, ptrs, 0, ctypes.byref(h)) == 0
     lib.cats_tp_comm_destroy(h)
     assert lib.cats_status_string(lib.cats_tp_comm_create(2, 2, 5120, ptrs, 0, ctypes.byref(h))).decode() == "CATS_E_SHAPE"
+    pb = ctypes.c_void_p()
+    assert lib.cats_status_string(lib.cats_tp_buffer_alloc(0, 0, ctypes.byref(pb))).decode() == "CATS_E_SHAPE"
+    assert lib.cats_status_string(lib.cats_tp_buffer_alloc(64, 0, None)).decode() == "CATS_E_NULL"
+    if not torch.cuda.is_available():
+        assert lib.cats_status_string(lib.cats_tp_buffer_alloc(1024, 0, ctypes.byref(pb))).decode() == "CATS_E_CUDA"
     bad = (ctypes.c_void_p * 2)(FAKE, FAKE + 4)
     assert lib.cats_status_string(lib.cats_tp_comm_create(0, 2, 5120, bad, 0, ctypes.byref(h))).decode() == "CATS_E_ALIGN"
