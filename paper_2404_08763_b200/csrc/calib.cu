@@ -280,38 +280,31 @@ calib_hist_tma_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint3
 #pragma unroll
             for (int u = 0; u < VPT; ++u) r[u] = lds128(sb + (uint32_t)((u * NC + tid) * 16));
             if constexpr (sizeof(K) == 2) {
-                // two keys per 32-bit word, SIMD within the register, ~4 ALU-pipe operations per word
-                // (the ALU pipe is what this loop saturates): k2 = keys with the sign bits cleared;
-                // (k2 + C1) has bit 15 of a half set iff key >= lo (C1 = 0x8000 - lo per half: no carry
-                // crosses halves), (hi2x - k2) iff key <= hi; the below-window count is a popcount (XU
-                // pipe), the non-finite flag a packed max, and in-window words only OR into `anyhit` --
-                // the rare stage that has one is rescanned from the registers afterwards
-                const uint32_t C1 = 0x80008000u - lo2;
-                uint32_t anyhit = 0;
+                // two keys per 32-bit word, SIMD within the register (see calib_hist_kernel)
+                uint32_t hit = 0;  // words holding an in-window key: handled after the sweep, from smem
 #pragma unroll
                 for (int u = 0; u < VPT; ++u) {
                     const uint32_t wv[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const uint32_t k2 = wv[q] & 0x7fff7fffu;
-                        const uint32_t gl = (k2 + C1) & 0x80008000u;
+                        const uint32_t gl = ((wv[q] | 0x80008000u) - lo2) & 0x80008000u;
                         nge2 += __popc(gl);
+                        const uint32_t k2 = wv[q] & 0x7fff7fffu;
                         kmax2 = __vmaxu2(kmax2, k2);
-                        anyhit |= (hi2x - k2) & gl;
+                        hit |= ((hi2x - k2) & gl) ? (1u << (u * 4 + q)) : 0u;
                     }
                 }
-                if (anyhit) {  // rare: classify this stage's in-window keys
-#pragma unroll
-                    for (int u = 0; u < VPT; ++u) {
-                        const uint32_t wv[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const uint32_t k2 = wv[q] & 0x7fff7fffu;
-                            const uint32_t iw = (hi2x - k2) & ((k2 + C1) & 0x80008000u);
-                            if (iw & 0x8000u) classify_in(k2 & 0xffffu);
-                            if (iw & 0x80000000u) classify_in(k2 >> 16);
-                        }
-                    }
+                while (hit) {  // rare: re-read the word from the (still owned) stage
+                    const int wq = __ffs(hit) - 1;
+                    hit &= hit - 1;
+                    uint32_t w;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w)
+                                 : "r"(sb + (uint32_t)(((wq >> 2) * NC + tid) * 16 + (wq & 3) * 4)));
+                    const uint32_t gl = ((w | 0x80008000u) - lo2) & 0x80008000u;
+                    const uint32_t k2 = w & 0x7fff7fffu;
+                    const uint32_t iw = (hi2x - k2) & gl;
+                    if (iw & 0x8000u) classify_in(k2 & 0xffffu);
+                    if (iw & 0x80000000u) classify_in(k2 >> 16);
                 }
                 seen_main += VPT * E;
             } else {
