@@ -281,15 +281,18 @@ calib_hist_tma_kernel(const K *__restrict__ acts, uint64_t n, uint32_t lo, uint3
             for (int u = 0; u < VPT; ++u) r[u] = lds128(sb + (uint32_t)((u * NC + tid) * 16));
             if constexpr (sizeof(K) == 2) {
                 // two keys per 32-bit word, SIMD within the register (see calib_hist_kernel)
+                // (k2 + C1, C1 = 0x8000 - lo per half: bit 15 of a half set iff key >= lo, no carry across
+                //  halves -- one ALU-pipe operation fewer than (w | 0x80008000) - lo2; the loop saturates the ALU pipe)
+                const uint32_t C1 = 0x80008000u - lo2;
                 uint32_t hit = 0;  // words holding an in-window key: handled after the sweep, from smem
 #pragma unroll
                 for (int u = 0; u < VPT; ++u) {
                     const uint32_t wv[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const uint32_t gl = ((wv[q] | 0x80008000u) - lo2) & 0x80008000u;
-                        nge2 += __popc(gl);
                         const uint32_t k2 = wv[q] & 0x7fff7fffu;
+                        const uint32_t gl = (k2 + C1) & 0x80008000u;
+                        nge2 += __popc(gl);
                         kmax2 = __vmaxu2(kmax2, k2);
                         hit |= ((hi2x - k2) & gl) ? (1u << (u * 4 + q)) : 0u;
                     }
