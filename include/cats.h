@@ -218,6 +218,7 @@ typedef struct {
     int32_t tail_rows;       /* K12 tail tiles: rows per tile for the last tail_tiles x grid tiles (0 = uniform;
                                 2 .. NR-1) -- finer work units where the dynamic schedule ends */
     int32_t tail_tiles;      /* K12 tail tiles per CTA (>= 0) */
+    int32_t gate_first_tail; /* 1: in K12's lazily claimed last tiles, GATE tiles are issued before queued UD jobs */
     int32_t convert_ctas;    /* K12: the last convert_ctas CTAs to finish convert the exact accumulator to fp32 y
                                 (a slice each); 0 or 1 = the last CTA alone */
     int32_t ud_pool;         /* 1: K12 streams every GATE tile first; retired tiles publish their up/down jobs to a

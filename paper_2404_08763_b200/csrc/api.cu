@@ -320,7 +320,8 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         (o.rows_per_tile != 0 && o.rows_per_tile != 2 && o.rows_per_tile != 4 && o.rows_per_tile != 6) ||
         o.xs_cols < 0 || o.xs_ranges < 0 || o.xs_ranges > 8 || o.tail_rows < 0 ||
         o.tail_rows > 6 || o.tail_tiles < 0 || o.tail_fused < 0 || o.tail_fused > 1 || o.ud_pool < 0 ||
-        o.ud_pool > 1 || o.convert_ctas < 0 || o.convert_ctas > 64)
+        o.ud_pool > 1 || o.convert_ctas < 0 || o.convert_ctas > 64 ||
+        o.gate_first_tail < 0 || o.gate_first_tail > 1)
         return CATS_E_SHAPE;
     if (d <= 0 || m <= 0) return CATS_E_SHAPE;
     if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
@@ -350,6 +351,7 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.tail_fused = o.tail_fused;
         p.ud_pool = o.ud_pool;
         p.convert_ctas = std::max(1, o.convert_ctas);
+        p.gate_first_tail = o.gate_first_tail;
         p.trace = o.trace != 0;
         p.kind = kind;
         p.g1 = 0;

@@ -54,6 +54,7 @@ struct PlanData {
     int tail_rows;      // K12 tail tiles: rows per tail tile (options.tail_rows; 0 = uniform tiles)
     int tail_tiles;     // K12 tail tiles per CTA (options.tail_tiles)
     int tail_fused;     // K12 tail tiles as fused gate+up+down jobs (options.tail_fused)
+    int gate_first_tail;  // K12: GATE before UD in the lazy tail (options.gate_first_tail)
     int convert_ctas;   // K12: CTAs converting the accumulator at the end (options.convert_ctas)
     int ud_pool;        // K12 gate-first with a grid-wide pool of up/down jobs (options.ud_pool)
     size_t off_pool;    // K12 UD pool slots (epoch-tagged 8-byte words)

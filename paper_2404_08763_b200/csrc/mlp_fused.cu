@@ -80,7 +80,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
              unsigned long long *__restrict__ yacc, float *__restrict__ y, unsigned int *__restrict__ sched,
              int32_t *__restrict__ gidx, float *__restrict__ gval, int t1, int ns, int tail_fused,
-             unsigned long long *__restrict__ pool, int ud_pool, int convert_ctas,
+             unsigned long long *__restrict__ pool, int ud_pool, int convert_ctas, int gate_first_tail,
              int lazy_tail, int eager, int l2pf, unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
@@ -224,32 +224,42 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             }
         };
 
+        // the next local UD job: W_up and W_down rows of <= NU active neurons of one retired tile
+        auto issue_local_ud = [&](Desc &D, unsigned char *dst, int s) {
+            const Desc &Q = queue[q_head % QCAP];
+            const int qn = Q.n;
+            // a negative id marks a row whose load Mask predicates off (Alg. 2 mode): no copy, read as 0
+            const bool has = lane < 2 * qn && Q.id[lane >> 1] >= 0;
+            const uint32_t nrows = (uint32_t)__popc(__ballot_sync(0xffffffffu, has));
+            if (lane == 0) {
+                D = Q;
+                mbar_arrive_expect_tx(&full[s], nrows * row_bytes);
+            }
+            __syncwarp();
+            CATS_DCHECK(q_tail - q_head <= QCAP);
+            if (has) {  // one bulk copy per lane: row (lane & 1) of neuron lane >> 1
+                const int i = lane >> 1;
+                const size_t j = (size_t)Q.id[i];
+                CATS_DCHECK(j < (size_t)m && (size_t)(lane + 1) * row_bytes <= stage_bytes);
+                bulk_g2s(dst + (size_t)lane * row_bytes, ((lane & 1) ? Wd : Wu) + j * d, row_bytes, &full[s],
+                         policy);
+            }
+            ++q_head;
+        };
+
         auto issue_job = [&]() -> bool {
             const int s = ps;
             Desc &D = desc[s];
             unsigned char *dst = ring + (size_t)s * stage_bytes;
+            // options.gate_first_tail: in the lazily claimed last tiles, GATE tiles go before queued UD jobs,
+            // so the last tiles' masks are known while a UD backlog still keeps the ring busy
+            const bool tail_gate_first = gate_first_tail && !gates_exhausted && snext >= batch &&
+                                         __shfl_sync(0xffffffffu, t_res == kNoTile ? 1u : 0u, 0) != 0u &&
+                                         q_tail - q_head < QCAP - 4;
             if (pooled && gates_exhausted) {
                 if (issue_pool(D, dst, s) == 0) return false;
-            } else if (q_head != q_tail) {  // UD job: W_up and W_down rows of <= NU active neurons
-                const Desc &Q = queue[q_head % QCAP];
-                const int qn = Q.n;
-                // a negative id marks a row whose load Mask predicates off (Alg. 2 mode): no copy, read as 0
-                const bool has = lane < 2 * qn && Q.id[lane >> 1] >= 0;
-                const uint32_t nrows = (uint32_t)__popc(__ballot_sync(0xffffffffu, has));
-                if (lane == 0) {
-                    D = Q;
-                    mbar_arrive_expect_tx(&full[s], nrows * row_bytes);
-                }
-                __syncwarp();
-                CATS_DCHECK(q_tail - q_head <= QCAP);
-                if (has) {  // one bulk copy per lane: row (lane & 1) of neuron lane >> 1
-                    const int i = lane >> 1;
-                    const size_t j = (size_t)Q.id[i];
-                    CATS_DCHECK(j < (size_t)m && (size_t)(lane + 1) * row_bytes <= stage_bytes);
-                    bulk_g2s(dst + (size_t)lane * row_bytes, ((lane & 1) ? Wd : Wu) + j * d, row_bytes, &full[s],
-                             policy);
-                }
-                ++q_head;
+            } else if (q_head != q_tail && !tail_gate_first) {  // UD job from the local queue
+                issue_local_ud(D, dst, s);
             } else if (list_mode) {  // Alg. 1 list kernel: UD job = the next NU entries of the global idcs
                 unsigned int tile = t_res;
                 if (lane == 0 && tile == kNoTile) tile = atomicAdd(&sched[0], 1u);
@@ -334,6 +344,14 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     if (pooled) {  // GATE tiles exhausted: from now on, UD jobs from the pool
                         gates_exhausted = true;
                         if (issue_pool(D, dst, s) == 0) return false;
+                        __syncwarp();
+                        ++prod;
+                        if (++ps == stages) ps = 0;
+                        return true;
+                    }
+                    gates_exhausted = true;
+                    if (q_head != q_tail) {  // (gate-first tail) the local backlog
+                        issue_local_ud(D, dst, s);
                         __syncwarp();
                         ++prod;
                         if (++ps == stages) ps = 0;
@@ -944,6 +962,7 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
         reinterpret_cast<unsigned int *>(w + p.off_sched), reinterpret_cast<int32_t *>(w + p.off_gidx),
         reinterpret_cast<float *>(w + p.off_gval), k12_t1(p, B), k12_tail_rows(p, B), p.tail_fused,
         reinterpret_cast<unsigned long long *>(w + p.off_pool), p.ud_pool, mode == kModeGateOnly ? 1 : p.convert_ctas,
+        p.gate_first_tail,
         p.lazy_tail * k12_grid(p, B),
         p.k12_eager, p.k12_l2pf,
         p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);

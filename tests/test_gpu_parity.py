@@ -198,6 +198,7 @@ def test_parity_app_d_ablation_modes(comp, model, b, k):
 
 
 @pytest.mark.parametrize("opts", [{"ud_pool": 1}, {"ud_pool": 1, "tail_rows": 2, "tail_tiles": 2}, {"convert_ctas": 8},
+                                  {"gate_first_tail": 1}, {"gate_first_tail": 1, "lazy_tail": 32},
                                   {"ud_pool": 1, "convert_ctas": 16},
                                   {"tail_rows": 2, "tail_tiles": 1},
                                   {"tail_rows": 2, "tail_tiles": 2, "tail_fused": 1},
