@@ -135,7 +135,6 @@ constexpr int kSplitAThreads = (kSplitAWarps + kSplitAGroups) * 32;
 constexpr int kSplitBMaxThreads = 672;                   // KB: <= 20 consumer warps + 1 producer warp
 constexpr int kSplitFifo = 64;                           // KA active-neuron FIFO (power of two)
 constexpr int kKbReducers = 64;                          // KB: the last K CTAs to finish sum the partials
-constexpr int kKbTilesPerThread = 16;                    // KB prologue: mask words per thread (ntiles <= 16 x threads)
 
 template <int NR, int B>
 struct SplitDesc {   // one KA ring stage: GATE(tile) or UP(<= NR active neurons)

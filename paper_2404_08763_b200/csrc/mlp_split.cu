@@ -510,48 +510,60 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
         fence_mbar_init();
     }
     // ---- per-tile active-row masks, published by KA's GATE retire (valid bit 31). KB does NOT wait
-    //      for KA to finish here: the list and the first W_down loads overlap KA's UP tail.
-    //      Thread t owns the contiguous tiles [a, e): it reads their mask words, the block scans the per-
-    //      thread active counts, and each thread scatters its own active rows whose global compact rank
-    //      falls in this CTA's range straight into the list (no per-element search). ----
-    const int per = (ntiles + nth - 1) / nth;
-    const int ta = min(ntiles, tid * per), te = min(ntiles, ta + per);
-    unsigned int mk[kKbTilesPerThread];
-    int sum = 0;
+    //      for KA to finish here: the list and the first W_down loads overlap KA's UP tail. ----
+    if (tid == 0) pre[0] = 0;
+    for (int base = 0; base < ntiles; base += 8 * nth) {  // 8 loads in flight per thread
+        unsigned int c[8];
 #pragma unroll
-    for (int u = 0; u < kKbTilesPerThread; ++u) {
-        mk[u] = 0x80000000u;
-        if (ta + u < te) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(mk[u]) : "l"(tmask + ta + u) : "memory");
-    }
+        for (int u = 0; u < 8; ++u) {
+            const int i = base + u * nth + tid;
+            c[u] = 0x80000000u;
+            if (i < ntiles) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c[u]) : "l"(tmask + i) : "memory");
+        }
 #pragma unroll
-    for (int u = 0; u < kKbTilesPerThread; ++u) {
-        if (ta + u < te) {
-            while (!(mk[u] & 0x80000000u)) {  // that tile's GATE job has not retired yet
-                __nanosleep(128);
-                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(mk[u]) : "l"(tmask + ta + u) : "memory");
+        for (int u = 0; u < 8; ++u) {
+            const int i = base + u * nth + tid;
+            if (i < ntiles) {
+                while (!(c[u] & 0x80000000u)) {  // that tile's GATE job has not retired yet
+                    __nanosleep(128);
+                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c[u]) : "l"(tmask + i) : "memory");
+                }
+                rowm[i] = (uint8_t)(c[u] & 0xffu);
+                pre[i + 1] = __popc(c[u] & 0xffu);
             }
-            sum += __popc(mk[u] & 0xffu);
         }
     }
     trace_stamp(trace, 1, 5);
-    int incl = sum;  // inclusive scan of the thread sums within the warp
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    if (tid == 0) s_rr = (int)rr_ticket;
     __syncthreads();
-    const int nwarps = nth / 32;
-    if (warp == 0) {
-        int w = lane < nwarps ? wsum[lane] : 0;
+    {
+        const int per = (ntiles + nth - 1) / nth;
+        const int a = min(ntiles, tid * per), e = min(ntiles, a + per);
+        int sum = 0;
+        for (int i = a; i < e; ++i) sum += pre[i + 1];
+        int incl = sum;  // inclusive scan of the thread sums within the warp
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += v;
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
         }
-        if (lane < nwarps) wsum[lane] = w;  // inclusive over warps
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const int nwarps = nth / 32;
+            int w = lane < nwarps ? wsum[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += v;
+            }
+            if (lane < nwarps) wsum[lane] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        int run = (warp > 0 ? wsum[warp - 1] : 0) + incl - sum;  // exclusive start of this thread
+        for (int i = a; i < e; ++i) {
+            run += pre[i + 1];
+            pre[i + 1] = run;
+        }
     }
     __syncthreads();
     trace_stamp(trace, 1, 6);
@@ -560,29 +572,28 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     // (weights 4R - r : 4R - r ... about +-14%) so that late arrivals finish with the early ones. The
     // boundaries are a fixed function of (U, R) and the partials are summed in range order: which CTA
     // computes which range does not change a bit of y.
+    if (tid == 0) s_rr = (int)rr_ticket;
+    __syncthreads();
     const int rr = s_rr;
-    const long long U = wsum[nwarps - 1];
+    const long long U = pre[ntiles];
     auto wcum = [R](long long r) { return r * (4LL * R + 1) - r * (r - 1) / 2; };  // sum_{i<r} (4R - i)
     const int lo = (int)(U * wcum(rr) / wcum(R)), hi = (int)(U * wcum(rr + 1) / wcum(R)), len = hi - lo;
     CATS_DCHECK(rr < R && 0 <= lo && lo <= hi && hi <= U && len <= maxr);
-    {
-        int g = (warp > 0 ? wsum[warp - 1] : 0) + incl - sum;  // global compact rank of this thread's first row
-        if (g < hi && g + sum > lo) {
-#pragma unroll
-            for (int u = 0; u < kKbTilesPerThread; ++u) {
-                if (ta + u < te) {
-                    unsigned int msk = mk[u] & 0xffu;
-                    for (int k = 0; msk; ++k, ++g) {
-                        const int row = __ffs(msk) - 1;
-                        msk &= msk - 1u;
-                        if (g >= lo && g < hi) {
-                            lj[g - lo] = (ta + u) * nr_tile + row;
-                            lpos[g - lo] = (ta + u) * nr_tile + k;
-                        }
-                    }
-                }
-            }
+
+    // ---- this range's neurons: compact rank g -> (tile, k) by binary search; neuron = k-th set row ----
+    for (int i = tid; i < len; i += nth) {
+        const int g = lo + i;
+        int a = 0, b = ntiles;  // largest tau with pre[tau] <= g
+        while (b - a > 1) {
+            const int mid = (a + b) >> 1;
+            if (pre[mid] <= g) a = mid; else b = mid;
         }
+        const int k = g - pre[a];
+        unsigned int msk = rowm[a];
+        for (int j = 0; j < k; ++j) msk &= msk - 1u;  // drop the k lowest set rows
+        lj[i] = a * nr_tile + (__ffs(msk) - 1);
+        lpos[i] = a * nr_tile + k;
+        CATS_DCHECK(msk != 0u && k < nr_tile);
     }
     __syncthreads();
     trace_stamp(trace, 1, 1);
@@ -872,7 +883,6 @@ bool kb_supported(const PlanData &p, int b) {  // KB alone fits this shape and b
     if (p.d % (split_q(p, b) * split_ept(p, b)) != 0) return false;
     if (((size_t)split_part_cols(p, b) * p.esize) % 16 != 0) return false;
     if (split_kb_consumers(p, b) + 32 > kSplitBMaxThreads) return false;
-    if (k12_ntiles(p, b) > kKbTilesPerThread * (split_kb_consumers(p, b) + 32)) return false;  // prologue
     const int sb = split_kb_stages(p, b);
     return sb >= 2 && split_kb_smem(p, b, sb) <= kSmemBudget;
 }

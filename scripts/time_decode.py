@@ -10,6 +10,10 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
+if "--lib" in sys.argv:  # A/B experiments: load another build of the library (e.g. libcats_ab.so)
+    from paper_2404_08763_b200 import _lib as _l
+    _l.LIB_PATH = os.path.join(os.path.dirname(_l.LIB_PATH), sys.argv[sys.argv.index("--lib") + 1])
+
 import cats_synth
 import paper_2404_08763_b200 as cats
 
@@ -22,6 +26,7 @@ ap.add_argument("--dense", action="store_true")
 ap.add_argument("--copies", type=int, default=0, help="weight copies (default: enough for >= 400 MB)")
 ap.add_argument("--reps", type=int, default=50)
 ap.add_argument("--tag", default="")
+ap.add_argument("--lib", default="", help="library file name in the package directory (A/B)")
 ap.add_argument("--opt", action="append", default=[],
                 help="plan option key=value (cats_mlp_plan_options_t field), repeatable")
 a = ap.parse_args()
