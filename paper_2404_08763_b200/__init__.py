@@ -21,7 +21,7 @@ __all__ = [
     "cats_calib_window_init", "cats_calib_hist", "cats_calib_step", "cats_mlp_decode", "cats_mlp_dense",
     "cats_mlp_decode_profiled",
     "cats_mlp_decode_host", "cats_mlp_gate_act", "cats_mlp_last_active", "cats_mlp_kernels_per_call", "library_path",
-    "XsparsePlan", "cats_xsparse_gemv", "plan_options", "CATS_PATH_AUTO", "CATS_PATH_FUSED", "CATS_PATH_SPLIT", "CATS_COMPACT_BALLOT",
+    "XsparsePlan", "cats_xsparse_gemv", "BoundDecodeHost", "plan_options", "CATS_PATH_AUTO", "CATS_PATH_FUSED", "CATS_PATH_SPLIT", "CATS_COMPACT_BALLOT",
     "CATS_COMPACT_PREDICATED", "CATS_COMPACT_ATOMIC",
 ]
 
@@ -330,6 +330,28 @@ def cats_mlp_decode_host(plan: MlpPlan, x_host: torch.Tensor, W_gate, W_up, W_do
                                         y_host.data_ptr(), _dev_ptr(ws, "ws"), ws.numel(), st.cuda_stream)
     _check(rc, "cats_mlp_decode_host")
     return y_host
+
+
+class BoundDecodeHost:
+    """cats_mlp_decode_host with its arguments validated and marshalled once (a serving loop's per-token
+    call): every call copies the CURRENT contents of x_host to the device, decodes and delivers y into
+    y_host, blocking on the stream -- the C ABI call alone, without re-checking tensors each token."""
+
+    def __init__(self, plan: MlpPlan, x_host, W_gate, W_up, W_down_nm, t: float, y_host=None, ws=None, stream=None):
+        # one validated call through the regular path (allocates y_host / ws if needed)
+        self.y_host = cats_mlp_decode_host(plan, x_host, W_gate, W_up, W_down_nm, t, y_host=y_host, ws=ws,
+                                           stream=stream)
+        x2 = x_host if x_host.dim() == 2 else x_host.unsqueeze(0)
+        ws = ws if ws is not None else plan.workspace(stream=stream)
+        st = _stream_obj(stream, torch.device(f"cuda:{plan.device}"))
+        self._keep = (plan, x_host, W_gate, W_up, W_down_nm, ws, st)  # lifetimes
+        self._fn = plan._lib.cats_mlp_decode_host
+        self._args = (plan.handle, x2.data_ptr(), x2.shape[0], W_gate.data_ptr(), W_up.data_ptr(), W_down_nm.data_ptr(),
+                      float(t), self.y_host.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)
+
+    def __call__(self) -> torch.Tensor:
+        _check(self._fn(*self._args), "cats_mlp_decode_host")
+        return self.y_host
 
 
 def cats_mlp_gate_act(plan: MlpPlan, x, W_gate, acts=None, ws=None, stream=None):

@@ -300,6 +300,11 @@ def test_decode_host_equals_device_path():
     x1 = x[:1].clone()                                                            # b = 1 (K12), pinned
     y1 = cats.cats_mlp_decode_host(plan, x1.pin_memory(), Wg, Wu, Wd, 0.1, ws=ws)
     assert torch.equal(cats.cats_mlp_decode(plan, _dev(x1), Wg, Wu, Wd, 0.1, ws=ws).cpu(), y1)
+    xp = x.pin_memory()                                                           # bound call: x re-read each call
+    call = cats.BoundDecodeHost(plan, xp, Wg, Wu, Wd, 0.1, ws=ws)
+    x2 = cats_synth.tokens(b, d, torch.bfloat16, seed=10)
+    xp.copy_(x2)
+    assert torch.equal(call().clone(), cats.cats_mlp_decode(plan, _dev(x2), Wg, Wu, Wd, 0.1, ws=ws).cpu())
 
 
 def test_tensor_parallel_emulated_on_one_gpu():
