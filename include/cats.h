@@ -215,17 +215,6 @@ typedef struct {
     int32_t min_tiles;       /* K12 grid <= ntiles / min_tiles (>= 1) */
     int32_t eager;           /* K12 fills every ring stage with claimed tiles at start (0 / 1) */
     int32_t l2_prefetch;     /* K12 static tiles per CTA prefetched into L2 before griddepcontrol.wait (>= 0) */
-    int32_t tail_rows;       /* K12 tail tiles: rows per tile for the last tail_tiles x grid tiles (0 = uniform;
-                                2 .. NR-1) -- finer work units where the dynamic schedule ends */
-    int32_t tail_tiles;      /* K12 tail tiles per CTA (>= 0) */
-    int32_t gate_first_tail; /* 1: in K12's lazily claimed last tiles, GATE tiles are issued before queued UD jobs */
-    int32_t convert_ctas;    /* K12: the last convert_ctas CTAs to finish convert the exact accumulator to fp32 y
-                                (a slice each); 0 or 1 = the last CTA alone */
-    int32_t ud_pool;         /* 1: K12 streams every GATE tile first; retired tiles publish their up/down jobs to a
-                                grid-wide pool that all CTAs drain (dynamic balancing of the second half) */
-    int32_t tail_fused;      /* 1: a tail tile of tail_rows <= NR / 3 rows is one job that loads its W_gate, W_up and
-                                W_down rows together (no mask -> load round trip at the end; reads the tail tiles'
-                                inactive W_up / W_down rows) */
     int32_t xs_cols;         /* App. B XS: columns per CTA (0 = auto) */
     int32_t xs_ranges;       /* App. B XS: cluster size R (0 = auto, else 1..8) */
     int32_t xs_mma;          /* App. B XS: 1 = tensor cores where the slab allows (default), 0 = FFMA2 only */

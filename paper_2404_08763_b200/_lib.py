@@ -31,8 +31,7 @@ class PlanOptions(ctypes.Structure):
     _fields_ = [("size", ctypes.c_uint32), ("path", ctypes.c_int32), ("compaction", ctypes.c_int32),
                 ("trace", ctypes.c_int32), ("rows_per_tile", ctypes.c_int32), ("max_stages", ctypes.c_int32),
                 ("lazy_tail", ctypes.c_int32), ("min_tiles", ctypes.c_int32), ("eager", ctypes.c_int32),
-                ("l2_prefetch", ctypes.c_int32), ("tail_rows", ctypes.c_int32), ("tail_tiles", ctypes.c_int32),
-                ("gate_first_tail", ctypes.c_int32), ("convert_ctas", ctypes.c_int32), ("ud_pool", ctypes.c_int32), ("tail_fused", ctypes.c_int32),
+                ("l2_prefetch", ctypes.c_int32),
                 ("xs_cols", ctypes.c_int32), ("xs_ranges", ctypes.c_int32),
                 ("xs_mma", ctypes.c_int32), ("xs_no_shrink", ctypes.c_int32)]
 

@@ -318,10 +318,7 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
     if (o.compaction < CATS_COMPACT_BALLOT || o.compaction > CATS_COMPACT_ATOMIC) return CATS_E_UNSUPPORTED;
     if (o.lazy_tail < 0 || o.min_tiles < 1 || o.l2_prefetch < 0 || o.max_stages < 0 || o.max_stages == 1 ||
         (o.rows_per_tile != 0 && o.rows_per_tile != 2 && o.rows_per_tile != 4 && o.rows_per_tile != 6) ||
-        o.xs_cols < 0 || o.xs_ranges < 0 || o.xs_ranges > 8 || o.tail_rows < 0 ||
-        o.tail_rows > 6 || o.tail_tiles < 0 || o.tail_fused < 0 || o.tail_fused > 1 || o.ud_pool < 0 ||
-        o.ud_pool > 1 || o.convert_ctas < 0 || o.convert_ctas > 64 ||
-        o.gate_first_tail < 0 || o.gate_first_tail > 1)
+        o.xs_cols < 0 || o.xs_ranges < 0 || o.xs_ranges > 8)
         return CATS_E_SHAPE;
     if (d <= 0 || m <= 0) return CATS_E_SHAPE;
     if (dt != CATS_BF16 && dt != CATS_F32) return CATS_E_DTYPE;
@@ -346,12 +343,6 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.nchunks = d * esize / 16;
         p.compaction = kind == 0 ? o.compaction : CATS_COMPACT_BALLOT;
         p.nr_force = o.rows_per_tile;
-        p.tail_rows = o.tail_rows;
-        p.tail_tiles = o.tail_tiles;
-        p.tail_fused = o.tail_fused;
-        p.ud_pool = o.ud_pool;
-        p.convert_ctas = std::max(1, o.convert_ctas);
-        p.gate_first_tail = o.gate_first_tail;
         p.trace = o.trace != 0;
         p.kind = kind;
         p.g1 = 0;
@@ -430,7 +421,7 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.off_idx = off;     off = align_up(off + (size_t)m * 4, 256);
         p.off_tokmask = off; off = align_up(off + (size_t)m, 256);
         p.off_vals = off;    off = align_up(off + (size_t)m * max_batch * 4, 256);
-        p.off_cnt = off;     off = align_up(off + (size_t)m * 4, 256);  // per-tile counts (tail tiles may be 1 row)
+        p.off_cnt = off;     off = align_up(off + (size_t)((m + 1) / 2) * 4, 256);  // per-tile counts (tiles >= 2 rows)
         p.off_ypart = off;   off = align_up(off + (size_t)max_batch * d * 8, 256);  // int64 y accumulator
         p.off_xstage = off;  off = align_up(off + (size_t)max_batch * d * esize, 256);
         p.off_ystage = off;  off = align_up(off + (size_t)max_batch * d * 4, 256);
@@ -453,13 +444,6 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         const bool atomic_list = p.compaction == CATS_COMPACT_ATOMIC;  // App. D Alg. 1: global idcs list
         p.off_gidx = off;    off = align_up(off + (atomic_list ? (size_t)m * 4 : 0), 256);
         p.off_gval = off;    off = align_up(off + (atomic_list ? (size_t)m * max_batch * 4 : 0), 256);
-        size_t pool_bytes = 0;  // K12 UD pool: 2 slots per tile, (1 + NU + NU b) epoch-tagged words per slot
-        if (p.ud_pool)
-            for (int b = 1; b <= max_batch; ++b) {
-                const size_t nu = (size_t)k12_rows_per_tile(p, b) / 2;
-                pool_bytes = std::max(pool_bytes, (size_t)2 * k12_ntiles_geo(p, b) * (1 + nu + nu * b) * 8);
-            }
-        p.off_pool = off;    off = align_up(off + pool_bytes, 256);
         p.k12_min_tiles = o.min_tiles;
         p.k12_l2pf = o.l2_prefetch;  // measured: prefetching only slows the drain (default 0)
         p.k12_eager = o.eager;
@@ -572,9 +556,6 @@ extern "C" cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, vo
                             static_cast<cudaStream_t>(s));
     if (e == cudaSuccess)
         e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_tmask, 0, (size_t)((plan->p.m + 1) / 2) * 4,
-                            static_cast<cudaStream_t>(s));
-    if (e == cudaSuccess && plan->p.ud_pool)  // pool words carry epochs: zero = never published
-        e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_pool, 0, plan->p.off_trace - plan->p.off_pool,
                             static_cast<cudaStream_t>(s));
     return cuda_status(e);
 }
@@ -734,9 +715,8 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
             *nnz_union = k;
             return CATS_OK;
         }
-        // per-tile segments: K12's geometry (tail tiles) when K12 ran, uniform tiles on the split path
-        const bool k12_ran = p.compaction != CATS_COMPACT_BALLOT || !(b >= p.split_min_b && split_supported(p, b));
-        const int ntiles = k12_ran ? k12_ntiles_geo(p, b) : k12_ntiles(p, b);
+        // per-tile segments of k12_rows_per_tile rows (K12 and the split path share the tile geometry)
+        const int ntiles = k12_ntiles(p, b), nr = k12_rows_per_tile(p, b);
         std::vector<int32_t> idx(p.m), cnt(ntiles);
         std::vector<uint8_t> tm(p.m);
         cudaError_t e = cudaSetDevice(p.device);
@@ -748,10 +728,8 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
         uint32_t k = 0;
         if (nnz_per_token) std::fill(nnz_per_token, nnz_per_token + b, 0u);
         for (int c = 0; c < ntiles; ++c) {
-            const int64_t r0 = k12_ran ? k12_tile_r0(p, b, c) : (int64_t)c * k12_rows_per_tile(p, b);
-            const int64_t r1 = k12_ran ? (c + 1 < ntiles ? k12_tile_r0(p, b, c + 1) : p.m)
-                                       : (int64_t)(c + 1) * k12_rows_per_tile(p, b);
-            const int64_t R = std::min<int64_t>(r1, p.m) - r0;
+            const int64_t r0 = (int64_t)c * nr;
+            const int64_t R = std::min<int64_t>(r0 + nr, p.m) - r0;
             if (cnt[c] < 0 || cnt[c] > R) return CATS_E_SHAPE;
             for (int i = 0; i < cnt[c]; ++i) {
                 idx_host[k] = idx[r0 + i];

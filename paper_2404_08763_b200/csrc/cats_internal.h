@@ -51,13 +51,6 @@ struct PlanData {
     int k12_l2pf;       // K12 static tiles per CTA prefetched into L2 at start (options.l2_prefetch)
     int nr_force;       // 0 = automatic tile height; 2 / 4 / 6 forces it (options.rows_per_tile)
     int compaction;     // cats_compaction_t (options.compaction)
-    int tail_rows;      // K12 tail tiles: rows per tail tile (options.tail_rows; 0 = uniform tiles)
-    int tail_tiles;     // K12 tail tiles per CTA (options.tail_tiles)
-    int tail_fused;     // K12 tail tiles as fused gate+up+down jobs (options.tail_fused)
-    int gate_first_tail;  // K12: GATE before UD in the lazy tail (options.gate_first_tail)
-    int convert_ctas;   // K12: CTAs converting the accumulator at the end (options.convert_ctas)
-    int ud_pool;        // K12 gate-first with a grid-wide pool of up/down jobs (options.ud_pool)
-    size_t off_pool;    // K12 UD pool slots (epoch-tagged 8-byte words)
     int kind;           // 0 = gated-MLP plan, 1 = App. B input-sparse projection plan (d = d_out, m = d_in)
     struct XsCfg {            // kind 1 (xsparse.cu), per batch size b = 1..8:
         int cols, q, r;       //   columns per CTA, column parts, cluster size (ranges of the kept list)
@@ -96,28 +89,6 @@ inline int k12_cpt(const PlanData &p, int b) {
 inline int k12_grid(const PlanData &p, int b) {  // >= k12_min_tiles tiles per CTA on small layers
     const int mt = std::max(1, p.k12_min_tiles);
     return std::max(1, std::min(p.num_sms * k12_ctas_per_sm_c(b), (k12_ntiles(p, b) + mt - 1) / mt));
-}
-// K12 tail tiles (options.tail_rows / tail_tiles): the last ~tail_tiles x grid work units are tiles of
-// tail_rows < NR rows, so the dynamically claimed end of the gate GEMV comes in finer pieces and the
-// mask -> UD-load chain of the last tiles is shorter. K12's geometry: t1 tiles of NR rows, then tiles of
-// k12_tail_rows (k12_ntiles stays the uniform count, used for grid sizing and by KA / KB).
-inline int k12_tail_rows(const PlanData &p, int b) {
-    const int nr = k12_rows_per_tile(p, b);
-    return (p.tail_rows >= 1 && p.tail_rows < nr && p.tail_tiles > 0) ? p.tail_rows : nr;
-}
-inline int k12_t1(const PlanData &p, int b) {
-    const int nr = k12_rows_per_tile(p, b), ns = k12_tail_rows(p, b);
-    if (ns == nr) return (p.m + nr - 1) / nr;
-    const long long S = std::min<long long>(p.m, (long long)p.tail_tiles * k12_grid(p, b) * ns);
-    return (int)((p.m - S) / nr);
-}
-inline int k12_ntiles_geo(const PlanData &p, int b) {
-    const int t1 = k12_t1(p, b), nr = k12_rows_per_tile(p, b), ns = k12_tail_rows(p, b);
-    return t1 + std::max(0, (p.m - t1 * nr + ns - 1) / ns);
-}
-inline int k12_tile_r0(const PlanData &p, int b, int tile) {
-    const int t1 = k12_t1(p, b), nr = k12_rows_per_tile(p, b);
-    return tile < t1 ? tile * nr : t1 * nr + (tile - t1) * k12_tail_rows(p, b);
 }
 size_t k12_smem_bytes(const PlanData &p, int b, int stages);
 inline int k12_stages(const PlanData &p, int b) {

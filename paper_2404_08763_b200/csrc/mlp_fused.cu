@@ -45,11 +45,7 @@
 
 namespace cats {
 
-enum : int { kJobEnd = 0, kJobGate = 1, kJobUD = 2, kJobGUD = 3 };
-// kJobGUD (tail tiles, options.tail_fused): one stage carries a tail tile's W_gate, W_up and W_down rows
-// ([NG rows of each], NG = NR / 3); the consumers compute u -> v -> keep themselves and finish the
-// tile in the same job -- the mask -> UD-load round trip (two loaded HBM latencies in a row at the end
-// of the schedule) becomes one, for the price of reading the tail tiles' inactive W_up / W_down rows.
+enum : int { kJobEnd = 0, kJobGate = 1, kJobUD = 2 };
 
 
 
@@ -73,14 +69,17 @@ __device__ __forceinline__ void claim_tile_async(unsigned int &t, unsigned int *
                  : "memory");
 }
 
-template <typename T, int B, int NR, int CPT>
+// ABL: the App. D ablation modes (kModePredicated, kModeAtomicGate, kModeAtomicList) are compiled in.
+// The default instantiation (ABL = false) carries only the CATS / dense / gate-only paths: the ablation
+// branches cost registers and issue slots in the producer's refill loop even when never taken
+// (measured: 42.3 vs 41.8 us per Mistral-7B layer with them compiled into the default kernel).
+template <typename T, int B, int NR, int CPT, bool ABL>
 __global__ void __launch_bounds__(k12_threads_c(B), k12_ctas_per_sm_c(B))
 k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restrict__ Wu, const T *__restrict__ Wd,
              int d, int m, int stages, float t, int mode, int32_t *__restrict__ idx, uint8_t *__restrict__ tokmask,
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
              unsigned long long *__restrict__ yacc, float *__restrict__ y, unsigned int *__restrict__ sched,
-             int32_t *__restrict__ gidx, float *__restrict__ gval, int t1, int ns, int tail_fused,
-             unsigned long long *__restrict__ pool, int ud_pool, int convert_ctas, int gate_first_tail,
+             int32_t *__restrict__ gidx, float *__restrict__ gval,
              int lazy_tail, int eager, int l2pf, unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
@@ -98,22 +97,10 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     const int nch = d * (int)sizeof(T) / 16;
     const uint32_t row_bytes = (uint32_t)d * (uint32_t)sizeof(T);
     const uint32_t stage_bytes = (uint32_t)NR * row_bytes;
-    // tile geometry: t1 tiles of NR rows, then (tail) tiles of ns <= NR rows -- finer work units for the
-    // last tiles the dynamic scheduler hands out (k12_t1 / k12_tail_rows; ns == NR: uniform)
-    const int ntiles = t1 + max(0, (m - t1 * NR + ns - 1) / ns);
-    auto tile_r0 = [t1, ns](int tile) { return tile < t1 ? tile * NR : t1 * NR + (tile - t1) * ns; };
-    auto tile_rows = [t1, ns, m](int tile, int r0) { return min(tile < t1 ? NR : ns, m - r0); };
-    const bool list_mode = mode == kModeAtomicList;  // App. D Alg. 1, launch 2: work units = chunks of idcs
-    const bool has_y = mode != kModeGateOnly && mode != kModeAtomicGate;
-    constexpr int NG = NR / 3 > 0 ? NR / 3 : 1;  // rows of a fused tail tile (GUD job)
-    // UD pool (options.ud_pool): every CTA first streams GATE tiles; each retired tile publishes its <= 2 UD
-    // jobs into fixed slots 2 tile + h of a grid-wide pool (epoch-tagged 8-byte words: no fences); once the
-    // tiles are exhausted, CTAs claim pool slots in order from a counter -- the up/down work of the whole
-    // layer is balanced dynamically across the grid and no CTA ends on its own last tile's dependency chain
-    constexpr int PW = 1 + NU + NU * B;          // pool words per slot: (n), (id_i), (v_i,tk), each with the epoch
-    static_assert(PW <= 32, "one pool word per lane");
-    const bool pooled = ud_pool && (mode == kModeCats || mode == kModeDense);
-    const bool gud_tail = tail_fused && NR >= 3 && ns <= NG && (mode == kModeCats || mode == kModeDense);
+    const int ntiles = (m + NR - 1) / NR;
+    const bool list_mode = ABL && mode == kModeAtomicList;  // App. D Alg. 1, launch 2: work units = chunks of idcs
+    const bool atomic_gate = ABL && mode == kModeAtomicGate;  // App. D Alg. 1, launch 1: gate + atomic appends
+    const bool has_y = mode != kModeGateOnly && !atomic_gate;
 
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char *ring = smem;                                                           // [stages][stage_bytes]
@@ -138,8 +125,8 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     if (warp == NW) {
         // ===================================== PRODUCER WARP =====================================
         const bool dense = mode == kModeDense;
-        const bool gate_only = mode == kModeGateOnly || mode == kModeAtomicGate;  // no UD jobs from this launch
-        const bool predicated = mode == kModePredicated;
+        const bool gate_only = mode == kModeGateOnly || atomic_gate;  // no UD jobs from this launch
+        const bool predicated = ABL && mode == kModePredicated;
         const uint64_t policy = l2_evict_first_policy();
         // Tile claims (lane 0). While many tiles remain, the next GATE tile is reserved one issue ahead
         // (t_res: a predicated atomic whose round trip overlaps the jobs in between; nothing reads
@@ -148,9 +135,6 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         // drain (balanced tail), and small layers spread over all CTAs.
         unsigned int t_res = kNoTile;  // raw counter value; tile id = dyn_base + counter
         unsigned int sched_list_n = 0; // list mode: length of the global idcs list
-        unsigned int pool_slot = kNoTile;  // pool mode: the next claimed slot (lane 0; async claim)
-        unsigned int pool_ep = 0;          // pool mode: this call's epoch (sched[7] + 1)
-        bool gates_exhausted = false;
         // static first tiles per CTA: `stages` of them go straight into the ring, up to l2pf more are
         // prefetched into L2 (cp.async.bulk.prefetch) -- both before griddepcontrol.wait, so they use
         // the HBM time while the previous kernel drains -- and taken in order before any claim
@@ -168,98 +152,34 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         unsigned long long p_wait = 0, p_busy = 0, p_issue = 0, t_last_gate = 0;  // diagnostics (options.trace)
 
         // issue job `prod` into its stage; returns false if nothing can be issued yet
-        // pool mode, after the GATE tiles are exhausted: the next claimed pool slot as a UD job.
-        // 1 = issued, 0 = nothing issuable yet (slot not published), 2 = END issued
-        auto issue_pool = [&](Desc &D, unsigned char *dst, int s) -> int {
-            for (;;) {
-                unsigned int slot = pool_slot;
-                if (lane == 0 && slot == kNoTile) slot = atomicAdd(&sched[4], 1u);
-                slot = __shfl_sync(0xffffffffu, slot, 0);
-                if (lane == 0) pool_slot = slot;
-                if (slot >= 2u * (unsigned)ntiles) {  // every slot claimed: end once no GATE job can publish
-                    if (gates_inflight != 0) return 0;
-                    if (lane == 0) {
-                        D.type = kJobEnd;
-                        D.n = 0;
-                        mbar_arrive_expect_tx(&full[s], 0u);
-                    }
-                    ended = true;
-                    return 2;
-                }
-                if (gud_tail && (int)(slot >> 1) >= t1) {  // fused tail tiles publish nothing: skip their slots
-                    if (lane == 0) pool_slot = kNoTile;
-                    continue;
-                }
-                unsigned long long w = 0ull;
-                if (lane < PW)
-                    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(pool + (size_t)slot * PW + lane) : "memory");
-                // word 0 (the slot's neuron count) first, then the words of its qn neurons; all epoch-tagged
-                const bool fresh0 = __shfl_sync(0xffffffffu, (unsigned int)(w >> 32), 0) == pool_ep;
-                const int qn = (int)__shfl_sync(0xffffffffu, (unsigned int)w, 0);
-                const int wi = lane - 1 - NU;  // v word index (neuron wi / B, token wi % B)
-                const bool used = (lane >= 1 && lane <= NU) ? lane - 1 < qn : (lane > NU && lane < PW) ? wi / B < qn : false;
-                const bool fresh = !used || (unsigned int)(w >> 32) == pool_ep;
-                if (!fresh0 || !__all_sync(0xffffffffu, fresh)) return 0;  // not published yet: retry later
-                if (lane == 0) {
-                    pool_slot = kNoTile;
-                    claim_tile_async(pool_slot, sched + 4, true);  // the next slot, claimed ahead
-                }
-                if (qn == 0) continue;  // an empty slot (tile with <= NU active neurons): take the next
-                if (lane >= 1 && lane <= NU) D.id[lane - 1] = used ? (int)(unsigned int)w : 0;
-                if (lane > NU && lane < PW) D.v[wi / B][wi % B] = used ? __uint_as_float((unsigned int)w) : 0.0f;
-                __syncwarp();
-                if (lane == 0) {
-                    D.type = kJobUD;
-                    D.tile = (int)(slot >> 1);
-                    D.n = qn;
-                    mbar_arrive_expect_tx(&full[s], (uint32_t)qn * 2u * row_bytes);
-                }
-                __syncwarp();
-                if (lane < 2 * qn) {
-                    const size_t j = (size_t)D.id[lane >> 1];
-                    CATS_DCHECK(j < (size_t)m);
-                    bulk_g2s(dst + (size_t)lane * row_bytes, ((lane & 1) ? Wd : Wu) + j * d, row_bytes, &full[s], policy);
-                }
-                return 1;
-            }
-        };
-
-        // the next local UD job: W_up and W_down rows of <= NU active neurons of one retired tile
-        auto issue_local_ud = [&](Desc &D, unsigned char *dst, int s) {
-            const Desc &Q = queue[q_head % QCAP];
-            const int qn = Q.n;
-            // a negative id marks a row whose load Mask predicates off (Alg. 2 mode): no copy, read as 0
-            const bool has = lane < 2 * qn && Q.id[lane >> 1] >= 0;
-            const uint32_t nrows = (uint32_t)__popc(__ballot_sync(0xffffffffu, has));
-            if (lane == 0) {
-                D = Q;
-                mbar_arrive_expect_tx(&full[s], nrows * row_bytes);
-            }
-            __syncwarp();
-            CATS_DCHECK(q_tail - q_head <= QCAP);
-            if (has) {  // one bulk copy per lane: row (lane & 1) of neuron lane >> 1
-                const int i = lane >> 1;
-                const size_t j = (size_t)Q.id[i];
-                CATS_DCHECK(j < (size_t)m && (size_t)(lane + 1) * row_bytes <= stage_bytes);
-                bulk_g2s(dst + (size_t)lane * row_bytes, ((lane & 1) ? Wd : Wu) + j * d, row_bytes, &full[s],
-                         policy);
-            }
-            ++q_head;
-        };
-
         auto issue_job = [&]() -> bool {
             const int s = ps;
             Desc &D = desc[s];
             unsigned char *dst = ring + (size_t)s * stage_bytes;
-            // options.gate_first_tail: in the lazily claimed last tiles, GATE tiles go before queued UD jobs,
-            // so the last tiles' masks are known while a UD backlog still keeps the ring busy
-            const bool tail_gate_first = gate_first_tail && !gates_exhausted && snext >= batch &&
-                                         __shfl_sync(0xffffffffu, t_res == kNoTile ? 1u : 0u, 0) != 0u &&
-                                         q_tail - q_head < QCAP - 4;
-            if (pooled && gates_exhausted) {
-                if (issue_pool(D, dst, s) == 0) return false;
-            } else if (q_head != q_tail && !tail_gate_first) {  // UD job from the local queue
-                issue_local_ud(D, dst, s);
+            if (q_head != q_tail) {  // UD job: W_up and W_down rows of <= NU active neurons
+                const Desc &Q = queue[q_head % QCAP];
+                const int qn = Q.n;
+                // a negative id marks a row whose load Mask predicates off (Alg. 2 mode): no copy, read as 0
+                bool has = lane < 2 * qn;
+                uint32_t nrows = (uint32_t)qn * 2u;
+                if constexpr (ABL) {
+                    has = has && Q.id[lane >> 1] >= 0;
+                    nrows = (uint32_t)__popc(__ballot_sync(0xffffffffu, has));
+                }
+                if (lane == 0) {
+                    D = Q;
+                    mbar_arrive_expect_tx(&full[s], nrows * row_bytes);
+                }
+                __syncwarp();
+                CATS_DCHECK(q_tail - q_head <= QCAP);
+                if (has) {  // one bulk copy per lane: row (lane & 1) of neuron lane >> 1
+                    const int i = lane >> 1;
+                    const size_t j = (size_t)Q.id[i];
+                    CATS_DCHECK(j < (size_t)m && (size_t)(lane + 1) * row_bytes <= stage_bytes);
+                    bulk_g2s(dst + (size_t)lane * row_bytes, ((lane & 1) ? Wd : Wu) + j * d, row_bytes, &full[s],
+                             policy);
+                }
+                ++q_head;
             } else if (list_mode) {  // Alg. 1 list kernel: UD job = the next NU entries of the global idcs
                 unsigned int tile = t_res;
                 if (lane == 0 && tile == kNoTile) tile = atomicAdd(&sched[0], 1u);
@@ -308,8 +228,8 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     tile = __shfl_sync(0xffffffffu, tile, 0) + dyn_base;
                 }
                 if (tile < (unsigned)ntiles) {  // GATE job: a new tile of W_gate rows
-                    const int r0 = tile_r0((int)tile);
-                    const int nr = tile_rows((int)tile, r0);
+                    const int r0 = (int)tile * NR;
+                    const int nr = min(NR, m - r0);
                     CATS_DCHECK(r0 >= 0 && nr >= 1 && r0 + nr <= m && (uint32_t)nr * row_bytes <= stage_bytes);
                     if (from_static) {
                         ++snext;
@@ -317,46 +237,17 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                         t_res = kNoTile;
                         claim_tile_async(t_res, sched, tile + (unsigned)lazy_tail < (unsigned)ntl);
                     }
-                    if (gud_tail && (int)tile >= t1) {  // fused tail tile: W_gate, W_up, W_down rows at once
-                        if (lane == 0) {
-                            D.type = kJobGUD;
-                            D.tile = (int)tile;
-                            D.n = nr;
-                            mbar_arrive_expect_tx(&full[s], 3u * (uint32_t)nr * row_bytes);
-                        }
-                        __syncwarp();
-                        if (lane < 3)
-                            bulk_g2s(dst + (size_t)lane * nr * row_bytes, (lane == 0 ? Wg : lane == 1 ? Wu : Wd) + (size_t)r0 * d,
-                                     (uint32_t)nr * row_bytes, &full[s], policy);
-                    } else {
-                        if (lane == 0) {
-                            D.type = kJobGate;
-                            D.tile = (int)tile;
-                            D.n = nr;
-                            mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
-                            bulk_g2s(dst, Wg + (size_t)r0 * d, (uint32_t)nr * row_bytes, &full[s], policy);
-                        }
-                        ++gates_inflight;
+                    if (lane == 0) {
+                        D.type = kJobGate;
+                        D.tile = (int)tile;
+                        D.n = nr;
+                        mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
+                        bulk_g2s(dst, Wg + (size_t)r0 * d, (uint32_t)nr * row_bytes, &full[s], policy);
                     }
+                    ++gates_inflight;
                     if (trace) t_last_gate = gtimer();
                 } else {
                     if (lane == 0) t_res = tile - dyn_base;  // past the end: keep it, no further claims
-                    if (pooled) {  // GATE tiles exhausted: from now on, UD jobs from the pool
-                        gates_exhausted = true;
-                        if (issue_pool(D, dst, s) == 0) return false;
-                        __syncwarp();
-                        ++prod;
-                        if (++ps == stages) ps = 0;
-                        return true;
-                    }
-                    gates_exhausted = true;
-                    if (q_head != q_tail) {  // (gate-first tail) the local backlog
-                        issue_local_ud(D, dst, s);
-                        __syncwarp();
-                        ++prod;
-                        if (++ps == stages) ps = 0;
-                        return true;
-                    }
                     if (gates_inflight != 0) return false;  // an in-flight GATE job may add UD work
                     // no tiles left and nothing in flight can create UD work: end the ring
                     if (lane == 0) {
@@ -379,15 +270,15 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             // before the PDL predecessor has finished; everything it writes (tile counter, y
             // accumulator, x, index lists) is touched only after griddepcontrol.wait below.
             for (int s = batch > stages ? stages : batch; s < batch; ++s) {  // the rest of the static tiles -> L2
-                const int r0 = tile_r0((int)(sbase + s));
+                const int r0 = (int)(sbase + s) * NR;
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Wg + (size_t)r0 * d),
-                             "r"((uint32_t)tile_rows((int)(sbase + s), r0) * row_bytes)
+                             "r"((uint32_t)min(NR, m - r0) * row_bytes)
                              : "memory");
             }
             for (int s = 0; s < min(batch, stages); ++s) {
                 const unsigned int tile = sbase + s;  // grid * batch <= ntiles
-                const int r0 = tile_r0((int)tile);
-                const int nr = tile_rows((int)tile, r0);
+                const int r0 = (int)tile * NR;
+                const int nr = min(NR, m - r0);
                 desc[s].type = kJobGate;
                 desc[s].tile = (int)tile;
                 desc[s].n = nr;
@@ -405,11 +296,6 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             ntl = (int)((sched_list_n + NU - 1) / NU);
         }
         if (lane == 0) claim_tile_async(t_res, sched, dyn_base + (unsigned)lazy_tail < (unsigned)ntl);
-        if (pooled) {
-            unsigned int e = 0;
-            if (lane == 0) e = *reinterpret_cast<volatile unsigned int *>(sched + 7) + 1u;
-            pool_ep = __shfl_sync(0xffffffffu, e, 0);
-        }
         prod = __shfl_sync(0xffffffffu, prod, 0);
         ps = prod % stages;
         gates_inflight = prod;
@@ -424,10 +310,6 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         int rs = 0;                  // = retire % stages
         uint32_t rphase = 0;         // = (retire / stages) & 1
         while (!ended) {
-            if (retire == prod) {  // nothing in flight (pool mode, waiting for a slot to be published): poll
-                if (!issue_job()) __nanosleep(64);
-                continue;
-            }
             // ---- retire job `retire` in order ----
             const unsigned long long tw0 = trace ? gtimer() : 0ull;
             mbar_wait(&empty[rs], rphase);
@@ -436,7 +318,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
             if (desc[rs].type == kJobGate) {
                 // u (fixed-order sum over the 16 consumer warps) -> v = SiLU(u) (Eq. 2) ->
                 // keep = |v| >= t (Eq. 4, ties kept) -> ballot compaction of the tile
-                const int tile = desc[rs].tile, n = desc[rs].n, r0 = tile_r0(tile);
+                const int tile = desc[rs].tile, n = desc[rs].n, r0 = tile * NR;
                 const float *rb = red + (size_t)rs * NW * NPMAX;
                 uint32_t bits = 0;
                 float vrow[B];
@@ -480,26 +362,14 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     tokmask[pos] = (uint8_t)bits;
 #pragma unroll
                     for (int tk = 0; tk < B; ++tk) vals[(size_t)pos * B + tk] = ((bits >> tk) & 1u) ? vrow[tk] : 0.0f;
-                    if (mode == kModeAtomicGate) {  // App. D Alg. 1 line 4: append (j, v_j) to the global idcs
+                    if (atomic_gate) {  // App. D Alg. 1 line 4: append (j, v_j) to the global idcs
                         const unsigned int ap = atomicAdd(&sched[3], 1u);
                         CATS_DCHECK(ap < (unsigned)m);
                         gidx[ap] = r0 + lane;
 #pragma unroll
                         for (int tk = 0; tk < B; ++tk) gval[(size_t)ap * B + tk] = ((bits >> tk) & 1u) ? vrow[tk] : 0.0f;
                     }
-                    if (pooled) {  // publish into slot 2 tile + rank / NU: (id, v) words tagged with the epoch
-                        unsigned long long *ps_ = pool + ((size_t)2 * tile + rank / NU) * PW;
-                        const int i = rank % NU;
-                        const unsigned long long ept = (unsigned long long)pool_ep << 32;
-                        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(ps_ + 1 + i),
-                                     "l"(ept | (unsigned int)(r0 + lane)) : "memory");
-#pragma unroll
-                        for (int tk = 0; tk < B; ++tk) {
-                            const float vv = ((bits >> tk) & 1u) ? vrow[tk] : 0.0f;
-                            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(ps_ + 1 + NU + i * B + tk),
-                                         "l"(ept | __float_as_uint(vv)) : "memory");
-                        }
-                    } else if (!gate_only && !predicated) {  // queue the tile's active neurons, NU per UD job, ascending
+                    if (!gate_only && !predicated) {  // queue the tile's active neurons, NU per UD job, ascending
                         Desc &Q = queue[(q_tail + rank / NU) % QCAP];
                         const int i = rank % NU;
                         Q.id[i] = r0 + lane;
@@ -513,13 +383,8 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     }
                 }
                 if (lane == 0) cnt[tile] = nact;
-                if (pooled && lane < 2) {  // the slots' neuron counts (0 for an empty slot), published last
-                    const int qn = min(NU, max(0, nact - lane * NU));
-                    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(pool + ((size_t)2 * tile + lane) * PW),
-                                 "l"(((unsigned long long)pool_ep << 32) | (unsigned int)qn) : "memory");
-                }
                 if (predicated) q_tail += (n + NU - 1) / NU;
-                else if (!gate_only && !pooled) q_tail += (nact + NU - 1) / NU;  // pool mode: published, not queued
+                else if (!gate_only) q_tail += (nact + NU - 1) / NU;
                 --gates_inflight;
                 __syncwarp();
             }
@@ -545,7 +410,6 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     } else {
         // ===================================== CONSUMER WARPS ====================================
         pdl_wait_primary();     // x (and the accumulators) may come from the PDL predecessor
-        const unsigned int pool_ep_c = pooled ? *reinterpret_cast<volatile unsigned int *>(sched + 7) + 1u : 0u;
         uint4 xr[B][CPT];  // x, own chunks, packed (bf16 pairs or fp32), 0 past the row end
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
@@ -608,120 +472,13 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                     }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);  // stage read + partials written -> producer
-            } else if (type == kJobGUD) {
-                ++n_ud;
-                const int tile = desc[s].tile, r0 = tile_r0(tile);
-                constexpr int NPGU = NG * B;
-                constexpr int PPR = 32 / NW;
-                uint4 wg[NG][CPT], wu[NG][CPT], wd[NG][CPT];
-#pragma unroll
-                for (int i = 0; i < NG; ++i)
-#pragma unroll
-                    for (int k = 0; k < CPT; ++k) {
-                        const int ch = tid + k * NC;
-                        const bool ok = i < n && ch < nch;
-                        const uint32_t off = (uint32_t)i * row_bytes + (uint32_t)ch * 16u;
-                        wg[i][k] = ok ? lds128(sbase + off) : make_uint4(0u, 0u, 0u, 0u);
-                        wu[i][k] = ok ? lds128(sbase + (uint32_t)n * row_bytes + off) : make_uint4(0u, 0u, 0u, 0u);
-                        wd[i][k] = ok ? lds128(sbase + 2u * (uint32_t)n * row_bytes + off) : make_uint4(0u, 0u, 0u, 0u);
-                    }
-                // u = x W_gate[:, j] and up = x W_up[:, j]: per-thread partials -> warp sums -> red
-                float pg[NG][B], pu[NG][B];
-#pragma unroll
-                for (int i = 0; i < NG; ++i)
-#pragma unroll
-                    for (int tk = 0; tk < B; ++tk) {
-                        pg[i][tk] = 0.f;
-                        pu[i][tk] = 0.f;
-#pragma unroll
-                        for (int k = 0; k < CPT; ++k) {
-                            pg[i][tk] = dot16<T>(wg[i][k], xr[tk][k], pg[i][tk]);
-                            pu[i][tk] = dot16<T>(wu[i][k], xr[tk][k], pu[i][tk]);
-                        }
-                    }
-#pragma unroll
-                for (int i = 0; i < NG; ++i)
-#pragma unroll
-                    for (int tk = 0; tk < B; ++tk) {
-                        const float vg = warp_allreduce_sum(pg[i][tk]);
-                        const float vu = warp_allreduce_sum(pu[i][tk]);
-                        if (lane == 0) {
-                            rb[warp * NPMAX + i * B + tk] = vg;
-                            rb[warp * NPMAX + NPGU + i * B + tk] = vu;
-                        }
-                    }
-                consumer_barrier<NC>();
-                // cross-warp sums (fixed tree, identical in every warp) of the 2 NG B pairs
-                float sg[2 * NPGU];
-#pragma unroll
-                for (int c = 0; c < (2 * NPGU + PPR - 1) / PPR; ++c) {
-                    const int pp = c * PPR + lane / NW;
-                    float v = (pp < 2 * NPGU) ? rb[(lane % NW) * NPMAX + pp] : 0.f;
-#pragma unroll
-                    for (int o = NW / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-#pragma unroll
-                    for (int q = 0; q < PPR; ++q)
-                        if (c * PPR + q < 2 * NPGU) sg[c * PPR + q] = __shfl_sync(0xffffffffu, v, q * NW);
-                }
-                consumer_barrier<NC>();  // every warp has read red[s]
-                if (lane == 0) mbar_arrive(&empty[s]);  // stage, descriptor and red[s] released
-                // v = SiLU(u) (Eq. 2), keep = |v| >= t (Eq. 4), x1 = up * v (Optimization 1), pre-scaled 2^8
-                float x1[NG][B];
-                uint32_t bits[NG];
-#pragma unroll
-                for (int i = 0; i < NG; ++i) {
-                    bits[i] = 0u;
-#pragma unroll
-                    for (int tk = 0; tk < B; ++tk) {
-                        const float u = sg[i * B + tk];
-                        const float v = __fdividef(u, 1.0f + __expf(-u));
-                        const bool keep = i < n && (mode == kModeDense || fabsf(v) >= t);
-                        bits[i] |= (keep ? 1u : 0u) << tk;
-                        x1[i][tk] = keep ? (sg[NPGU + i * B + tk] * v) * kFixPre : 0.f;
-                    }
-                }
-                if (warp == 0) {  // bookkeeping of the tile: ascending active rows at [r0, r0 + cnt)
-                    int rank = 0;
-#pragma unroll
-                    for (int i = 0; i < NG; ++i) {
-                        if (lane == 0 && bits[i]) {
-                            const int pos = r0 + rank;
-                            idx[pos] = r0 + i;
-                            tokmask[pos] = (uint8_t)bits[i];
-#pragma unroll
-                            for (int tk = 0; tk < B; ++tk) {
-                                const float u = sg[i * B + tk];
-                                const float v = __fdividef(u, 1.0f + __expf(-u));
-                                vals[(size_t)pos * B + tk] = ((bits[i] >> tk) & 1u) ? v : 0.0f;
-                            }
-                        }
-                        rank += bits[i] ? 1 : 0;
-                    }
-                    if (lane == 0) cnt[tile] = rank;
-                }
-                // ---- down: y_job[c] = sum_i x1_i W_down[i][c] (fp32, fixed order) -> fixed point ----
-#pragma unroll
-                for (int k = 0; k < CPT; ++k) {
-                    float wf[NG][VEC];
-#pragma unroll
-                    for (int i = 0; i < NG; ++i) unpack16(wd[i][k], wf[i]);
-#pragma unroll
-                    for (int tk = 0; tk < B; ++tk)
-#pragma unroll
-                        for (int e = 0; e < VEC; ++e) {
-                            float yj = 0.f;
-#pragma unroll
-                            for (int i = 0; i < NG; ++i) yj = fmaf(x1[i][tk], wf[i][e], yj);
-                            fix_acc(yhi[tk][k][e], ylo[tk][k][e], yj);
-                        }
-                }
             } else {  // kJobUD
                 ++n_ud;
                 float vj[NU][B];  // descriptor -> registers before releasing the stage
                 bool live[NU];    // row loaded (false: predicated off by Mask in Alg. 2 mode -> zeros)
 #pragma unroll
                 for (int i = 0; i < NU; ++i) {
-                    live[i] = i < n && (mode != kModePredicated || desc[s].id[i] >= 0);
+                    live[i] = i < n && (!ABL || mode != kModePredicated || desc[s].id[i] >= 0);
 #pragma unroll
                     for (int tk = 0; tk < B; ++tk) vj[i][tk] = desc[s].v[i][tk];
                 }
@@ -863,58 +620,35 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         }
         consumer_barrier<NC>();
         trace_stamp(trace, 0, 4);  // partial reduced into yacc
-        // The last KC CTAs to arrive convert the accumulator (a 1/KC slice each) once every CTA's partial is
-        // in (KC = options.convert_ctas; 1 = the last CTA alone). A converter only waits for CTAs that
-        // have not arrived; the last converter to pass the wait re-arms the counters.
-        __shared__ unsigned int s_ticket, s_reset;
-        if (tid == 0) s_ticket = atomicAdd(&sched[1], 1u);
+        if (tid == 0) s_last = (atomicAdd(&sched[1], 1u) == gridDim.x - 1) ? 1u : 0u;
         consumer_barrier<NC>();
-        const int G = (int)gridDim.x;
-        const int KC = min(G, max(1, convert_ctas));
-        const int ri = (int)s_ticket - (G - KC);
-        if (ri >= 0) {
-            if (tid == 0) {
-                if (KC > 1) {
-                    unsigned int seen;
-                    do {
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(sched + 1) : "memory");
-                    } while (seen < (unsigned)G);
-                }
-                s_reset = (KC == 1 || atomicAdd(&sched[6], 1u) == (unsigned)KC - 1u) ? 1u : 0u;
-            }
-            consumer_barrier<NC>();
+        if (s_last) {
             __threadfence();
             if (has_y) {
                 // 8 independent L2 loads in flight per thread (the accumulator was just written by
                 // the bulk-reduce engine of every SM; a serial loop would pay one L2 trip per step)
                 const int n2 = B * d / 2;
-                const int cb = (int)((long long)n2 * ri / KC), ce = (int)((long long)n2 * (ri + 1) / KC);
-                for (int c0 = cb; c0 < ce; c0 += 8 * NC) {
+                for (int c0 = 0; c0 < n2; c0 += 8 * NC) {
                     longlong2 v[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const int c = c0 + u * NC + tid;
-                        v[u] = c < ce ? __ldcg(reinterpret_cast<const longlong2 *>(yacc) + c) : make_longlong2(0, 0);
+                        v[u] = c < n2 ? __ldcg(reinterpret_cast<const longlong2 *>(yacc) + c) : make_longlong2(0, 0);
                     }
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const int c = c0 + u * NC + tid;
-                        if (c < ce) {
+                        if (c < n2) {
                             reinterpret_cast<float2 *>(y)[c] = make_float2(fix_to_float(v[u].x), fix_to_float(v[u].y));
                             reinterpret_cast<longlong2 *>(yacc)[c] = make_longlong2(0, 0);
                         }
                     }
                 }
             }
-            if (tid == 0 && s_reset) {
+            if (tid == 0) {
                 sched[0] = 0u;
                 sched[1] = 0u;
-                sched[6] = 0u;
                 if (list_mode) sched[3] = 0u;  // the idcs list was consumed: re-arm the append counter
-                if (pooled) {
-                    sched[4] = 0u;             // pool claims
-                    sched[7] = pool_ep_c;      // the pool's epoch: the next call publishes with epoch + 1
-                }
             }
         }
         trace_stamp(trace, 0, 3);
@@ -933,10 +667,10 @@ size_t k12_smem_bytes(const PlanData &p, int b, int stages) {
     return (s + 127) & ~(size_t)127;
 }
 
-template <typename T, int B, int NR, int CPT>
+template <typename T, int B, int NR, int CPT, bool ABL>
 static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
                                 float t, int mode, float *acts, float *y, void *ws, cudaStream_t s) {
-    auto kern = k12_cats_mlp<T, B, NR, CPT>;
+    auto kern = k12_cats_mlp<T, B, NR, CPT, ABL>;
     const int stages = p.k12_max_stages > 0 ? std::min(p.k12_max_stages, k12_stages(p, B)) : k12_stages(p, B);
     const size_t smem = k12_smem_bytes(p, B, stages);
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(kern), smem);
@@ -960,28 +694,35 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
         reinterpret_cast<uint8_t *>(w + p.off_tokmask), reinterpret_cast<float *>(w + p.off_vals),
         reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<unsigned long long *>(w + p.off_ypart), y,
         reinterpret_cast<unsigned int *>(w + p.off_sched), reinterpret_cast<int32_t *>(w + p.off_gidx),
-        reinterpret_cast<float *>(w + p.off_gval), k12_t1(p, B), k12_tail_rows(p, B), p.tail_fused,
-        reinterpret_cast<unsigned long long *>(w + p.off_pool), p.ud_pool, mode == kModeGateOnly ? 1 : p.convert_ctas,
-        p.gate_first_tail,
-        p.lazy_tail * k12_grid(p, B),
+        reinterpret_cast<float *>(w + p.off_gval), p.lazy_tail * k12_grid(p, B),
         p.k12_eager, p.k12_l2pf,
         p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
+template <typename T, int B, int NR, bool ABL>
+static cudaError_t launch_k12_a(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
+                                float t, int mode, float *acts, float *y, void *ws, cudaStream_t s) {
+    switch (k12_cpt(p, B)) {
+        case 1: return launch_k12_t<T, B, NR, 1, ABL>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 2: return launch_k12_t<T, B, NR, 2, ABL>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
+        case 3:
+            return B == 1 ? launch_k12_t<T, B, NR, (B == 1 ? 3 : 2), ABL>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s)
+                          : cudaErrorInvalidValue;
+        case 4:
+            return B == 1 ? launch_k12_t<T, B, NR, (B == 1 ? 4 : 2), ABL>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s)
+                          : cudaErrorInvalidValue;
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 template <typename T, int B, int NR>
 static cudaError_t launch_k12_r(const PlanData &p, const void *x, const void *Wg, const void *Wu, const void *Wd,
                                 float t, int mode, float *acts, float *y, void *ws, cudaStream_t s) {
-    switch (k12_cpt(p, B)) {
-        case 1: return launch_k12_t<T, B, NR, 1>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
-        case 2: return launch_k12_t<T, B, NR, 2>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
-        case 3: return B == 1 ? launch_k12_t<T, B, NR, (B == 1 ? 3 : 2)>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s)
-                              : cudaErrorInvalidValue;
-        case 4: return B == 1 ? launch_k12_t<T, B, NR, (B == 1 ? 4 : 2)>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s)
-                              : cudaErrorInvalidValue;
-        default: return cudaErrorInvalidValue;
-    }
+    const bool abl = mode == kModePredicated || mode == kModeAtomicGate || mode == kModeAtomicList;
+    return abl ? launch_k12_a<T, B, NR, true>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s)
+               : launch_k12_a<T, B, NR, false>(p, x, Wg, Wu, Wd, t, mode, acts, y, ws, s);
 }
 
 template <typename T, int B>

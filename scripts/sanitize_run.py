@@ -20,8 +20,7 @@ from paper_2404_08763_b200 import tp
 dev = "cuda"
 d, m = 512, 1000
 Wg, Wu, Wd = (w.to(dev) for w in cats_synth.mlp_weights(d, m, torch.bfloat16))
-for opts in ({}, {"ud_pool": 1}, {"ud_pool": 1, "convert_ctas": 8, "path": cats.CATS_PATH_FUSED},
-             {"path": cats.CATS_PATH_FUSED}, {"compaction": cats.CATS_COMPACT_PREDICATED},
+for opts in ({}, {"path": cats.CATS_PATH_FUSED}, {"path": cats.CATS_PATH_FUSED, "lazy_tail": 0, "eager": 1}, {"compaction": cats.CATS_COMPACT_PREDICATED},
              {"compaction": cats.CATS_COMPACT_ATOMIC}, {"path": cats.CATS_PATH_SPLIT}):
     plan = cats.MlpPlan(d, m, max_batch=8, **opts)
     ws = plan.workspace()

@@ -197,17 +197,14 @@ def test_parity_app_d_ablation_modes(comp, model, b, k):
         assert float((y - y2).norm() / y.norm()) < 1e-6
 
 
-@pytest.mark.parametrize("opts", [{"ud_pool": 1}, {"ud_pool": 1, "tail_rows": 2, "tail_tiles": 2}, {"convert_ctas": 8},
-                                  {"gate_first_tail": 1}, {"gate_first_tail": 1, "lazy_tail": 32},
-                                  {"ud_pool": 1, "convert_ctas": 16},
-                                  {"tail_rows": 2, "tail_tiles": 1},
-                                  {"tail_rows": 2, "tail_tiles": 2, "tail_fused": 1},
-                                  {"tail_rows": 1, "tail_tiles": 3, "tail_fused": 1, "rows_per_tile": 4}])
+@pytest.mark.parametrize("opts", [{"lazy_tail": 0}, {"lazy_tail": 64}, {"max_stages": 2}, {"eager": 1},
+                                  {"min_tiles": 16}, {"l2_prefetch": 4}, {"rows_per_tile": 2},
+                                  {"rows_per_tile": 4, "eager": 1, "lazy_tail": 1000}])
 @pytest.mark.parametrize("model,b,k", [("mistral-7b", 1, 0.5), ("llama2-7b", 3, 0.7)])
-def test_parity_k12_tail_geometry(opts, model, b, k):
-    """K12 schedule variants against the oracle, bit-reproducible: the grid-wide up/down job pool (gate tiles
-    first, retired tiles publish their jobs, every CTA drains the pool), tail tiles (finer last work units)
-    and fused tail jobs (W_gate + W_up + W_down rows in one stage, the mask computed by the consumers)."""
+def test_parity_k12_schedule_knobs(opts, model, b, k):
+    """K12 under the schedule knobs (tile reservation off / everywhere, shallow ring, eager fill, few CTAs,
+    L2 prefetch of static tiles, other tile heights) against the oracle, bit-reproducible: the dynamic
+    schedule changes which CTA takes which tile, never y."""
     d, m = cats_synth.MODELS[model]
     res, (plan, ws, dx, dg, du, dd, y) = run_parity(d, m, b, torch.bfloat16, k, seed=85,
                                                     opts={"path": cats.CATS_PATH_FUSED, **opts})
