@@ -262,10 +262,11 @@ cats_status_t cats_mlp_dense(const cats_mlp_plan_t *plan, const void *x, int b, 
                              const void *W_up, const void *W_down_nm, float *y,
                              void *ws, size_t ws_bytes, cats_stream_t s);
 
-/* End-to-end variant for host activations: copies x_host [b][d] (pinned memory recommended)
- * into the workspace, runs cats_mlp_decode and delivers y to y_host [b][d] fp32 — written by the
- * kernel straight into host memory when y_host is pinned (mapped), else via a device-to-host copy.
- * BLOCKS on s. */
+/* End-to-end variant for host activations: brings x_host [b][d] into the workspace, runs
+ * cats_mlp_decode and delivers y to y_host [b][d] fp32. Pinned (mapped) x_host: a small kernel reads
+ * it across PCIe and the decode kernel overlaps its start with that read (programmatic dependent
+ * launch); pageable x_host: a host-to-device copy. Pinned y_host: written by the kernel straight
+ * into host memory; pageable: a device-to-host copy. BLOCKS on s. */
 cats_status_t cats_mlp_decode_host(const cats_mlp_plan_t *plan, const void *x_host, int b,
                                    const void *W_gate, const void *W_up, const void *W_down_nm,
                                    float t, float *y_host, void *ws, size_t ws_bytes, cats_stream_t s);

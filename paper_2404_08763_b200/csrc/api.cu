@@ -655,17 +655,24 @@ extern "C" cats_status_t cats_mlp_decode_host(const cats_mlp_plan_t *plan, const
     void *xd = w + p.off_xstage;
     float *yd = reinterpret_cast<float *>(w + p.off_ystage);
     cudaError_t e = cudaSetDevice(p.device);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(xd, x_host, (size_t)b * p.d * p.esize, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_status(e);
-    // pinned (mapped) y_host: the kernel writes y straight into host memory (one small PCIe write
-    // from the converting CTAs) instead of a separate device-to-host copy
-    cudaPointerAttributes pa{};
-    float *y_direct = nullptr;
-    if (cudaPointerGetAttributes(&pa, y_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer &&
-        aligned16(pa.devicePointer))
-        y_direct = static_cast<float *>(pa.devicePointer);
-    else
+    // pinned (mapped) host buffers: a small kernel pulls x across PCIe (the decode kernel then overlaps its
+    // start with it through programmatic dependent launch) and the kernel writes y straight into host memory
+    // (one small PCIe write from the converting CTAs); pageable buffers go through copies
+    auto mapped = [](const void *h) -> void * {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, h) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer &&
+            aligned16(pa.devicePointer))
+            return pa.devicePointer;
         (void)cudaGetLastError();  // clear a pageable-pointer query error
+        return nullptr;
+    };
+    const size_t x_bytes = (size_t)b * p.d * p.esize;
+    const void *x_direct = mapped(x_host);
+    float *y_direct = static_cast<float *>(mapped(y_host));
+    e = x_direct ? launch_x_stage(x_direct, xd, x_bytes, st)
+                 : cudaMemcpyAsync(xd, x_host, x_bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_status(e);
     cats_status_t rc = run_mlp(p, xd, b, W_gate, W_up, W_down_nm, t, 0, y_direct ? y_direct : yd, ws, st);
     if (rc != CATS_OK) return rc;
     if (!y_direct) e = cudaMemcpyAsync(y_host, yd, (size_t)b * p.d * 4, cudaMemcpyDeviceToHost, st);

@@ -163,6 +163,7 @@ cudaError_t ensure_smem_attr(const void *func, size_t smem);
 
 // launchers: return cudaError_t of the launch
 // K12 = the whole decode (gate ... down projection and the split-K reduction; y written by the last CTA)
+cudaError_t launch_x_stage(const void *x_mapped, void *xd, size_t bytes, cudaStream_t s);  // mlp_fused.cu
 cudaError_t launch_k12(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd,
                        float t, int mode, float *acts, float *y, void *ws, cudaStream_t s);
 

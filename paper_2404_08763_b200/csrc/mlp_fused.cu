@@ -754,6 +754,22 @@ static cudaError_t launch_k12_dt(const PlanData &p, const void *x, int b, const 
     }
 }
 
+// cats_mlp_decode_host with a mapped (pinned) x: x crosses PCIe in a small kernel instead of a copy-engine
+// transfer, so the decode kernel that follows can use programmatic dependent launch -- its CTAs become
+// resident and stream their static W_gate tiles while x is in flight (they read x after
+// griddepcontrol.wait, which also orders this kernel's stores before their loads).
+__global__ void x_stage_kernel(const uint4 *__restrict__ src, uint4 *__restrict__ dst, int n16) {
+    pdl_launch_dependents();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
+cudaError_t launch_x_stage(const void *x_mapped, void *xd, size_t bytes, cudaStream_t s) {
+    const int n16 = (int)(bytes / 16);
+    const int grid = std::max(1, std::min(64, (n16 + 255) / 256));
+    x_stage_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4 *>(x_mapped), static_cast<uint4 *>(xd), n16);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_k12(const PlanData &p, const void *x, int b, const void *Wg, const void *Wu, const void *Wd,
                        float t, int mode, float *acts, float *y, void *ws, cudaStream_t s) {
     if (p.dt == CATS_BF16) return launch_k12_dt<bf16_bits>(p, x, b, Wg, Wu, Wd, t, mode, acts, y, ws, s);
