@@ -422,7 +422,7 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         p.off_tokmask = off; off = align_up(off + (size_t)m, 256);
         p.off_vals = off;    off = align_up(off + (size_t)m * max_batch * 4, 256);
         p.off_cnt = off;     off = align_up(off + (size_t)((m + 1) / 2) * 4, 256);  // per-tile counts (tiles >= 2 rows)
-        p.off_ypart = off;   off = align_up(off + (size_t)max_batch * d * 8, 256);  // int64 y accumulator
+        p.off_ypart = off;   off = align_up(off + (size_t)2 * max_batch * d * 8, 256);  // 2 int64 y accumulators (K12)
         p.off_xstage = off;  off = align_up(off + (size_t)max_batch * d * esize, 256);
         p.off_ystage = off;  off = align_up(off + (size_t)max_batch * d * 4, 256);
         // split path (b >= 2): x1 per compact position and the KB range partials
@@ -552,7 +552,7 @@ extern "C" cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, vo
                                               static_cast<cudaStream_t>(s));
     if (plan->p.kind == 1) return cuda_status(e);  // XS keeps no state between calls
     if (e == cudaSuccess)
-        e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_ypart, 0, (size_t)plan->p.max_batch * plan->p.d * 8,
+        e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_ypart, 0, (size_t)2 * plan->p.max_batch * plan->p.d * 8,
                             static_cast<cudaStream_t>(s));
     if (e == cudaSuccess)
         e = cudaMemsetAsync(static_cast<char *>(ws) + plan->p.off_tmask, 0, (size_t)((plan->p.m + 1) / 2) * 4,

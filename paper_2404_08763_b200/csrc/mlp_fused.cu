@@ -36,7 +36,8 @@
 //    bit-reproducible. (Replaces the paper's fp16 tl.atomic_add into Y.)
 //  * Split-K reduction: each CTA stages its integer partial in the (idle) ring and bulk-reduces it
 //    (TMA cp.reduce.async.bulk .add.u64) into one global accumulator; the last CTA converts it to
-//    fp32 once, writes y, re-zeroes the accumulator and re-arms the tile counter.
+//    fp32 once, writes y and re-arms the tile counter. Two accumulators alternate per call: the next
+//    call's CTAs zero the one just converted, so the last CTA only reads.
 //
 // Workspace outputs for introspection: tile tau's cnt[tau] active neurons are written ascending at
 // positions [tau*NR, tau*NR + cnt[tau]) of idx / tokmask / vals (v in fp32, 0 where |v| < t).
@@ -80,7 +81,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
              float *__restrict__ vals, int32_t *__restrict__ cnt, float *__restrict__ acts,
              unsigned long long *__restrict__ yacc, float *__restrict__ y, unsigned int *__restrict__ sched,
              int32_t *__restrict__ gidx, float *__restrict__ gval,
-             int lazy_tail, int eager, int l2pf, unsigned long long *__restrict__ trace) {
+             int ystride, int lazy_tail, int eager, int l2pf, unsigned long long *__restrict__ trace) {
     constexpr int NU = NR / 2;   // neurons per UD job (2 rows each) = the bytes of a GATE job
     constexpr int VEC = VecTraits<T>::kVec;
     constexpr int NW = k12_consumer_warps_c(B);
@@ -410,6 +411,17 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
     } else {
         // ===================================== CONSUMER WARPS ====================================
         pdl_wait_primary();     // x (and the accumulators) may come from the PDL predecessor
+        // Two int64 accumulators, alternating per decode (parity in sched[4]): the previous decode's
+        // converting CTA left its buffer dirty; this call's CTAs zero it here, a slice each, off the
+        // critical path (its conversion completed before griddepcontrol.wait returned), so the last
+        // CTA of a call only reads its accumulator.
+        const unsigned int par = *reinterpret_cast<volatile unsigned int *>(sched + 4) & 1u;
+        yacc += (size_t)par * ystride;
+        {
+            longlong2 *yo = reinterpret_cast<longlong2 *>(par ? yacc - ystride : yacc + ystride);
+            for (int c = (int)blockIdx.x * NC + tid; c < ystride / 2; c += (int)gridDim.x * NC)
+                yo[c] = make_longlong2(0, 0);
+        }
         uint4 xr[B][CPT];  // x, own chunks, packed (bf16 pairs or fp32), 0 past the row end
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
@@ -566,7 +578,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         // The CTA's exact int64 partial is staged in shared memory (the ring is idle after END)
         // and added into the global accumulator yacc[b][d] with cp.reduce.async.bulk .add.u64
         // (integer adds performed at L2, any order -> deterministic). The last CTA to finish converts
-        // yacc to fp32 once, writes y, and re-zeroes yacc and the tile scheduler for the next call.
+        // yacc to fp32 once, writes y, flips the accumulator parity and re-arms the tile scheduler.
         __shared__ unsigned int s_last;
         if (has_y) {
             consumer_barrier<NC>();  // every consumer warp is past its last job: the ring is idle
@@ -640,7 +652,6 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                         const int c = c0 + u * NC + tid;
                         if (c < n2) {
                             reinterpret_cast<float2 *>(y)[c] = make_float2(fix_to_float(v[u].x), fix_to_float(v[u].y));
-                            reinterpret_cast<longlong2 *>(yacc)[c] = make_longlong2(0, 0);
                         }
                     }
                 }
@@ -649,6 +660,7 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 sched[0] = 0u;
                 sched[1] = 0u;
                 if (list_mode) sched[3] = 0u;  // the idcs list was consumed: re-arm the append counter
+                if (has_y) sched[4] = par ^ 1u;  // the next decode accumulates into the other (zeroed) buffer
             }
         }
         trace_stamp(trace, 0, 3);
@@ -694,7 +706,7 @@ static cudaError_t launch_k12_t(const PlanData &p, const void *x, const void *Wg
         reinterpret_cast<uint8_t *>(w + p.off_tokmask), reinterpret_cast<float *>(w + p.off_vals),
         reinterpret_cast<int32_t *>(w + p.off_cnt), acts, reinterpret_cast<unsigned long long *>(w + p.off_ypart), y,
         reinterpret_cast<unsigned int *>(w + p.off_sched), reinterpret_cast<int32_t *>(w + p.off_gidx),
-        reinterpret_cast<float *>(w + p.off_gval), p.lazy_tail * k12_grid(p, B),
+        reinterpret_cast<float *>(w + p.off_gval), p.max_batch * p.d, p.lazy_tail * k12_grid(p, B),
         p.k12_eager, p.k12_l2pf,
         p.trace ? reinterpret_cast<unsigned long long *>(w + p.off_trace) : nullptr);
     if (e != cudaSuccess) return e;

@@ -9,5 +9,5 @@ IFS=';'; for spec in $SPECS; do
   IFS=' '; set -- $spec
   timeout 60 python scripts/time_decode.py --model $1 --m $2 --batch $3 --lib $lib --tag $lib >> $out 2>> gpurun_out/ab.err
 done; IFS=' '; done; done
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "k12 or app_d or fused_path or small or deterministic" > gpurun_out/ab_tests.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "k12 or app_d or fused_path or small or deterministic or mixed or decode_host or gate_act or t0" > gpurun_out/ab_tests.log 2>&1
 echo "tests rc=$?" >> gpurun_out/ab_tests.log
