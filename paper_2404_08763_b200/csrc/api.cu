@@ -436,7 +436,7 @@ cats_status_t plan_create(int d, int m, int max_batch, cats_dtype_t dt, int devi
         for (int b = p.split_min_b; b <= max_batch; ++b) {
             if (!split_supported(p, b)) continue;
             part_bytes = std::max(part_bytes, (size_t)split_ranges(p, b) * b * d * 4);
-            x1_bytes = std::max(x1_bytes, (size_t)k12_ntiles(p, b) * k12_rows_per_tile(p, b) * b * 4);
+            x1_bytes = std::max(x1_bytes, (size_t)split_ntiles(p, b) * split_rows_per_tile(p, b) * b * 4);
         }
         p.off_x1 = off;      off = align_up(off + x1_bytes, 256);
         p.off_tmask = off;   off = align_up(off + (size_t)((m + 1) / 2) * 4, 256);
@@ -722,8 +722,11 @@ extern "C" cats_status_t cats_mlp_last_active(const cats_mlp_plan_t *plan, const
             *nnz_union = k;
             return CATS_OK;
         }
-        // per-tile segments of k12_rows_per_tile rows (K12 and the split path share the tile geometry)
-        const int ntiles = k12_ntiles(p, b), nr = k12_rows_per_tile(p, b);
+        // per-tile segments: the tile geometry of the kernel that ran (K12, or KA's 8-row tiles in
+        // column parts on the split path)
+        const bool split = b >= p.split_min_b && split_supported(p, b);
+        const int ntiles = split ? split_ntiles(p, b) : k12_ntiles(p, b);
+        const int nr = split ? split_rows_per_tile(p, b) : k12_rows_per_tile(p, b);
         std::vector<int32_t> idx(p.m), cnt(ntiles);
         std::vector<uint8_t> tm(p.m);
         cudaError_t e = cudaSetDevice(p.device);

@@ -105,11 +105,12 @@ constexpr int kSplitAGroups = 2;                         // KA job streams per C
 constexpr int kSplitAThreads = (kSplitAWarps + kSplitAGroups) * 32;
 constexpr int kSplitBMaxThreads = 672;                   // KB: <= 20 consumer warps + 1 producer warp
 constexpr int kSplitFifo = 64;                           // KA active-neuron FIFO (power of two)
+constexpr int kSplitFifoCs = 128;                        // the same with 8-row tiles (ka_colsplit)
 constexpr int kKbReducers = 64;                          // KB: the last K CTAs to finish sum the partials
 
 template <int NR, int B>
-struct SplitDesc {   // one KA ring stage: GATE(tile) or UP(<= NR active neurons)
-    int type, tile, n;
+struct SplitDesc {   // one KA ring stage: GATE(tile) or UP(<= NR active neurons), column part `part`
+    int type, tile, n, part;
     int id[NR];      // UP: neuron ids
     int pos[NR];     // UP: compact positions (tile * NR + rank)
     float v[NR][B];  // UP: v = SiLU(u), 0 for tokens where |v| < t
@@ -122,6 +123,24 @@ struct SplitFifoEntry {  // one active neuron waiting for its UP job
 
 // KB on tensor cores (bf16, d a multiple of 1024: 4 column parts of 16-column tiles over 16 warps)
 constexpr int kSplitMmaMinB = 4;  // batches from which KA / KB use warp-level bf16 MMA (measured crossover)
+// KA's tensor-core path in column parts (bf16, b >= kSplitMmaMinB, d a multiple of kKaPartCols): tiles of
+// 8 rows -- all 8 columns of the m16n8k16 B operand distinct rows -- and every GATE / UP job streamed as
+// d / kKaPartCols consecutive ring stages of 8 rows x kKaPartCols columns, the consumers accumulating in
+// registers across the parts: x [b][d] is read (ldmatrix) once per 8 rows instead of once per NR.
+// Taken where full-row jobs would shrink to 2-row tiles (x leaves room for fewer than 2 stages of 4 rows
+// per job stream: d = 5120 from b = 6). Measured (A/B, one box): Llama2-13B b = 8 89.6 vs 112.9 us, the
+// TP8 shard at b = 8 25.8 vs 27.2; but at d = 4096 (4-row full-row jobs fit) 70.3 vs 59.4 us at b = 8:
+// next to x, the 8-row partial buffers and the larger FIFO only 3 stages of 16.5 KB fit per stream
+// (ncu: shared-memory wavefronts 54 -> 25 % of peak, but DRAM 4.1 -> 3.4 TB/s, consumers waiting on data).
+constexpr int kKaPartCols = 1024;
+inline bool ka_colsplit(const PlanData &p, int b) {
+    return p.esize == 2 && b >= kSplitMmaMinB && p.d % kKaPartCols == 0 && split_ka_stages_nr(p, b, 4) < 2;
+}
+// tile height of the split path (KA's tiles, KB's per-tile masks)
+inline int split_rows_per_tile(const PlanData &p, int b) { return ka_colsplit(p, b) ? 8 : k12_rows_per_tile(p, b); }
+inline int split_ntiles(const PlanData &p, int b) {
+    return (p.m + split_rows_per_tile(p, b) - 1) / split_rows_per_tile(p, b);
+}
 inline bool split_kb_mma(const PlanData &p, int b) {  // instantiated for 1, 4, 5 tiles per warp
     return b >= kSplitMmaMinB && p.esize == 2 && (p.d == 1024 || p.d == 4096 || p.d == 5120);
 }
@@ -149,7 +168,7 @@ inline int split_ranges(const PlanData &p, int b) {  // R: static ranges of the 
 }
 inline int split_kb_grid(const PlanData &p, int b) { return split_ranges(p, b) * split_q(p, b); }
 inline int split_ka_grid(const PlanData &p, int b) {
-    return std::max(1, std::min(p.num_sms, (k12_ntiles(p, b) + kSplitAGroups - 1) / kSplitAGroups));
+    return std::max(1, std::min(p.num_sms, (split_ntiles(p, b) + kSplitAGroups - 1) / kSplitAGroups));
 }
 int split_ka_ks(const PlanData &p, int b);
 size_t split_ka_smem(const PlanData &p, int b, int stages);

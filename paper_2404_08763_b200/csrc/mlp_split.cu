@@ -108,7 +108,10 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
     constexpr int NCG = NWG * 32;
     constexpr int NP = NR * B;          // (row, token) dot products per job
     constexpr int PP = pow2_ceil(NP);   // padded to a power of two for the reduce-scatter
-    static_assert(PP <= 32, "one lane per (row, token) pair");
+    constexpr bool CS = KS == 2;        // tensor cores in column parts (ka_colsplit)
+    constexpr int NS = CS ? (NP + 31) / 32 : 1;  // (row, token) pairs per producer lane
+    constexpr int FIFO = CS ? kSplitFifoCs : kSplitFifo;
+    static_assert(CS ? (NR == 8 && PP <= 64) : PP <= 32, "one or two (row, token) pairs per lane");
     constexpr uint32_t TKM = (1u << B) - 1u;
     using Desc = SplitDesc<NR, B>;
     using Ent = SplitFifoEntry<B>;
@@ -117,9 +120,12 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
     const int g = warp < NW ? warp / NWG : warp - NW;  // this warp's group
     const int nch = d * (int)sizeof(T) / 16;
     const uint32_t row_bytes = (uint32_t)d * (uint32_t)sizeof(T);
+    // column parts (CS): a job is H consecutive stages, part h = columns [h C, (h + 1) C), C = kKaPartCols
+    const int H = CS ? d / kKaPartCols : 1;
+    const uint32_t srow_bytes = CS ? (uint32_t)kKaPartCols * (uint32_t)sizeof(T) : row_bytes;  // a stage row
     // stage rows are padded by 16 B: the NR rows of a stage start in different shared-memory bank
     // groups (conflict-free ldmatrix) and the zeroed pad absorbs a half 16-wide k-step at the row end
-    const uint32_t rs_bytes = row_bytes + 16u;
+    const uint32_t rs_bytes = srow_bytes + 16u;
     const uint32_t stage_bytes = (uint32_t)NR * rs_bytes;
     const int ntiles = (m + NR - 1) / NR;
 
@@ -130,13 +136,14 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
     uint64_t *full0 = reinterpret_cast<uint64_t *>(ring0 + (size_t)NG * stages * stage_bytes);  // [NG][stages]
     uint64_t *empty0 = full0 + NG * stages;                                               // [NG][stages]
     Desc *desc0 = reinterpret_cast<Desc *>(empty0 + NG * stages);                         // [NG][stages]
-    Ent *fifo0 = reinterpret_cast<Ent *>(desc0 + NG * stages);                            // [NG][kSplitFifo]
-    float *red0 = reinterpret_cast<float *>(fifo0 + NG * kSplitFifo);                     // [NG][stages][NWG][PP]
+    Ent *fifo0 = reinterpret_cast<Ent *>(desc0 + NG * stages);                            // [NG][FIFO]
+    float *red0 = reinterpret_cast<float *>(fifo0 + NG * FIFO);                           // [NG][stages][NWG][PP]
+    Desc *jt0 = reinterpret_cast<Desc *>(red0 + (size_t)NG * stages * NWG * PP);          // CS: [NG] job in flight
     unsigned char *ring = ring0 + (size_t)g * stages * stage_bytes;
     uint64_t *full = full0 + g * stages;
     uint64_t *empty = empty0 + g * stages;
     Desc *desc = desc0 + g * stages;
-    Ent *fifo = fifo0 + g * kSplitFifo;
+    Ent *fifo = fifo0 + g * FIFO;
     float *red = red0 + (size_t)g * stages * NWG * PP;
 
     trace_stamp(trace, 0, 0);
@@ -151,7 +158,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
         fence_mbar_init();
     }
     for (int i = tid; i < NG * stages * NR; i += blockDim.x)  // row pads (never written by copies)
-        *reinterpret_cast<uint4 *>(ring0 + (size_t)i * rs_bytes + row_bytes) = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4 *>(ring0 + (size_t)i * rs_bytes + srow_bytes) = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
 
     if (warp >= NW) {
@@ -162,36 +169,78 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
         unsigned int res0 = kNoTileS, res1 = kNoTileS;  // reserved tiles (raw counter values)
         int rsel = 0;                                    // slot the next GATE issue uses
         const int nstreams = (int)gridDim.x * NG;  // job streams in the grid
-        const int batch = max(1, min(stages, ntiles / nstreams));
+        // static tiles per stream: enough to fill the ring (a tile is H stages in column parts)
+        const int batch = max(1, min((stages + H - 1) / H, ntiles / nstreams));
         const unsigned int dyn_base = (unsigned)nstreams * (unsigned)batch;
         int prod = 0, ps = 0, retire = 0;
         int q_head = 0, q_tail = 0;  // active-neuron FIFO (uniform across the warp)
         int gates_inflight = 0;
         bool ended = false;
+        Desc &J = jt0[g];            // CS: the job being streamed part by part
+        int cur_part = 0;            // CS: its next column part (0 = no job in progress)
 
+        // CS: stage s <- column part `part` of job J (descriptor copy, then one copy per row)
+        auto issue_part = [&](int s, int part) {
+            const int *src = reinterpret_cast<const int *>(&J);
+            int *dst = reinterpret_cast<int *>(&desc[s]);
+            for (int i = lane; i < (int)(sizeof(Desc) / 4); i += 32) dst[i] = src[i];
+            __syncwarp();
+            const int n = J.n;
+            if (lane == 0) {
+                desc[s].part = part;
+                mbar_arrive_expect_tx(&full[s], (uint32_t)n * srow_bytes);
+            }
+            __syncwarp();
+            if (lane < n) {
+                const size_t row = J.type == kSJobGate ? (size_t)(J.tile * NR + lane) : (size_t)J.id[lane];
+                bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)lane * rs_bytes,
+                         (J.type == kSJobGate ? Wg : Wu) + row * d + (size_t)part * kKaPartCols, srow_bytes,
+                         &full[s], policy);
+            }
+        };
         auto issue_up = [&](int n) {  // UP job: W_up rows of the next n FIFO neurons
             const int s = ps;
-            Desc &D = desc[s];
+            Desc &D = CS ? J : desc[s];
             if (lane < n) {
-                const Ent &E = fifo[(q_head + lane) & (kSplitFifo - 1)];
+                const Ent &E = fifo[(q_head + lane) & (FIFO - 1)];
                 D.id[lane] = E.id;
                 D.pos[lane] = E.pos;
 #pragma unroll
                 for (int tk = 0; tk < B; ++tk) D.v[lane][tk] = E.v[tk];
             }
-            if (lane == 0) {
-                D.type = kSJobUp;
-                D.n = n;
-                mbar_arrive_expect_tx(&full[s], (uint32_t)n * row_bytes);
+            if constexpr (CS) {
+                if (lane == 0) {
+                    J.type = kSJobUp;
+                    J.n = n;
+                }
+                __syncwarp();
+                issue_part(s, 0);
+                cur_part = H > 1 ? 1 : 0;
+            } else {
+                if (lane == 0) {
+                    D.type = kSJobUp;
+                    D.n = n;
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)n * row_bytes);
+                }
+                __syncwarp();
+                if (lane < n)
+                    bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)lane * rs_bytes, Wu + (size_t)D.id[lane] * d,
+                             row_bytes, &full[s], policy);
             }
-            __syncwarp();
-            if (lane < n)
-                bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)lane * rs_bytes, Wu + (size_t)D.id[lane] * d,
-                         row_bytes, &full[s], policy);
             q_head += n;
         };
         auto issue_job = [&]() -> bool {
             const int s = ps;
+            if constexpr (CS) {
+                if (cur_part != 0) {  // the next column part of the job in flight
+                    issue_part(s, cur_part);
+                    if (++cur_part == H) cur_part = 0;
+                    __syncwarp();
+                    ++prod;
+                    if (++ps == stages) ps = 0;
+                    return true;
+                }
+            }
             const int qn = q_tail - q_head;
             if (qn >= NR) {
                 issue_up(NR);
@@ -232,15 +281,28 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
                             claim_async(res1, sched, more);
                         }
                         rsel ^= 1;
-                        desc[s].type = kSJobGate;
-                        desc[s].tile = (int)tile;
-                        desc[s].n = nr;
-                        mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
                     }
-                    __syncwarp();
-                    if (lane < nr)  // one copy per (padded) row
-                        bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)lane * rs_bytes,
-                                 Wg + (size_t)(r0 + lane) * d, row_bytes, &full[s], policy);
+                    if constexpr (CS) {
+                        if (lane == 0) {
+                            J.type = kSJobGate;
+                            J.tile = (int)tile;
+                            J.n = nr;
+                        }
+                        __syncwarp();
+                        issue_part(s, 0);
+                        cur_part = H > 1 ? 1 : 0;
+                    } else {
+                        if (lane == 0) {
+                            desc[s].type = kSJobGate;
+                            desc[s].tile = (int)tile;
+                            desc[s].n = nr;
+                            mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
+                        }
+                        __syncwarp();
+                        if (lane < nr)  // one copy per (padded) row
+                            bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)lane * rs_bytes,
+                                     Wg + (size_t)(r0 + lane) * d, row_bytes, &full[s], policy);
+                    }
                     ++gates_inflight;
                 } else {
                     if (qn > 0) {
@@ -263,25 +325,39 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
             return true;
         };
 
+        int nstatic = 0;  // static tiles started
         if (lane == 0) {  // static first batch (weights only: safe before the PDL wait)
             const unsigned int base = (blockIdx.x * NG + g) * (unsigned)batch;
             for (int s = 0; s < batch; ++s) {
                 if (base + s >= (unsigned)ntiles) break;  // tiny layers: fewer tiles than streams
-                ++prod;
                 const int r0 = (int)(base + s) * NR;
                 const int nr = min(NR, m - r0);
-                desc[s].type = kSJobGate;
-                desc[s].tile = (int)(base + s);
-                desc[s].n = nr;
-                mbar_arrive_expect_tx(&full[s], (uint32_t)nr * row_bytes);
-                for (int r = 0; r < nr; ++r)
-                    bulk_g2s(ring + (size_t)s * stage_bytes + (size_t)r * rs_bytes, Wg + (size_t)(r0 + r) * d,
-                             row_bytes, &full[s], policy);
+                ++nstatic;
+                // CS: the tile's column parts in consecutive stages while the ring has room; a tile cut
+                // off by the ring's end continues from J / cur_part (the first dynamic issues)
+                for (int part = 0; part < H && prod < stages; ++part) {
+                    desc[prod].type = kSJobGate;
+                    desc[prod].tile = (int)(base + s);
+                    desc[prod].n = nr;
+                    desc[prod].part = part;
+                    mbar_arrive_expect_tx(&full[prod], (uint32_t)nr * srow_bytes);
+                    for (int r = 0; r < nr; ++r)
+                        bulk_g2s(ring + (size_t)prod * stage_bytes + (size_t)r * rs_bytes,
+                                 Wg + (size_t)(r0 + r) * d + (size_t)part * (srow_bytes / sizeof(T)), srow_bytes,
+                                 &full[prod], policy);
+                    ++prod;
+                    if (CS && part + 1 < H && prod == stages) {
+                        J = desc[prod - 1];
+                        cur_part = part + 1;
+                    }
+                }
             }
         }
         prod = __shfl_sync(0xffffffffu, prod, 0);
+        cur_part = __shfl_sync(0xffffffffu, cur_part, 0);
         ps = prod % stages;
-        gates_inflight = prod;
+        gates_inflight = __shfl_sync(0xffffffffu, nstatic, 0);
+        __syncwarp();
         pdl_wait_primary();
         pdl_launch_dependents();
         if (lane == 0) {
@@ -307,6 +383,80 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
             const Desc &D = desc[rs];
             if (trace) { if (D.type == kSJobGate) ++n_gate; else ++n_up; }
             const int n = D.n;
+            if constexpr (CS) {
+                // column parts: the consumers accumulate across a job's H stages and publish the warp
+                // partials with the last part; earlier parts only free their stage
+                if (D.part == H - 1) {
+                    float u[NS];
+                    bool ok[NS];
+#pragma unroll
+                    for (int j = 0; j < NS; ++j) {
+                        const int p = lane + 32 * j;
+                        ok[j] = p < NP && p / B < n;
+                        u[j] = 0.f;
+                        if (ok[j]) {
+                            const float *rb = red + (size_t)rs * NWG * PP + p;
+#pragma unroll
+                            for (int w = 0; w < NWG; ++w) u[j] += rb[w * PP];
+                        }
+                    }
+                    if (D.type == kSJobGate) {
+                        const int tile = D.tile, r0 = tile * NR;
+                        float v[NS];
+                        bool keep[NS];
+                        unsigned long long m64 = 0ull;  // bit p: pair p = (row p / B, token p % B) kept
+#pragma unroll
+                        for (int j = 0; j < NS; ++j) {
+                            v[j] = __fdividef(u[j], 1.0f + __expf(-u[j]));  // SiLU (Eq. 2)
+                            keep[j] = ok[j] && (dense || fabsf(v[j]) >= t);  // Eq. 4, ties kept
+                            m64 |= (unsigned long long)__ballot_sync(0xffffffffu, keep[j]) << (32 * j);
+                        }
+                        uint32_t rowact = 0;
+#pragma unroll
+                        for (int rr = 0; rr < NR; ++rr)
+                            if ((m64 >> (rr * B)) & TKM) rowact |= 1u << rr;
+                        const int nact = __popc(rowact);
+#pragma unroll
+                        for (int j = 0; j < NS; ++j) {
+                            const int p = lane + 32 * j, rj = p / B, tj = p % B;
+                            if (ok[j] && ((rowact >> rj) & 1u)) {
+                                const int rank = __popc(rowact & ((1u << rj) - 1u));
+                                const int pos = r0 + rank;
+                                const float vk = keep[j] ? v[j] : 0.f;
+                                vals[(size_t)pos * B + tj] = vk;
+                                Ent &E = fifo[(q_tail + rank) & (FIFO - 1)];
+                                E.v[tj] = vk;
+                                if (tj == 0) {
+                                    idx[pos] = r0 + rj;
+                                    tokmask[pos] = (uint8_t)((m64 >> (rj * B)) & TKM);
+                                    E.id = r0 + rj;
+                                    E.pos = pos;
+                                }
+                            }
+                        }
+                        if (lane == 0) {
+                            cnt[tile] = nact;
+                            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(tmask + tile),
+                                         "r"(0x80000000u | rowact)
+                                         : "memory");
+                        }
+                        q_tail += nact;
+                        --gates_inflight;
+                    } else {  // UP: x1 = (x W_up[j]) * v_j, per token
+#pragma unroll
+                        for (int j = 0; j < NS; ++j) {
+                            const int p = lane + 32 * j, rj = p / B, tj = p % B;
+                            if (ok[j]) x1out[(size_t)D.pos[rj] * B + tj] = u[j] * D.v[rj][tj];
+                        }
+                    }
+                }
+                __syncwarp();
+                ++retire;
+                if (++rs == stages) { rs = 0; rphase ^= 1u; }
+                while (!ended && prod < retire + stages && issue_job()) {
+                }
+                continue;
+            }
             const bool mine = lane < NP && r < n;
             float u = 0.f;
             if (mine) {
@@ -330,7 +480,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
                     const int pos = r0 + rank;
                     const float vk = keep ? v : 0.f;
                     vals[(size_t)pos * B + tk] = vk;
-                    Ent &E = fifo[(q_tail + rank) & (kSplitFifo - 1)];
+                    Ent &E = fifo[(q_tail + rank) & (FIFO - 1)];
                     E.v[tk] = vk;
                     if (tk == 0) {
                         idx[pos] = r0 + r;
@@ -387,6 +537,43 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
             }
             consumer_barrier<NC>();
             const int g4 = lane >> 2, t4 = lane & 3;
+            if constexpr (CS) {
+                // column parts: warp w owns k-steps [w SPW, (w + 1) SPW) of every part; the 8 B columns are
+                // the tile's 8 distinct rows; D accumulates over the job's H consecutive stages
+                constexpr int SPW = kKaPartCols / 16 / NWG;
+                static_assert(SPW % 2 == 0, "two k-steps per ldmatrix.x4");
+                const uint32_t koff = (uint32_t)(lane >> 3) * 16u + (uint32_t)(cwarp * SPW) * 32u;
+                const uint32_t arow =
+                    smem_u32(xs) + (uint32_t)((lane & 7) < B ? (lane & 7) : 0) * (row_bytes + 16u) + koff;
+                const uint32_t brow = (uint32_t)(lane & 7) * rs_bytes + koff;
+                float dacc[4] = {0.f, 0.f, 0.f, 0.f};
+                for (;;) {
+                    const unsigned long long cw0 = trace ? gtimer() : 0ull;
+                    mbar_wait(&full[s], phase);
+                    if (trace) c_wait += gtimer() - cw0;
+                    if (desc[s].type == kSJobEnd) break;
+                    const int part = desc[s].part;
+                    if (part == 0) dacc[0] = dacc[1] = dacc[2] = dacc[3] = 0.f;
+                    const uint32_t sb = smem_u32(ring + (size_t)s * stage_bytes) + brow;
+                    const uint32_t ab = arow + (uint32_t)part * srow_bytes;
+#pragma unroll
+                    for (int j = 0; j < SPW; j += 2) {
+                        uint32_t a0, a2, a4, a6, b0, b1, b2, b3;
+                        ldsm_x4(ab + (uint32_t)j * 32u, a0, a2, a4, a6);
+                        ldsm_x4(sb + (uint32_t)j * 32u, b0, b1, b2, b3);
+                        mma_bf16_16816(dacc, a0, a0, a2, a2, b0, b1);  // rows 8..15 of A: ignored copies
+                        mma_bf16_16816(dacc, a4, a4, a6, a6, b2, b3);
+                    }
+                    if (part == H - 1 && g4 < B) {  // lane (g4, t4): D[token g4][rows 2 t4, 2 t4 + 1]
+                        float *rb = red + ((size_t)s * NWG + cwarp) * PP;
+                        rb[(2 * t4) * B + g4] = dacc[0];
+                        rb[(2 * t4 + 1) * B + g4] = dacc[1];
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[s]);
+                    if (++s == stages) { s = 0; phase ^= 1u; }
+                }
+            } else {
             const int nsteps = (d + 15) / 16;
             const int spw = (nsteps + NWG - 1) / NWG;
             const int j0 = cwarp * spw, j1 = min(nsteps, j0 + spw);
@@ -417,6 +604,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
                 if (++s == stages) { s = 0; phase ^= 1u; }
+            }
             }
         } else {
         {
@@ -817,12 +1005,18 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
 // KA dot-product engine: 1 = warp-level bf16 MMA (bf16 weights, b >= kSplitMmaMinB), 0 = FHFMA.BF16 / FFMA.
 // Measured (Llama2-7B): the MMA path wins from b = 4 (b = 8: KA 58 -> 38 us); at b = 2 its ldmatrix
 // traffic (x re-read per job, half the B columns duplicated) makes it slower than FHFMA.
-int split_ka_ks(const PlanData &p, int b) { return (p.esize == 2 && b >= kSplitMmaMinB) ? 1 : 0; }
+// 2 = MMA in column parts (ka_colsplit: 8-row tiles, jobs of d / kKaPartCols stages)
+int split_ka_ks(const PlanData &p, int b) {
+    return ka_colsplit(p, b) ? 2 : (p.esize == 2 && b >= kSplitMmaMinB) ? 1 : 0;
+}
+static size_t ka_stage_row_bytes(const PlanData &p, int b) {  // bytes of one row in a ring stage (unpadded)
+    return (size_t)(ka_colsplit(p, b) ? kKaPartCols : p.d) * p.esize;
+}
 // KA shared memory: x [b][d] (FHFMA path only), then per group (kSplitAGroups): the ring of padded
 // rows, 2 mbarriers, a descriptor and the warp partial sums per stage, and the FIFO. `stages` counts
 // stages per group.
 static size_t split_ka_per_stage_nr(const PlanData &p, int b, int nr) {
-    const size_t desc = (3 + 2 * (size_t)nr + (size_t)nr * b) * 4;  // sizeof(SplitDesc<nr, b>)
+    const size_t desc = (4 + 2 * (size_t)nr + (size_t)nr * b) * 4;  // sizeof(SplitDesc<nr, b>)
     return (size_t)nr * ((size_t)p.d * p.esize + 16) + 16 + desc +
            (size_t)(kSplitAWarps / kSplitAGroups) * pow2_ceil(nr * b) * 4;
 }
@@ -835,15 +1029,19 @@ int split_ka_stages_nr(const PlanData &p, int b, int nr) {
     return (int)std::min<size_t>((kSmemBudget - fixed) / (kSplitAGroups * split_ka_per_stage_nr(p, b, nr)), kMaxStages);
 }
 static size_t split_ka_per_stage(const PlanData &p, int b) {
-    const int nr = k12_rows_per_tile(p, b);
-    const size_t desc = (3 + 2 * (size_t)nr + (size_t)nr * b) * 4;  // sizeof(SplitDesc<nr, b>)
-    return (size_t)nr * ((size_t)p.d * p.esize + 16) + 16 + desc +
+    const int nr = split_rows_per_tile(p, b);
+    const size_t desc = (4 + 2 * (size_t)nr + (size_t)nr * b) * 4;  // sizeof(SplitDesc<nr, b>)
+    return (size_t)nr * (ka_stage_row_bytes(p, b) + 16) + 16 + desc +
            (size_t)(kSplitAWarps / kSplitAGroups) * pow2_ceil(nr * b) * 4;
 }
 size_t split_ka_smem(const PlanData &p, int b, int stages) {
     const size_t ent = (2 + (size_t)b) * 4;  // sizeof(SplitFifoEntry<b>)
+    const size_t desc = (4 + 2 * (size_t)split_rows_per_tile(p, b) + (size_t)split_rows_per_tile(p, b) * b) * 4;
     const size_t xs = (size_t)b * ((size_t)p.d * p.esize + (split_ka_ks(p, b) > 0 ? 16 : 0));
-    return xs + kSplitAGroups * ((size_t)stages * split_ka_per_stage(p, b) + kSplitFifo * ent);
+    // column parts: one more descriptor per group (the job being streamed part by part)
+    const size_t fifo = split_ka_ks(p, b) == 2 ? kSplitFifoCs : kSplitFifo;
+    return xs + kSplitAGroups * ((size_t)stages * split_ka_per_stage(p, b) + fifo * ent +
+                                 (split_ka_ks(p, b) == 2 ? desc : 0));
 }
 int split_ka_stages(const PlanData &p, int b) {
     const size_t fixed = split_ka_smem(p, b, 0);
@@ -863,7 +1061,7 @@ static int split_kb_maxr(const PlanData &p, int b) {  // the largest (first) tap
 size_t split_kb_smem(const PlanData &p, int b, int stages) {
     const size_t seg = (size_t)split_part_cols(p, b) * p.esize + 16;  // padded rows
     const size_t stage = (size_t)split_kb_rows_per_stage(p, b) * seg;
-    const int ntiles = k12_ntiles(p, b);
+    const int ntiles = split_ntiles(p, b);
     const int maxr = split_kb_maxr(p, b);
     return (size_t)stages * stage + (size_t)stages * 16 + (size_t)(ntiles + 1 + 32) * 4 + (size_t)maxr * 8 +
            (size_t)maxr * b * 4 + (size_t)ntiles;
@@ -911,7 +1109,7 @@ static cudaLaunchConfig_t pdl_config(cudaLaunchAttribute *attr, int grid, int th
 template <typename T, int B, int NR, int KS>
 static cudaError_t launch_ka(const PlanData &p, const void *x, const void *Wg, const void *Wu, float t, int mode,
                              void *ws, cudaStream_t s) {
-    static_assert(sizeof(SplitDesc<NR, B>) == (3 + 2 * NR + NR * B) * 4, "split_ka_smem layout");
+    static_assert(sizeof(SplitDesc<NR, B>) == (4 + 2 * NR + NR * B) * 4, "split_ka_smem layout");
     static_assert(sizeof(SplitFifoEntry<B>) == (2 + B) * 4, "split_ka_smem layout");
     auto kern = ka_gate_up<T, B, NR, KS>;
     const int stages = split_ka_stages(p, B);
@@ -942,7 +1140,7 @@ static cudaError_t launch_kb(const PlanData &p, const void *Wd, float *y, void *
     cudaLaunchAttribute attr[1];
     const int threads = split_kb_consumers(p, B) + 32;
     cudaLaunchConfig_t cfg = pdl_config(attr, split_kb_grid(p, B), threads, smem, s);
-    return cudaLaunchKernelEx(&cfg, kern, static_cast<const T *>(Wd), p.d, k12_ntiles(p, B), k12_rows_per_tile(p, B),
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<const T *>(Wd), p.d, split_ntiles(p, B), split_rows_per_tile(p, B),
                               split_q(p, B), split_ranges(p, B), stages, split_kb_rows_per_stage(p, B),
                               split_kb_maxr(p, B), reinterpret_cast<unsigned int *>(w + p.off_tmask),
                               reinterpret_cast<const float *>(w + p.off_x1), reinterpret_cast<float *>(w + p.off_part), y,
@@ -970,9 +1168,9 @@ static cudaError_t launch_split_b(const PlanData &p, const void *x, const void *
     cudaError_t e;
     const int ks = split_ka_ks(p, B);
     if constexpr (sizeof(T) == 2 && B >= kSplitMmaMinB) {
-        (void)ks;
-        e = k12_rows_per_tile(p, B) == 4 ? launch_ka<T, B, 4, 1>(p, x, Wg, Wu, t, mode, ws, s)
-                                         : launch_ka<T, B, 2, 1>(p, x, Wg, Wu, t, mode, ws, s);
+        e = ks == 2 ? launch_ka<T, B, 8, 2>(p, x, Wg, Wu, t, mode, ws, s)
+            : k12_rows_per_tile(p, B) == 4 ? launch_ka<T, B, 4, 1>(p, x, Wg, Wu, t, mode, ws, s)
+                                           : launch_ka<T, B, 2, 1>(p, x, Wg, Wu, t, mode, ws, s);
     } else {
         const int nr = k12_rows_per_tile(p, B);
         if constexpr (B == 1) {  // b = 1 on large layers tiles by 6 rows (the split path at b = 1: options)

@@ -13,6 +13,10 @@ import numpy as np
 import torch
 
 import cats_synth
+
+if "--lib" in sys.argv:  # A/B experiments: load another build of the library (e.g. libcats_ab.so)
+    from paper_2404_08763_b200 import _lib as _l
+    _l.LIB_PATH = os.path.join(os.path.dirname(_l.LIB_PATH), sys.argv[sys.argv.index("--lib") + 1])
 import paper_2404_08763_b200 as cats
 
 ap = argparse.ArgumentParser()
@@ -23,6 +27,7 @@ ap.add_argument("--dense", action="store_true")
 ap.add_argument("--json")
 ap.add_argument("--m", type=int, default=0, help="override m (e.g. a TP shard)")
 ap.add_argument("--opt", action="append", default=[], help="plan option key=value, repeatable")
+ap.add_argument("--lib", default="", help="library file name in the package directory (A/B)")
 a = ap.parse_args()
 opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt}
 d, m = cats_synth.MODELS[a.model]

@@ -149,15 +149,24 @@ def test_parity_full_size(model, b, k, heavy):
 
 # Every kernel instantiation the planner selects for the BASELINE shapes: per model,
 # b = 1 -> K12 (NR = 6 at d = 4096, NR = 4 at d = 5120); b = 2, 3 -> KA + KB on CUDA cores; b = 4..8 ->
-# KA + KB on bf16 MMA (KB MT = 4 at d = 4096, MT = 5 at d = 5120). The batch is a template parameter, so
-# each (model, b) is a distinct kernel pair.
+# KA + KB on bf16 MMA (KB MT = 4 at d = 4096, MT = 5 at d = 5120; KA in column parts with 8-row tiles at
+# d = 5120 from b = 6). The batch is a template parameter, so each (model, b) is a distinct kernel pair.
 @pytest.mark.parametrize("model", ["mistral-7b", "llama2-7b", "llama2-13b"])
 @pytest.mark.parametrize("b", [2, 3, 4, 5, 6, 7, 8])
 def test_parity_every_planned_batch(model, b):
     d, m = cats_synth.MODELS[model]
     k = {2: 0.5, 3: 0.7, 4: 0.5, 5: 0.9, 6: 0.7, 7: 0.5, 8: 0.5}[b]
     res, _ = run_parity(d, m, b, torch.bfloat16, k, seed=50 + b, heavy=(b % 2 == 1))
-    # the split path KA + KB (Llama2-13B d = 5120 from b = 6: 2-row tiles so that KA's ring fits)
+    # the split path KA + KB (Llama2-13B d = 5120 from b = 6: KA in column parts, 8-row tiles)
+    assert res["kernels"] == 2
+
+
+@pytest.mark.parametrize("m", [1003, 77, 8])
+@pytest.mark.parametrize("b", [6, 8])
+def test_parity_ka_column_parts_ragged(m, b):
+    """KA in column parts (d = 5120, b >= 6: 8-row tiles, each job streamed as 5 stages of 1024 columns)
+    on ragged and tiny layers: a last tile of 3 rows, fewer tiles than job streams, one tile."""
+    res, _ = run_parity(5120, m, b, torch.bfloat16, 0.5, seed=90 + m + b)
     assert res["kernels"] == 2
 
 
