@@ -145,7 +145,8 @@ inline bool split_kb_mma(const PlanData &p, int b) {  // instantiated for 1, 4, 
     return b >= kSplitMmaMinB && p.esize == 2 && (p.d == 1024 || p.d == 4096 || p.d == 5120);
 }
 // scheduler words at the workspace base: [0..1] tile counter / CTA exits, [2] KB arrival tickets,
-// [3] App. D Alg. 1 append counter, [8 + q] KB range tickets of column part q (q < 16)
+// [3] App. D Alg. 1 append counter, [4] K12 accumulator parity, [5] tokens the last K12 call left in the
+// other accumulator, [8 + q] KB range tickets of column part q (q < 16)
 constexpr size_t kSchedBytes = 128;
 inline int split_q(const PlanData &p, int b) {  // KB column parts (<= 16)
     if (split_kb_mma(p, b)) return 4;

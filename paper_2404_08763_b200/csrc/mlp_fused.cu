@@ -412,14 +412,15 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
         // ===================================== CONSUMER WARPS ====================================
         pdl_wait_primary();     // x (and the accumulators) may come from the PDL predecessor
         // Two int64 accumulators, alternating per decode (parity in sched[4]): the previous decode's
-        // converting CTA left its buffer dirty; this call's CTAs zero it here, a slice each, off the
-        // critical path (its conversion completed before griddepcontrol.wait returned), so the last
-        // CTA of a call only reads its accumulator.
+        // converting CTA left the first sched[5] x d words of its buffer dirty; this call's CTAs zero
+        // them here, a slice each, off the critical path (that conversion completed before
+        // griddepcontrol.wait returned), so the last CTA of a call only reads its accumulator.
         const unsigned int par = *reinterpret_cast<volatile unsigned int *>(sched + 4) & 1u;
+        const int dirty = min(ystride, (int)*reinterpret_cast<volatile unsigned int *>(sched + 5) * d);
         yacc += (size_t)par * ystride;
         {
             longlong2 *yo = reinterpret_cast<longlong2 *>(par ? yacc - ystride : yacc + ystride);
-            for (int c = (int)blockIdx.x * NC + tid; c < ystride / 2; c += (int)gridDim.x * NC)
+            for (int c = (int)blockIdx.x * NC + tid; c < dirty / 2; c += (int)gridDim.x * NC)
                 yo[c] = make_longlong2(0, 0);
         }
         uint4 xr[B][CPT];  // x, own chunks, packed (bf16 pairs or fp32), 0 past the row end
@@ -660,7 +661,10 @@ k12_cats_mlp(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restr
                 sched[0] = 0u;
                 sched[1] = 0u;
                 if (list_mode) sched[3] = 0u;  // the idcs list was consumed: re-arm the append counter
-                if (has_y) sched[4] = par ^ 1u;  // the next decode accumulates into the other (zeroed) buffer
+                if (has_y) {
+                    sched[4] = par ^ 1u;     // the next decode accumulates into the other (zeroed) buffer
+                    sched[5] = (unsigned)B;  // ... and zeroes these B x d words of this one
+                }
             }
         }
         trace_stamp(trace, 0, 3);
