@@ -224,7 +224,8 @@ def test_kernels_per_call_path_choice():
     toy = cats.MlpPlan(64, 176, max_batch=3, dtype=torch.float32, num_sms=148)
     assert cats.cats_mlp_kernels_per_call(toy, 3) == 2
     wide = cats.MlpPlan(8192, 512, max_batch=8, dtype=torch.bfloat16, num_sms=148)
-    assert cats.cats_mlp_kernels_per_call(wide, 8) == 1  # x alone would take 128 KB of KA's shared memory
+    # x takes 128 KB of KA's shared memory: full-row stages no longer fit, 8 x 1024-column parts do
+    assert cats.cats_mlp_kernels_per_call(wide, 8) == 2
     with pytest.raises(cats.CatsError) as e:
         cats.cats_mlp_kernels_per_call(p, 9)
     assert e.value.name == "CATS_E_BATCH"

@@ -161,12 +161,13 @@ def test_parity_every_planned_batch(model, b):
     assert res["kernels"] == 2
 
 
-@pytest.mark.parametrize("m", [1003, 77, 8])
+@pytest.mark.parametrize("d,m", [(5120, 1003), (5120, 77), (5120, 8), (8192, 512)])
 @pytest.mark.parametrize("b", [6, 8])
-def test_parity_ka_column_parts_ragged(m, b):
-    """KA in column parts (d = 5120, b >= 6: 8-row tiles, each job streamed as 5 stages of 1024 columns)
-    on ragged and tiny layers: a last tile of 3 rows, fewer tiles than job streams, one tile."""
-    res, _ = run_parity(5120, m, b, torch.bfloat16, 0.5, seed=90 + m + b)
+def test_parity_ka_column_parts_ragged(d, m, b):
+    """KA in column parts (d = 5120, b >= 6: 8-row tiles, each job streamed as 5 stages of 1024 columns;
+    d = 8192: 8 parts, two stages per stream next to 128 KB of x) on ragged and tiny layers: a last tile of
+    3 rows, fewer tiles than job streams, one tile."""
+    res, _ = run_parity(d, m, b, torch.bfloat16, 0.5, seed=90 + m + b)
     assert res["kernels"] == 2
 
 
