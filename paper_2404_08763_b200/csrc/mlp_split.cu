@@ -587,7 +587,8 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
                 if (trace) c_wait += gtimer() - cw0;
                 if (desc[s].type == kSJobEnd) break;
                 const uint32_t sb = smem_u32(ring + (size_t)s * stage_bytes) + brow;
-                float dacc[4] = {0.f, 0.f, 0.f, 0.f};
+                // two accumulator chains (even / odd k-steps): half the dependent-MMA latency per stage
+                float dacc[4] = {0.f, 0.f, 0.f, 0.f}, dacc2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
                 for (int j = j0; j < j1; j += 2) {
                     const uint32_t o = (uint32_t)(j - j0) * 32u;
@@ -595,12 +596,12 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
                     ldsm_x4(arow + o, a0, a2, a4, a6);  // steps j (a0, a2) and j + 1 (a4, a6)
                     ldsm_x4(sb + o, b0, b1, b2, b3);    // steps j (b0, b1) and j + 1 (b2, b3)
                     mma_bf16_16816(dacc, a0, a0, a2, a2, b0, b1);  // rows 8..15 of A: ignored copies
-                    if (j + 1 < j1) mma_bf16_16816(dacc, a4, a4, a6, a6, b2, b3);
+                    if (j + 1 < j1) mma_bf16_16816(dacc2, a4, a4, a6, a6, b2, b3);
                 }
                 // lane (g4, t4) holds D[token g4][row 2 t4] and D[g4][2 t4 + 1]
                 float *rb = red + ((size_t)s * NWG + cwarp) * PP;
-                if (g4 < B && 2 * t4 < NR) rb[(2 * t4) * B + g4] = dacc[0];
-                if (g4 < B && 2 * t4 + 1 < NR) rb[(2 * t4 + 1) * B + g4] = dacc[1];
+                if (g4 < B && 2 * t4 < NR) rb[(2 * t4) * B + g4] = dacc[0] + dacc2[0];
+                if (g4 < B && 2 * t4 + 1 < NR) rb[(2 * t4 + 1) * B + g4] = dacc[1] + dacc2[1];
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
                 if (++s == stages) { s = 0; phase ^= 1u; }
