@@ -464,9 +464,27 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
 #pragma unroll
                 for (int w = 0; w < NWG; ++w) u += rb[w * PP];
             }
-            if (D.type == kSJobGate) {
+            // everything the retire needs from the stage's descriptor and partials; on the tensor-core
+            // path the stage is refilled first, so its load latency starts before the retire arithmetic
+            // (the refill may not see this job's FIFO entries yet; they go out with the next issue).
+            // Measured (A/B): 1-1.4 % faster at b = 4 / 8; on the FHFMA path (b <= 3) 1-2.6 % slower.
+            const int jtype = D.type, jtile = D.tile;
+            int jpos = 0;
+            float jv = 0.f;
+            if (mine && jtype != kSJobGate) {
+                jpos = D.pos[r];
+                jv = D.v[r][tk];
+            }
+            __syncwarp();
+            ++retire;
+            if (++rs == stages) { rs = 0; rphase ^= 1u; }
+            if constexpr (KS == 1) {
+                while (!ended && prod < retire + stages && issue_job()) {
+                }
+            }
+            if (jtype == kSJobGate) {
                 // u -> v = SiLU(u) (Eq. 2) -> keep = |v| >= t (Eq. 4, ties kept) -> compaction
-                const int tile = D.tile, r0 = tile * NR;
+                const int tile = jtile, r0 = tile * NR;
                 const float v = __fdividef(u, 1.0f + __expf(-u));
                 const bool keep = mine && (dense || fabsf(v) >= t);
                 const uint32_t bal = __ballot_sync(0xffffffffu, keep);
@@ -499,11 +517,9 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
                 q_tail += nact;
                 --gates_inflight;
             } else if (mine) {  // UP: x1 = (x W_up[j]) * v_j, per token
-                x1out[(size_t)D.pos[r] * B + tk] = u * D.v[r][tk];
+                x1out[(size_t)jpos * B + tk] = u * jv;
             }
             __syncwarp();
-            ++retire;
-            if (++rs == stages) { rs = 0; rphase ^= 1u; }
             while (!ended && prod < retire + stages && issue_job()) {
             }
         }
