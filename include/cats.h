@@ -271,6 +271,20 @@ cats_status_t cats_mlp_decode_host(const cats_mlp_plan_t *plan, const void *x_ho
                                    const void *W_gate, const void *W_up, const void *W_down_nm,
                                    float t, float *y_host, void *ws, size_t ws_bytes, cats_stream_t s);
 
+/* A bound end-to-end call for a serving loop: the work of cats_mlp_decode_host for fixed arguments,
+ * captured once into a CUDA graph (the x staging kernel, the decode kernels chained by programmatic
+ * dependent launch, y written by the kernel into host memory), replayed by cats_mlp_host_call_run, which
+ * BLOCKS until y_host holds the call's y. Every run re-reads the CURRENT contents of x_host; weights, t,
+ * the workspace and the stream are fixed at creation. x_host and y_host must be pinned and mapped
+ * (cudaHostAlloc / cudaHostRegister; torch's pin_memory()), else CATS_E_UNSUPPORTED. Creation validates
+ * like cats_mlp_decode_host and runs the call once (uncaptured). Not thread-safe per handle. */
+typedef struct cats_mlp_host_call cats_mlp_host_call_t;
+cats_status_t cats_mlp_host_call_create(const cats_mlp_plan_t *plan, const void *x_host, int b, const void *W_gate,
+                                        const void *W_up, const void *W_down_nm, float t, float *y_host, void *ws,
+                                        size_t ws_bytes, cats_stream_t s, cats_mlp_host_call_t **out);
+cats_status_t cats_mlp_host_call_run(cats_mlp_host_call_t *call);
+void cats_mlp_host_call_destroy(cats_mlp_host_call_t *call);
+
 /* Measurement variant of cats_mlp_decode: the identical launch bracketed by events[0] and events[1]
  * (cudaEvent_t created by the caller with timing enabled; events[2] is recorded right after
  * events[1]) -- the kernel's device time for the roofline report. */

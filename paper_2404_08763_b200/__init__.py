@@ -335,7 +335,8 @@ def cats_mlp_decode_host(plan: MlpPlan, x_host: torch.Tensor, W_gate, W_up, W_do
 class BoundDecodeHost:
     """cats_mlp_decode_host with its arguments validated and marshalled once (a serving loop's per-token
     call): every call copies the CURRENT contents of x_host to the device, decodes and delivers y into
-    y_host, blocking on the stream -- the C ABI call alone, without re-checking tensors each token."""
+    y_host, blocking on the stream. With pinned x_host and y_host the call is the library's bound host call
+    (cats_mlp_host_call_*: one CUDA graph replay per call); otherwise cats_mlp_decode_host per call."""
 
     def __init__(self, plan: MlpPlan, x_host, W_gate, W_up, W_down_nm, t: float, y_host=None, ws=None, stream=None):
         # one validated call through the regular path (allocates y_host / ws if needed)
@@ -345,13 +346,26 @@ class BoundDecodeHost:
         ws = ws if ws is not None else plan.workspace(stream=stream)
         st = _stream_obj(stream, torch.device(f"cuda:{plan.device}"))
         self._keep = (plan, x_host, W_gate, W_up, W_down_nm, ws, st)  # lifetimes
-        self._fn = plan._lib.cats_mlp_decode_host
-        self._args = (plan.handle, x2.data_ptr(), x2.shape[0], W_gate.data_ptr(), W_up.data_ptr(), W_down_nm.data_ptr(),
-                      float(t), self.y_host.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)
+        self._lib = plan._lib
+        args = (plan.handle, x2.data_ptr(), x2.shape[0], W_gate.data_ptr(), W_up.data_ptr(), W_down_nm.data_ptr(),
+                float(t), self.y_host.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)
+        self._call = None
+        if x_host.is_pinned() and self.y_host.is_pinned():
+            h = ctypes.c_void_p()
+            _check(self._lib.cats_mlp_host_call_create(*args, ctypes.byref(h)), "cats_mlp_host_call_create")
+            self._call = h
+            self._fn, self._args = self._lib.cats_mlp_host_call_run, (h,)
+        else:
+            self._fn, self._args = self._lib.cats_mlp_decode_host, args
 
     def __call__(self) -> torch.Tensor:
-        _check(self._fn(*self._args), "cats_mlp_decode_host")
+        _check(self._fn(*self._args), "cats_mlp_host_call_run" if self._call is not None else "cats_mlp_decode_host")
         return self.y_host
+
+    def __del__(self):
+        if getattr(self, "_call", None) is not None:
+            self._lib.cats_mlp_host_call_destroy(self._call)
+            self._call = None
 
 
 def cats_mlp_gate_act(plan: MlpPlan, x, W_gate, acts=None, ws=None, stream=None):

@@ -74,6 +74,9 @@ _SIGS = {
     "cats_mlp_decode_profiled": (I, [P, P, I, P, P, P, F, P, P, SZ, P, P]),
     "cats_mlp_dense": (I, [P, P, I, P, P, P, P, P, SZ, P]),
     "cats_mlp_decode_host": (I, [P, P, I, P, P, P, F, P, P, SZ, P]),
+    "cats_mlp_host_call_create": (I, [P, P, I, P, P, P, F, P, P, SZ, P, P]),
+    "cats_mlp_host_call_run": (I, [P]),
+    "cats_mlp_host_call_destroy": (None, [P]),
     "cats_mlp_gate_act": (I, [P, P, I, P, P, P, SZ, P]),
     "cats_mlp_last_active": (I, [P, P, I, P, P, P, P, P]),
     "cats_mlp_trace_info": (I, [P, P, P]),

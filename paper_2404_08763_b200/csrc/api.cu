@@ -680,6 +680,83 @@ extern "C" cats_status_t cats_mlp_decode_host(const cats_mlp_plan_t *plan, const
     return cuda_status(e);
 }
 
+struct cats_mlp_host_call {
+    cudaGraphExec_t exec;
+    cudaStream_t stream;
+    int device;
+};
+
+extern "C" cats_status_t cats_mlp_host_call_create(const cats_mlp_plan_t *plan, const void *x_host, int b,
+                                                   const void *W_gate, const void *W_up, const void *W_down_nm,
+                                                   float t, float *y_host, void *ws, size_t ws_bytes, cats_stream_t s,
+                                                   cats_mlp_host_call_t **out) {
+    if (!out) return CATS_E_NULL;
+    *out = nullptr;
+    // validation, attribute setup and one uncaptured call (also the pageable-buffer errors)
+    cats_status_t rc = cats_mlp_decode_host(plan, x_host, b, W_gate, W_up, W_down_nm, t, y_host, ws, ws_bytes, s);
+    if (rc != CATS_OK) return rc;
+    const PlanData &p = plan->p;
+    auto mapped = [](const void *h) -> void * {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, h) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer &&
+            aligned16(pa.devicePointer))
+            return pa.devicePointer;
+        (void)cudaGetLastError();
+        return nullptr;
+    };
+    const void *xm = mapped(x_host);
+    float *ym = static_cast<float *>(mapped(y_host));
+    if (!xm || !ym) return CATS_E_UNSUPPORTED;
+    cudaStream_t st = static_cast<cudaStream_t>(s);
+    char *w = static_cast<char *>(ws);
+    void *xd = w + p.off_xstage;
+    // captured on a private stream (s may be the legacy default stream, which cannot capture); the graph
+    // is launched on s. The uncaptured call above has completed (it blocks), so nothing is pending.
+    cudaStream_t cs = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_status(e);
+    e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    cats_status_t rr = CATS_OK;
+    if (e == cudaSuccess) {
+        e = launch_x_stage(xm, xd, (size_t)b * p.d * p.esize, cs);
+        if (e == cudaSuccess) rr = run_mlp(p, xd, b, W_gate, W_up, W_down_nm, t, 0, ym, ws, cs);
+        const cudaError_t ee = cudaStreamEndCapture(cs, &graph);
+        if (e == cudaSuccess) e = ee;
+    }
+    if (e == cudaSuccess && rr == CATS_OK) e = cudaGraphInstantiate(&exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    cudaStreamDestroy(cs);
+    if (e != cudaSuccess || rr != CATS_OK) {
+        const cats_status_t out_rc = e != cudaSuccess ? cuda_status(e) : rr;
+        (void)cudaGetLastError();  // a failed capture must not leak into the next call's launch checks
+        return out_rc;
+    }
+    cats_mlp_host_call_t *c = new (std::nothrow) cats_mlp_host_call{exec, st, p.device};
+    if (!c) {
+        cudaGraphExecDestroy(exec);
+        g_last_cuda_error = "host allocation failed";
+        return CATS_E_CUDA;
+    }
+    *out = c;
+    return CATS_OK;
+}
+
+extern "C" cats_status_t cats_mlp_host_call_run(cats_mlp_host_call_t *c) {
+    if (!c) return CATS_E_NULL;
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e == cudaSuccess) e = cudaGraphLaunch(c->exec, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    return cuda_status(e);
+}
+
+extern "C" void cats_mlp_host_call_destroy(cats_mlp_host_call_t *c) {
+    if (!c) return;
+    cudaGraphExecDestroy(c->exec);
+    delete c;
+}
+
 extern "C" cats_status_t cats_mlp_gate_act(const cats_mlp_plan_t *plan, const void *x, int b, const void *W_gate,
                                            float *acts, void *ws, size_t ws_bytes, cats_stream_t s) {
     if (!plan || !x || !W_gate || !acts) return CATS_E_NULL;

@@ -338,3 +338,23 @@ def test_tp_comm_validation_without_gpu():
         assert lib.cats_status_string(lib.cats_tp_buffer_alloc(1024, 0, ctypes.byref(pb))).decode() == "CATS_E_CUDA"
     bad = (ctypes.c_void_p * 2)(FAKE, FAKE + 4)
     assert lib.cats_status_string(lib.cats_tp_comm_create(0, 2, 5120, bad, 0, ctypes.byref(h))).decode() == "CATS_E_ALIGN"
+
+
+def test_host_call_validation_before_cuda():
+    """cats_mlp_host_call_create validates like cats_mlp_decode_host before touching the device."""
+    p = cats.MlpPlan(4096, 14336, max_batch=2, dtype=torch.bfloat16, num_sms=148)
+    h = ctypes.c_void_p()
+
+    def rc(*args):
+        return lib.cats_status_string(lib.cats_mlp_host_call_create(*args)).decode()
+
+    wsb = p.workspace_bytes
+    assert rc(p.handle, FAKE, 1, FAKE, FAKE, FAKE, 0.1, FAKE, FAKE, wsb, None, None) == "CATS_E_NULL"
+    assert rc(None, FAKE, 1, FAKE, FAKE, FAKE, 0.1, FAKE, FAKE, wsb, None, ctypes.byref(h)) == "CATS_E_NULL"
+    assert rc(p.handle, None, 1, FAKE, FAKE, FAKE, 0.1, FAKE, FAKE, wsb, None, ctypes.byref(h)) == "CATS_E_NULL"
+    assert rc(p.handle, FAKE, 3, FAKE, FAKE, FAKE, 0.1, FAKE, FAKE, wsb, None, ctypes.byref(h)) == "CATS_E_BATCH"
+    assert rc(p.handle, FAKE, 1, FAKE, FAKE, FAKE, 0.1, FAKE, FAKE, wsb - 1, None, ctypes.byref(h)) == "CATS_E_WORKSPACE"
+    assert rc(p.handle, FAKE, 1, FAKE, FAKE, FAKE, -1.0, FAKE, FAKE, wsb, None, ctypes.byref(h)) == "CATS_E_THRESHOLD"
+    assert h.value is None
+    assert lib.cats_status_string(lib.cats_mlp_host_call_run(None)).decode() == "CATS_E_NULL"
+    lib.cats_mlp_host_call_destroy(None)  # no-op

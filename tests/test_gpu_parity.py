@@ -6,6 +6,7 @@ Acceptance (BASELINE.json north_star):
     those band entries only (reading R9);
   * calibration threshold bit-exact with the oracle's order statistic (and its counts).
 """
+import ctypes
 import os
 from concurrent.futures import ThreadPoolExecutor
 
@@ -307,11 +308,18 @@ def test_decode_host_equals_device_path():
     x1 = x[:1].clone()                                                            # b = 1 (K12), pinned
     y1 = cats.cats_mlp_decode_host(plan, x1.pin_memory(), Wg, Wu, Wd, 0.1, ws=ws)
     assert torch.equal(cats.cats_mlp_decode(plan, _dev(x1), Wg, Wu, Wd, 0.1, ws=ws).cpu(), y1)
-    xp = x.pin_memory()                                                           # bound call: x re-read each call
-    call = cats.BoundDecodeHost(plan, xp, Wg, Wu, Wd, 0.1, ws=ws)
-    x2 = cats_synth.tokens(b, d, torch.bfloat16, seed=10)
-    xp.copy_(x2)
-    assert torch.equal(call().clone(), cats.cats_mlp_decode(plan, _dev(x2), Wg, Wu, Wd, 0.1, ws=ws).cpu())
+    for bb in (b, 1):  # bound call (graph replay of x staging + KA/KB or K12): x re-read on every call
+        xp = x[:bb].clone().pin_memory()
+        call = cats.BoundDecodeHost(plan, xp, Wg, Wu, Wd, 0.1, ws=ws)
+        assert call._call is not None
+        for seed in (10, 11, 12):
+            x2 = cats_synth.tokens(bb, d, torch.bfloat16, seed=seed)
+            xp.copy_(x2)
+            assert torch.equal(call().clone(), cats.cats_mlp_decode(plan, _dev(x2), Wg, Wu, Wd, 0.1, ws=ws).cpu())
+    h = ctypes.c_void_p()                                                         # pageable buffers: not bindable
+    rc = plan._lib.cats_mlp_host_call_create(plan.handle, x.data_ptr(), b, Wg.data_ptr(), Wu.data_ptr(), Wd.data_ptr(),
+                                             0.1, y_pageable.data_ptr(), ws.data_ptr(), ws.numel(), None, ctypes.byref(h))
+    assert plan._lib.cats_status_string(rc).decode() == "CATS_E_UNSUPPORTED" and h.value is None
 
 
 def test_tensor_parallel_emulated_on_one_gpu():
