@@ -533,6 +533,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
         // ===================================== CONSUMER WARPS ====================================
         pdl_wait_primary();  // x may come from the predecessor
         pdl_launch_dependents();
+        trace_stamp(trace, 0, 4);  // this CTA's consumers have released KB's launch
         const int ctid = tid - g * NCG;  // consumer thread index within the group
         const int cwarp = warp - g * NWG;
         int s = 0;
@@ -779,26 +780,25 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     // computes which range does not change a bit of y.
     if (tid == 0) s_rr = (int)rr_ticket;
     __syncthreads();
+    trace_stamp(trace, 1, 7);  // range ticket known
     const int rr = s_rr;
     const long long U = pre[ntiles];
     auto wcum = [R](long long r) { return r * (4LL * R + 1) - r * (r - 1) / 2; };  // sum_{i<r} (4R - i)
     const int lo = (int)(U * wcum(rr) / wcum(R)), hi = (int)(U * wcum(rr + 1) / wcum(R)), len = hi - lo;
     CATS_DCHECK(rr < R && 0 <= lo && lo <= hi && hi <= U && len <= maxr);
 
-    // ---- this range's neurons: compact rank g -> (tile, k) by binary search; neuron = k-th set row ----
-    for (int i = tid; i < len; i += nth) {
-        const int g = lo + i;
-        int a = 0, b = ntiles;  // largest tau with pre[tau] <= g
-        while (b - a > 1) {
-            const int mid = (a + b) >> 1;
-            if (pre[mid] <= g) a = mid; else b = mid;
+    // ---- this range's neurons: one thread per tile scatters the tile's active rows whose compact ranks
+    //      g = pre[tau] + k fall in [lo, hi) (no search: every tile is one independent shared-memory read) ----
+    for (int tau = tid; tau < ntiles; tau += nth) {
+        const int p0 = pre[tau], p1 = pre[tau + 1];
+        if (p1 <= lo || p0 >= hi) continue;
+        unsigned int msk = rowm[tau];
+        for (int g = p0; g < p1; ++g, msk &= msk - 1u) {  // k-th set row of the tile = rank p0 + k
+            if (g < lo || g >= hi) continue;
+            lj[g - lo] = tau * nr_tile + (__ffs(msk) - 1);
+            lpos[g - lo] = tau * nr_tile + (g - p0);
+            CATS_DCHECK(msk != 0u && g - p0 < nr_tile);
         }
-        const int k = g - pre[a];
-        unsigned int msk = rowm[a];
-        for (int j = 0; j < k; ++j) msk &= msk - 1u;  // drop the k lowest set rows
-        lj[i] = a * nr_tile + (__ffs(msk) - 1);
-        lpos[i] = a * nr_tile + k;
-        CATS_DCHECK(msk != 0u && k < nr_tile);
     }
     __syncthreads();
     trace_stamp(trace, 1, 1);

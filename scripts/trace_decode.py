@@ -65,8 +65,8 @@ torch.cuda.synchronize()
 tr = ws[off.value:off.value + nbytes.value].cpu().numpy().view(np.uint64).reshape(3, 512, 8).astype(np.int64)
 rep = {}
 t0 = None
-names = {0: ["start", "primed", "jobs_done", "exit", "reduced", "all_warps_done", "staged", "bulk_done"],
-         1: ["start", "list_ready", "jobs_done", "reducer_go", "exit", "masks_read", "prefix_done"]}
+names = {0: ["start", "primed", "jobs_done", "exit", "reduced|KA:pdl_trig", "all_warps_done", "staged", "bulk_done"],
+         1: ["start", "list_ready", "jobs_done", "reducer_go", "exit", "masks_read", "prefix_done", "ticket_known"]}
 titles = {0: "K12 / KA", 1: "KB"}
 for k in range(2):
     g = int((tr[k, :, 0] > 0).sum())  # CTAs that stamped
