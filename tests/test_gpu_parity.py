@@ -466,3 +466,25 @@ def test_mixed_batches_share_one_workspace():
         assert torch.equal(y_shared, y_fresh), b
         y_dense = cats.cats_mlp_dense(plan, x, Wg, Wu, Wd, ws=ws)
         assert torch.isfinite(y_dense).all()
+
+
+@pytest.mark.parametrize("opts", [{"path": cats.CATS_PATH_FUSED}, {"compaction": cats.CATS_COMPACT_ATOMIC}])
+def test_k12_alternating_accumulators_across_batches_and_gate_calls(opts):
+    """K12's two int64 accumulators alternate per call, and each call zeroes the rows the previous one
+    left in the other (a batch-dependent extent): K12 at changing batch sizes, with gate-only
+    (calibration collection) launches in between, gives the same bits as fresh workspaces."""
+    d, m = 2048, 3000
+    Wg, Wu, Wd = (_dev(a) for a in cats_synth.mlp_weights(d, m, torch.bfloat16, layer=5))
+    plan = cats.MlpPlan(d, m, max_batch=8, **opts)
+    ws = plan.workspace()
+    for i, b in enumerate([3, 1, 8, 2, 1, 1, 6]):
+        x = _dev(cats_synth.tokens(b, d, torch.bfloat16, seed=70 + i))
+        assert cats.cats_mlp_kernels_per_call(plan, b) == (2 if "compaction" in opts else 1)
+        y_shared = cats.cats_mlp_decode(plan, x, Wg, Wu, Wd, 0.1, ws=ws).clone()
+        y_fresh = cats.cats_mlp_decode(plan, x, Wg, Wu, Wd, 0.1, ws=plan.workspace())
+        if "compaction" in opts:  # Alg. 1: append order varies run to run (reading R15)
+            assert float((y_shared - y_fresh).norm() / y_fresh.norm()) < 1e-6, b
+        else:
+            assert torch.equal(y_shared, y_fresh), b
+        if i % 2 == 0:
+            cats.cats_mlp_gate_act(plan, x, Wg, ws=ws)
