@@ -163,7 +163,7 @@ def test_parity_every_planned_batch(model, b):
 
 
 @pytest.mark.parametrize("d,m", [(5120, 1003), (5120, 77), (5120, 8), (8192, 512)])
-@pytest.mark.parametrize("b", [6, 8])
+@pytest.mark.parametrize("b", [4, 6, 8])
 def test_parity_ka_column_parts_ragged(d, m, b):
     """KA in column parts (d = 5120, b >= 6: 8-row tiles, each job streamed as 5 stages of 1024 columns;
     d = 8192: 8 parts, two stages per stream next to 128 KB of x) on ragged and tiny layers: a last tile of
