@@ -25,6 +25,7 @@ ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--k", type=float, default=0.5)
 ap.add_argument("--dense", action="store_true")
 ap.add_argument("--json")
+ap.add_argument("--graph", action="store_true", help="trace a CUDA-graph replay of the step (no host launch gaps)")
 ap.add_argument("--m", type=int, default=0, help="override m (e.g. a TP shard)")
 ap.add_argument("--opt", action="append", default=[], help="plan option key=value, repeatable")
 ap.add_argument("--lib", default="", help="library file name in the package directory (A/B)")
@@ -59,8 +60,21 @@ def step(i):
 for i in range(20):
     step(i)
 torch.cuda.synchronize()
+if a.graph:  # the traced step as a graph replay: the kernels' launches carry no host latency between them
+    side = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        step(20)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=side):
+            step(20)
+    g.replay()
+    torch.cuda.synchronize()
 ws[off.value:off.value + nbytes.value].zero_()
-step(20)
+if a.graph:
+    g.replay()
+else:
+    step(20)
 torch.cuda.synchronize()
 tr = ws[off.value:off.value + nbytes.value].cpu().numpy().view(np.uint64).reshape(3, 512, 8).astype(np.int64)
 rep = {}
