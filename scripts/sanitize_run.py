@@ -39,6 +39,21 @@ ws2 = p2.workspace()
 for b in (1, 4):
     cats.cats_mlp_decode(p2, cats_synth.tokens(b, d2, torch.bfloat16).to(dev), *W2, 0.05, ws=ws2)
 acts = cats.cats_mlp_gate_act(p2, cats_synth.tokens(4, d2, torch.bfloat16).to(dev), W2[0], ws=ws2)
+# KA in column parts (d = 5120, b >= 6: 8-row tiles, 1024-column stages), ragged m
+p3 = cats.MlpPlan(d2, 1003, max_batch=8)
+W3 = [w.to(dev) for w in cats_synth.mlp_weights(d2, 1003, torch.bfloat16)]
+ws3 = p3.workspace()
+for b in (6, 8):
+    cats.cats_mlp_decode(p3, cats_synth.tokens(b, d2, torch.bfloat16).to(dev), *W3, 0.05, ws=ws3)
+    cats.cats_mlp_last_active(p3, ws3, b)
+# bound host call (graph: x staging kernel + decode kernels), K12 and the split path
+hp = cats.MlpPlan(d, m, max_batch=2)
+hws = hp.workspace()
+for b in (1, 2):
+    xh = cats_synth.tokens(b, d, torch.bfloat16).pin_memory()
+    call = cats.BoundDecodeHost(hp, xh, Wg, Wu, Wd, 0.05, ws=hws)
+    for _ in range(3):
+        call()
 print("wide ok", flush=True)
 # App. B input-sparse projection
 xp = cats.XsparsePlan(512, 768, max_batch=8)
