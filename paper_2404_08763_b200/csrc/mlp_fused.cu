@@ -41,6 +41,10 @@
 //
 // Workspace outputs for introspection: tile tau's cnt[tau] active neurons are written ascending at
 // positions [tau*NR, tau*NR + cnt[tau]) of idx / tokmask / vals (v in fp32, 0 where |v| < t).
+//
+// The App. D ablation modes (Alg. 2 mask-predicated loads, Alg. 1 atomic appends + list launch; DESIGN.md
+// §5.9) are a separate instantiation of the same kernel (template flag ABL), so the product kernel
+// carries none of their branches.
 #include "cats_device.cuh"
 #include "cats_internal.h"
 
