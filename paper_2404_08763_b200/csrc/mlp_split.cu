@@ -86,6 +86,26 @@ __device__ __forceinline__ void ldsm_x4(uint32_t saddr, uint32_t &r0, uint32_t &
                  : "memory");
 }
 
+// tensor memory: columns to allocate (a power of two >= 32), and 16-column (x16) stores / loads of one warp's
+// 32 lanes (lane quarter = warp % 4 of the CTA), 32-bit per column
+constexpr uint32_t tmem_cols_c(int n) { return n <= 32 ? 32u : n <= 64 ? 64u : n <= 128 ? 128u : n <= 256 ? 256u : 512u; }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                 "%13, %14, %15, %16};" ::"r"(taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+                 "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                 "%14, %15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(taddr)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void claim_async(unsigned int &t, unsigned int *ctr, bool pred) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p atom.global.add.u32 %0, [%1], 1;\n\t}"
                  : "+r"(t)
@@ -132,7 +152,8 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
     // shared memory: x, then per group: ring, barriers, descriptors, FIFO, partial sums
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char *xs = smem;  // x: [B][d] (dot-product path) or [B][d + 8] (tensor-core path, padded rows)
-    unsigned char *ring0 = xs + (size_t)B * (KS > 0 ? row_bytes + 16u : row_bytes);       // [NG][stages][stage]
+    // (KS == 3 keeps x in tensor memory, not here)
+    unsigned char *ring0 = xs + (KS == 3 ? (size_t)0 : (size_t)B * (KS > 0 ? row_bytes + 16u : row_bytes));  // [NG][stages][stage]
     uint64_t *full0 = reinterpret_cast<uint64_t *>(ring0 + (size_t)NG * stages * stage_bytes);  // [NG][stages]
     uint64_t *empty0 = full0 + NG * stages;                                               // [NG][stages]
     Desc *desc0 = reinterpret_cast<Desc *>(empty0 + NG * stages);                         // [NG][stages]
@@ -478,7 +499,7 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
             __syncwarp();
             ++retire;
             if (++rs == stages) { rs = 0; rphase ^= 1u; }
-            if constexpr (KS == 1) {
+            if constexpr (KS == 1 || KS == 3) {
                 while (!ended && prod < retire + stages && issue_job()) {
                 }
             }
@@ -539,7 +560,75 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
         int s = 0;
         uint32_t phase = 0;
         unsigned long long c_wait = 0;
-        if constexpr (KS > 0) {
+        if constexpr (KS == 3) {
+            // ---- tensor cores with x in TENSOR MEMORY: warp w's A fragments (x rows = tokens, its k-steps
+            //      [w spw, (w + 1) spw)) are written once into TMEM columns of the warp's lane quarter and
+            //      re-read per stage with tcgen05.ld, so no x lives in shared memory (the ring gets that
+            //      space: three 4-row stages per job stream at b = 8) and no ldmatrix of x competes with
+            //      the stage reads. The warps of both groups that own the same k-steps share columns. ----
+            __shared__ uint32_t s_tmem;
+            const int nsteps = d / 16, spw = nsteps / NWG;  // a multiple of 8: d % 1024 == 0 (split_ka_ks)
+            const uint32_t tcols = tmem_cols_c(4 * spw);
+            if (warp == 0) {
+                asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                             "r"(tcols));
+                asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            consumer_barrier<NC>();
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int g4 = lane >> 2, t4 = lane & 3;
+            // lane quarter = warp % 4; within it, cwarp 0-3 and 4-7 own different k-steps (column blocks)
+            const uint32_t taddr = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((cwarp >> 2) * 2 * spw);
+            if (g == 0) {  // fill: column 2j = a0, 2j + 1 = a2 of k-step j (A row = token g4, or token 0)
+                const uint32_t *xw = reinterpret_cast<const uint32_t *>(x) + (size_t)(g4 < B ? g4 : 0) * (d / 2);
+                for (int j0 = 0; j0 < spw; j0 += 8) {
+                    uint32_t r[16];
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) {
+                        const int kk = (cwarp * spw + j0 + jj) * 16;
+                        r[2 * jj] = __ldg(xw + (kk >> 1) + t4);
+                        r[2 * jj + 1] = __ldg(xw + ((kk + 8) >> 1) + t4);
+                    }
+                    tmem_st16(taddr + (uint32_t)(2 * j0), r);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            consumer_barrier<NC>();
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t koff = (uint32_t)(lane >> 3) * 16u + (uint32_t)(cwarp * spw) * 32u;
+            const uint32_t brow = (uint32_t)((lane & 7) % NR) * rs_bytes + koff;
+            for (;;) {
+                const unsigned long long cw0 = trace ? gtimer() : 0ull;
+                mbar_wait(&full[s], phase);
+                if (trace) c_wait += gtimer() - cw0;
+                if (desc[s].type == kSJobEnd) break;
+                const uint32_t sb = smem_u32(ring + (size_t)s * stage_bytes) + brow;
+                float dacc[4] = {0.f, 0.f, 0.f, 0.f}, dacc2[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int j0 = 0; j0 < spw; j0 += 8) {  // 8 k-steps (16 TMEM columns) per load
+                    uint32_t a[16];
+                    tmem_ld16(taddr + (uint32_t)(2 * j0), a);
+#pragma unroll
+                    for (int jj = 0; jj < 8; jj += 2) {
+                        uint32_t b0, b1, b2, b3;
+                        ldsm_x4(sb + (uint32_t)(j0 + jj) * 32u, b0, b1, b2, b3);
+                        mma_bf16_16816(dacc, a[2 * jj], a[2 * jj], a[2 * jj + 1], a[2 * jj + 1], b0, b1);
+                        mma_bf16_16816(dacc2, a[2 * jj + 2], a[2 * jj + 2], a[2 * jj + 3], a[2 * jj + 3], b2, b3);
+                    }
+                }
+                float *rb = red + ((size_t)s * NWG + cwarp) * PP;
+                if (g4 < B && 2 * t4 < NR) rb[(2 * t4) * B + g4] = dacc[0] + dacc2[0];
+                if (g4 < B && 2 * t4 + 1 < NR) rb[(2 * t4 + 1) * B + g4] = dacc[1] + dacc2[1];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                if (++s == stages) { s = 0; phase ^= 1u; }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            consumer_barrier<NC>();
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(tcols));
+        } else if constexpr (KS > 0) {
             // ---- tensor-core dot products (bf16): D[16 x 8] += A[16 x 16] B[16 x 8] per 16-wide k-step,
             //      A = x (rows = tokens; rows >= b repeat token 0 and are ignored), B = W^T (columns =
             //      the job's NR rows; the other 8 - NR columns repeat them and are ignored). Warp w of the
@@ -1023,8 +1112,11 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
 // Measured (Llama2-7B): the MMA path wins from b = 4 (b = 8: KA 58 -> 38 us); at b = 2 its ldmatrix
 // traffic (x re-read per job, half the B columns duplicated) makes it slower than FHFMA.
 // 2 = MMA in column parts (ka_colsplit: 8-row tiles, jobs of d / kKaPartCols stages)
+// 3 = MMA with x in tensor memory (d % 1024 == 0: each warp's k-steps come in whole 8-step TMEM loads)
 int split_ka_ks(const PlanData &p, int b) {
-    return ka_colsplit(p, b) ? 2 : (p.esize == 2 && b >= kSplitMmaMinB) ? 1 : 0;
+    if (ka_colsplit(p, b)) return 2;
+    if (p.esize == 2 && b >= kSplitMmaMinB) return p.d % 1024 == 0 && p.d <= 8192 ? 3 : 1;
+    return 0;
 }
 static size_t ka_stage_row_bytes(const PlanData &p, int b) {  // bytes of one row in a ring stage (unpadded)
     return (size_t)(ka_colsplit(p, b) ? kKaPartCols : p.d) * p.esize;
@@ -1054,7 +1146,8 @@ static size_t split_ka_per_stage(const PlanData &p, int b) {
 size_t split_ka_smem(const PlanData &p, int b, int stages) {
     const size_t ent = (2 + (size_t)b) * 4;  // sizeof(SplitFifoEntry<b>)
     const size_t desc = (4 + 2 * (size_t)split_rows_per_tile(p, b) + (size_t)split_rows_per_tile(p, b) * b) * 4;
-    const size_t xs = (size_t)b * ((size_t)p.d * p.esize + (split_ka_ks(p, b) > 0 ? 16 : 0));
+    const int ks = split_ka_ks(p, b);
+    const size_t xs = ks == 3 ? 0 : (size_t)b * ((size_t)p.d * p.esize + (ks > 0 ? 16 : 0));
     // column parts: one more descriptor per group (the job being streamed part by part)
     const size_t fifo = split_ka_ks(p, b) == 2 ? kSplitFifoCs : kSplitFifo;
     return xs + kSplitAGroups * ((size_t)stages * split_ka_per_stage(p, b) + fifo * ent +
@@ -1186,8 +1279,11 @@ static cudaError_t launch_split_b(const PlanData &p, const void *x, const void *
     const int ks = split_ka_ks(p, B);
     if constexpr (sizeof(T) == 2 && B >= kSplitMmaMinB) {
         e = ks == 2 ? launch_ka<T, B, 8, 2>(p, x, Wg, Wu, t, mode, ws, s)
-            : k12_rows_per_tile(p, B) == 4 ? launch_ka<T, B, 4, 1>(p, x, Wg, Wu, t, mode, ws, s)
-                                           : launch_ka<T, B, 2, 1>(p, x, Wg, Wu, t, mode, ws, s);
+            : k12_rows_per_tile(p, B) == 4
+                ? (ks == 3 ? launch_ka<T, B, 4, 3>(p, x, Wg, Wu, t, mode, ws, s)
+                           : launch_ka<T, B, 4, 1>(p, x, Wg, Wu, t, mode, ws, s))
+                : (ks == 3 ? launch_ka<T, B, 2, 3>(p, x, Wg, Wu, t, mode, ws, s)
+                           : launch_ka<T, B, 2, 1>(p, x, Wg, Wu, t, mode, ws, s));
     } else {
         const int nr = k12_rows_per_tile(p, B);
         if constexpr (B == 1) {  // b = 1 on large layers tiles by 6 rows (the split path at b = 1: options)
