@@ -133,6 +133,11 @@ constexpr int kSplitMmaMinB = 4;  // batches from which KA / KB use warp-level b
 // next to x, the 8-row partial buffers and the larger FIFO only 3 stages of 16.5 KB fit per stream
 // (ncu: shared-memory wavefronts 54 -> 25 % of peak, but DRAM 4.1 -> 3.4 TB/s, consumers waiting on data).
 constexpr int kKaPartCols = 1024;
+// KA keeps x in tensor memory on its tensor-core path where each warp's k-steps come in whole 8-step
+// TMEM loads (d % 1024 == 0) -- then x takes no shared memory (split_ka_stages_nr, split_ka_smem)
+inline bool ka_x_in_tmem(const PlanData &p, int b) {
+    return p.esize == 2 && b >= kSplitMmaMinB && p.d % 1024 == 0 && p.d <= 8192;
+}
 inline bool ka_colsplit(const PlanData &p, int b) {
     return p.esize == 2 && b >= kSplitMmaMinB && p.d % kKaPartCols == 0 && split_ka_stages_nr(p, b, 4) < 2;
 }

@@ -1115,7 +1115,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
 // 3 = MMA with x in tensor memory (d % 1024 == 0: each warp's k-steps come in whole 8-step TMEM loads)
 int split_ka_ks(const PlanData &p, int b) {
     if (ka_colsplit(p, b)) return 2;
-    if (p.esize == 2 && b >= kSplitMmaMinB) return p.d % 1024 == 0 && p.d <= 8192 ? 3 : 1;
+    if (p.esize == 2 && b >= kSplitMmaMinB) return ka_x_in_tmem(p, b) ? 3 : 1;
     return 0;
 }
 static size_t ka_stage_row_bytes(const PlanData &p, int b) {  // bytes of one row in a ring stage (unpadded)
@@ -1132,7 +1132,8 @@ static size_t split_ka_per_stage_nr(const PlanData &p, int b, int nr) {
 // KA ring stages per group with tiles of nr rows (used by k12_rows_per_tile to pick nr at b >= 2)
 int split_ka_stages_nr(const PlanData &p, int b, int nr) {
     const size_t ent = (2 + (size_t)b) * 4;
-    const size_t xs = (size_t)b * ((size_t)p.d * p.esize + ((p.esize == 2 && b >= kSplitMmaMinB) ? 16 : 0));
+    const size_t xs = ka_x_in_tmem(p, b) ? 0
+                      : (size_t)b * ((size_t)p.d * p.esize + ((p.esize == 2 && b >= kSplitMmaMinB) ? 16 : 0));
     const size_t fixed = xs + kSplitAGroups * kSplitFifo * ent;
     if (fixed >= kSmemBudget) return 0;
     return (int)std::min<size_t>((kSmemBudget - fixed) / (kSplitAGroups * split_ka_per_stage_nr(p, b, nr)), kMaxStages);
