@@ -1279,12 +1279,19 @@ static cudaError_t launch_split_b(const PlanData &p, const void *x, const void *
     cudaError_t e;
     const int ks = split_ka_ks(p, B);
     if constexpr (sizeof(T) == 2 && B >= kSplitMmaMinB) {
-        e = ks == 2 ? launch_ka<T, B, 8, 2>(p, x, Wg, Wu, t, mode, ws, s)
-            : k12_rows_per_tile(p, B) == 4
-                ? (ks == 3 ? launch_ka<T, B, 4, 3>(p, x, Wg, Wu, t, mode, ws, s)
-                           : launch_ka<T, B, 4, 1>(p, x, Wg, Wu, t, mode, ws, s))
-                : (ks == 3 ? launch_ka<T, B, 2, 3>(p, x, Wg, Wu, t, mode, ws, s)
-                           : launch_ka<T, B, 2, 1>(p, x, Wg, Wu, t, mode, ws, s));
+        const int nr = split_rows_per_tile(p, B);
+        if (ks == 2) {
+            e = launch_ka<T, B, 8, 2>(p, x, Wg, Wu, t, mode, ws, s);
+        } else if (nr == 6) {
+            if constexpr (B <= 5) e = launch_ka<T, B, 6, 3>(p, x, Wg, Wu, t, mode, ws, s);
+            else e = cudaErrorInvalidValue;
+        } else if (nr == 4) {
+            e = ks == 3 ? launch_ka<T, B, 4, 3>(p, x, Wg, Wu, t, mode, ws, s)
+                        : launch_ka<T, B, 4, 1>(p, x, Wg, Wu, t, mode, ws, s);
+        } else {
+            e = ks == 3 ? launch_ka<T, B, 2, 3>(p, x, Wg, Wu, t, mode, ws, s)
+                        : launch_ka<T, B, 2, 1>(p, x, Wg, Wu, t, mode, ws, s);
+        }
     } else {
         const int nr = k12_rows_per_tile(p, B);
         if constexpr (B == 1) {  // b = 1 on large layers tiles by 6 rows (the split path at b = 1: options)
