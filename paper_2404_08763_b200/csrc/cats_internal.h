@@ -142,10 +142,10 @@ inline bool ka_colsplit(const PlanData &p, int b) {
     return p.esize == 2 && b >= kSplitMmaMinB && p.d % kKaPartCols == 0 && split_ka_stages_nr(p, b, 4) < 2;
 }
 // tile height of the split path (KA's tiles, KB's per-tile masks)
-// 6-row tiles on the x-in-TMEM path at b = 4, 5 (6 of the 8 B-operand columns distinct, a third fewer jobs;
-// 6 b <= 32 (row, token) pairs: one per producer lane) where two such stages fit per job stream
+// 6-row tiles on the x-in-TMEM path (6 of the 8 B-operand columns distinct, a third fewer jobs than 4-row
+// tiles) where two such stages fit per job stream
 inline bool ka_nr6(const PlanData &p, int b) {
-    return ka_x_in_tmem(p, b) && !ka_colsplit(p, b) && b <= 5 && p.nr_force == 0 && split_ka_stages_nr(p, b, 6) >= 2;
+    return ka_x_in_tmem(p, b) && !ka_colsplit(p, b) && p.nr_force == 0 && split_ka_stages_nr(p, b, 6) >= 2;
 }
 inline int split_rows_per_tile(const PlanData &p, int b) {
     return ka_colsplit(p, b) ? 8 : ka_nr6(p, b) ? 6 : k12_rows_per_tile(p, b);

@@ -129,9 +129,11 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
     constexpr int NP = NR * B;          // (row, token) dot products per job
     constexpr int PP = pow2_ceil(NP);   // padded to a power of two for the reduce-scatter
     constexpr bool CS = KS == 2;        // tensor cores in column parts (ka_colsplit)
-    constexpr int NS = CS ? (NP + 31) / 32 : 1;  // (row, token) pairs per producer lane
+    constexpr bool MP = CS || NP > 32;  // two (row, token) pairs per producer lane (8-row / 6-row tiles at b > 5)
+    constexpr int NS = MP ? (NP + 31) / 32 : 1;  // (row, token) pairs per producer lane
     constexpr int FIFO = CS ? kSplitFifoCs : kSplitFifo;
-    static_assert(CS ? (NR == 8 && PP <= 64) : PP <= 32, "one or two (row, token) pairs per lane");
+    static_assert(MP ? PP <= 64 : PP <= 32, "one or two (row, token) pairs per lane");
+    static_assert(!CS || NR == 8, "column parts use 8-row tiles");
     constexpr uint32_t TKM = (1u << B) - 1u;
     using Desc = SplitDesc<NR, B>;
     using Ent = SplitFifoEntry<B>;
@@ -404,10 +406,11 @@ ka_gate_up(const T *__restrict__ x, const T *__restrict__ Wg, const T *__restric
             const Desc &D = desc[rs];
             if (trace) { if (D.type == kSJobGate) ++n_gate; else ++n_up; }
             const int n = D.n;
-            if constexpr (CS) {
+            if constexpr (MP) {
                 // column parts: the consumers accumulate across a job's H stages and publish the warp
-                // partials with the last part; earlier parts only free their stage
-                if (D.part == H - 1) {
+                // partials with the last part; earlier parts only free their stage. Also the retire of
+                // tiles with more (row, token) pairs than lanes (two per lane).
+                if (!CS || D.part == H - 1) {
                     float u[NS];
                     bool ok[NS];
 #pragma unroll
@@ -1283,8 +1286,7 @@ static cudaError_t launch_split_b(const PlanData &p, const void *x, const void *
         if (ks == 2) {
             e = launch_ka<T, B, 8, 2>(p, x, Wg, Wu, t, mode, ws, s);
         } else if (nr == 6) {
-            if constexpr (B <= 5) e = launch_ka<T, B, 6, 3>(p, x, Wg, Wu, t, mode, ws, s);
-            else e = cudaErrorInvalidValue;
+            e = launch_ka<T, B, 6, 3>(p, x, Wg, Wu, t, mode, ws, s);
         } else if (nr == 4) {
             e = ks == 3 ? launch_ka<T, B, 4, 3>(p, x, Wg, Wu, t, mode, ws, s)
                         : launch_ka<T, B, 4, 1>(p, x, Wg, Wu, t, mode, ws, s);
