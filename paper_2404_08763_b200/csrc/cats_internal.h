@@ -143,9 +143,12 @@ inline bool ka_colsplit(const PlanData &p, int b) {
 }
 // tile height of the split path (KA's tiles, KB's per-tile masks)
 // 6-row tiles on the x-in-TMEM path (6 of the 8 B-operand columns distinct, a third fewer jobs than 4-row
-// tiles) where two such stages fit per job stream
+// tiles) where two such stages fit per job stream; on the CUDA-core path (b = 2, 3) of large bf16 layers
+// likewise (K12's b = 1 shape: fewer, larger jobs where the per-job chain bounds the rate)
 inline bool ka_nr6(const PlanData &p, int b) {
-    return ka_x_in_tmem(p, b) && !ka_colsplit(p, b) && p.nr_force == 0 && split_ka_stages_nr(p, b, 6) >= 2;
+    if (p.nr_force != 0 || ka_colsplit(p, b)) return false;
+    if (ka_x_in_tmem(p, b)) return split_ka_stages_nr(p, b, 6) >= 2;
+    return p.esize == 2 && b >= 2 && b < kSplitMmaMinB && p.m >= 8192 && split_ka_stages_nr(p, b, 6) >= 2;
 }
 inline int split_rows_per_tile(const PlanData &p, int b) {
     return ka_colsplit(p, b) ? 8 : ka_nr6(p, b) ? 6 : k12_rows_per_tile(p, b);

@@ -1295,13 +1295,15 @@ static cudaError_t launch_split_b(const PlanData &p, const void *x, const void *
                         : launch_ka<T, B, 2, 1>(p, x, Wg, Wu, t, mode, ws, s);
         }
     } else {
-        const int nr = k12_rows_per_tile(p, B);
-        if constexpr (B == 1) {  // b = 1 on large layers tiles by 6 rows (the split path at b = 1: options)
+        const int nr = split_rows_per_tile(p, B);
+        // 6-row tiles: b = 1 on large layers (the split path at b = 1: options), bf16 b = 2, 3 (ka_nr6)
+        constexpr bool kNr6 = B == 1 || (sizeof(T) == 2 && B < kSplitMmaMinB);
+        if constexpr (kNr6) {
             if (nr == 6) e = launch_ka<T, B, 6, 0>(p, x, Wg, Wu, t, mode, ws, s);
         }
         if (nr != 6) e = nr == 4 ? launch_ka<T, B, 4, 0>(p, x, Wg, Wu, t, mode, ws, s)
                                  : launch_ka<T, B, 2, 0>(p, x, Wg, Wu, t, mode, ws, s);
-        else if (B != 1) e = cudaErrorInvalidValue;
+        else if (!kNr6) e = cudaErrorInvalidValue;
     }
     if (e != cudaSuccess) return e;
     if (ev_mid) {

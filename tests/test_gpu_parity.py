@@ -162,12 +162,14 @@ def test_parity_every_planned_batch(model, b):
     assert res["kernels"] == 2
 
 
-@pytest.mark.parametrize("d,m", [(5120, 1003), (5120, 77), (5120, 8), (8192, 512)])
+@pytest.mark.parametrize("d,m", [(5120, 1003), (5120, 77), (5120, 8), (8192, 512), (4096, 1003), (4096, 77),
+                                 (4096, 8)])
 @pytest.mark.parametrize("b", [4, 6, 8])
 def test_parity_ka_column_parts_ragged(d, m, b):
     """KA in column parts (d = 5120, b >= 6: 8-row tiles, each job streamed as 5 stages of 1024 columns;
-    d = 8192: 8 parts, two stages per stream next to 128 KB of x) on ragged and tiny layers: a last tile of
-    3 rows, fewer tiles than job streams, one tile."""
+    d = 8192: 8 parts, two stages per stream next to 128 KB of x) and KA's 6-row tiles with x in tensor
+    memory (d = 4096, b >= 4; two (row, token) pairs per producer lane from b = 6) on ragged and tiny
+    layers: a last tile of 1-5 rows, fewer tiles than job streams, one tile."""
     res, _ = run_parity(d, m, b, torch.bfloat16, 0.5, seed=90 + m + b)
     assert res["kernels"] == 2
 
