@@ -930,7 +930,10 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
             for (int jn = 0; jn < njobs; ++jn) {
                 const int s = jn % stages;
                 mbar_wait(&full[s], (uint32_t)(jn / stages) & 1u);
-                const int r0 = jn * rows_per_stage, nrow = min(rows_per_stage, len - r0);
+                const int rs0 = jn * rows_per_stage, nrs = min(rows_per_stage, len - rs0);
+                // one 16-neuron MMA k-step per 16 rows of the stage (rows_per_stage = 16 or 32)
+                for (int k0 = 0; k0 < nrs; k0 += 16) {
+                const int r0 = rs0 + k0, nrow = min(16, nrs - k0);
                 // B fragments: x1 of neurons 2 t4, 2 t4 + 1 (b0) and 2 t4 + 8, + 9 (b1), token g4
                 uint32_t bh[2], bl[2];
 #pragma unroll
@@ -950,7 +953,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
                 // A: lane -> neuron row r8 + 8 (mat / 2) (rows past nrow repeat row 0: finite, x1 = 0),
                 //    columns + 8 (mat % 2)
                 const int arow = r8 + 8 * (mat >> 1);
-                const uint32_t abase = smem_u32(ring + (size_t)s * stage_bytes) + (uint32_t)(arow < nrow ? arow : 0) * sst +
+                const uint32_t abase = smem_u32(ring + (size_t)s * stage_bytes) + (uint32_t)(k0 + (arow < nrow ? arow : 0)) * sst +
                                        (uint32_t)(col0 + 8 * (mat & 1)) * 2u;
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
@@ -958,6 +961,7 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
                     ldsm_x4_trans(abase + (uint32_t)mt * 32u, a0, a1, a2, a3);
                     mma_bf16_16816(dacc[mt], a0, a1, a2, a3, bh[0], bh[1]);
                     mma_bf16_16816(dacc[mt], a0, a1, a2, a3, bl[0], bl[1]);
+                }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
@@ -1162,23 +1166,27 @@ int split_ka_stages(const PlanData &p, int b) {
     if (fixed >= kSmemBudget) return 0;
     return (int)std::min<size_t>((kSmemBudget - fixed) / (kSplitAGroups * split_ka_per_stage(p, b)), kMaxStages);
 }
-static int split_kb_rows_per_stage(const PlanData &p, int b) {
-    if (split_kb_mma(p, b)) return 16;  // one 16-neuron MMA k-step per stage
-    const size_t seg = (size_t)split_part_cols(p, b) * p.esize;
-    return (int)std::max<size_t>(1, std::min<size_t>(32, (32 * 1024) / seg));
-}
 static int split_kb_maxr(const PlanData &p, int b) {  // the largest (first) tapered range, + rounding
     const long long R = split_ranges(p, b);
     const long long wtot = R * (4 * R + 1) - R * (R - 1) / 2;
     return (int)(((long long)p.m * 4 * R + wtot - 1) / wtot) + 2;
 }
+static size_t split_kb_fixed_smem(const PlanData &p, int b) {  // everything but the ring's stages
+    const int ntiles = split_ntiles(p, b), maxr = split_kb_maxr(p, b);
+    return (size_t)(ntiles + 1 + 32) * 4 + (size_t)maxr * 8 + (size_t)maxr * b * 4 + (size_t)ntiles;
+}
+static int split_kb_rows_per_stage(const PlanData &p, int b) {
+    if (split_kb_mma(p, b)) {  // 16-neuron MMA k-steps: two per stage where 3 such stages fit, else one
+        const size_t seg = (size_t)split_part_cols(p, b) * p.esize + 16;
+        return 3 * (32 * seg + 16) + split_kb_fixed_smem(p, b) <= kSmemBudget ? 32 : 16;
+    }
+    const size_t seg = (size_t)split_part_cols(p, b) * p.esize;
+    return (int)std::max<size_t>(1, std::min<size_t>(32, (32 * 1024) / seg));
+}
 size_t split_kb_smem(const PlanData &p, int b, int stages) {
     const size_t seg = (size_t)split_part_cols(p, b) * p.esize + 16;  // padded rows
     const size_t stage = (size_t)split_kb_rows_per_stage(p, b) * seg;
-    const int ntiles = split_ntiles(p, b);
-    const int maxr = split_kb_maxr(p, b);
-    return (size_t)stages * stage + (size_t)stages * 16 + (size_t)(ntiles + 1 + 32) * 4 + (size_t)maxr * 8 +
-           (size_t)maxr * b * 4 + (size_t)ntiles;
+    return (size_t)stages * stage + (size_t)stages * 16 + split_kb_fixed_smem(p, b);
 }
 int split_kb_stages(const PlanData &p, int b) {
     const size_t seg = (size_t)split_part_cols(p, b) * p.esize + 16;  // padded rows
