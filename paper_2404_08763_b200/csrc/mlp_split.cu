@@ -1176,12 +1176,15 @@ static size_t split_kb_fixed_smem(const PlanData &p, int b) {  // everything but
     return (size_t)(ntiles + 1 + 32) * 4 + (size_t)maxr * 8 + (size_t)maxr * b * 4 + (size_t)ntiles;
 }
 static int split_kb_rows_per_stage(const PlanData &p, int b) {
+    // (rows per stage <= 32: one bulk copy per producer lane)
     if (split_kb_mma(p, b)) {  // 16-neuron MMA k-steps: two per stage where 3 such stages fit, else one
         const size_t seg = (size_t)split_part_cols(p, b) * p.esize + 16;
         return 3 * (32 * seg + 16) + split_kb_fixed_smem(p, b) <= kSmemBudget ? 32 : 16;
     }
+    // CUDA cores: ~32 KB stages; ~64 KB at b = 1 (KB runs at b = 1 only for d >= 5120: Llama2-13B and
+    // its TP shards, 51.4 / 16.9 vs 52.3 / 17.2 us; at b = 2 the larger stages measured 0.1-0.6 us slower)
     const size_t seg = (size_t)split_part_cols(p, b) * p.esize;
-    return (int)std::max<size_t>(1, std::min<size_t>(32, (32 * 1024) / seg));
+    return (int)std::max<size_t>(1, std::min<size_t>(32, ((b == 1 ? 64 : 32) * 1024) / seg));
 }
 size_t split_kb_smem(const PlanData &p, int b, int stages) {
     const size_t seg = (size_t)split_part_cols(p, b) * p.esize + 16;  // padded rows
