@@ -785,12 +785,14 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     unsigned char *ring = smem;                                                               // [stages][stage]
     uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * stage_bytes);       // [stages]
     uint64_t *empty = full + stages;                                                          // [stages]
-    int *pre = reinterpret_cast<int *>(empty + stages);                                       // [ntiles + 1]
+    // x1 of the range (8-byte aligned): fp32 [maxr][B], or on the MMA path bf16x2 hi + lo per neuron pair
+    float *lx = reinterpret_cast<float *>(empty + stages);
+    const int lxn = MT > 0 ? (maxr + 15) / 16 * 16 * B : maxr * B;
+    int *pre = reinterpret_cast<int *>(lx + lxn);                                             // [ntiles + 1]
     int *wsum = pre + ntiles + 1;                                                             // [32]
     int *lj = wsum + 32;                                                                      // [maxr]
     int *lpos = lj + maxr;                                                                    // [maxr]
-    float *lx = reinterpret_cast<float *>(lpos + maxr);                                       // [maxr][B]
-    uint8_t *rowm = reinterpret_cast<uint8_t *>(lx + (size_t)maxr * B);                       // [ntiles]
+    uint8_t *rowm = reinterpret_cast<uint8_t *>(lpos + maxr);                                 // [ntiles]
     __shared__ int s_rr;
 
     trace_stamp(trace, 1, 0);
@@ -912,7 +914,24 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
     } else {
         // ---- consumers: y[tk][c] += x1[j][tk] * W_down[j][c] over the range, list order, fp32 ----
         pdl_wait_primary();  // x1 comes from KA's UP jobs: KA must have completed
-        for (int i = tid; i < len * B; i += NCt) lx[i] = __ldcg(x1in + (size_t)lpos[i / B] * B + (i % B));
+        if constexpr (MT > 0) {
+            // the MMA B operand, built once per CTA instead of once per warp and k-step: per neuron pair
+            // (2 i, 2 i + 1) and token, the bf16x2 hi and lo parts of x1 (zero past the range, up to the
+            // next 16-neuron k-step)
+            uint2 *lxp = reinterpret_cast<uint2 *>(lx);
+            const int npair = ((len + 15) / 16) * 8;
+            for (int i = tid; i < npair * B; i += NCt) {
+                const int pr = i / B, tk = i % B, r = 2 * pr;
+                const float v0 = r < len ? __ldcg(x1in + (size_t)lpos[r] * B + tk) : 0.f;
+                const float v1 = r + 1 < len ? __ldcg(x1in + (size_t)lpos[r + 1] * B + tk) : 0.f;
+                const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
+                const float2 hf = __bfloat1622float2(hi);
+                const __nv_bfloat162 lo = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
+                lxp[i] = make_uint2(*reinterpret_cast<const uint32_t *>(&hi), *reinterpret_cast<const uint32_t *>(&lo));
+            }
+        } else {
+            for (int i = tid; i < len * B; i += NCt) lx[i] = __ldcg(x1in + (size_t)lpos[i / B] * B + (i % B));
+        }
         asm volatile("bar.sync 1, %0;" ::"r"(NCt) : "memory");  // consumers only
         if constexpr (MT > 0) {
             // ---- tensor cores (bf16): D[16 cols x 8 tokens] += A[16 cols x 16 neurons] B[16 neurons x 8]
@@ -934,21 +953,15 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
                 // one 16-neuron MMA k-step per 16 rows of the stage (rows_per_stage = 16 or 32)
                 for (int k0 = 0; k0 < nrs; k0 += 16) {
                 const int r0 = rs0 + k0, nrow = min(16, nrs - k0);
-                // B fragments: x1 of neurons 2 t4, 2 t4 + 1 (b0) and 2 t4 + 8, + 9 (b1), token g4
+                // B fragments: x1 of neurons 2 t4, 2 t4 + 1 (b0) and 2 t4 + 8, + 9 (b1), token g4, as the
+                // precomputed bf16 hi + lo pairs (|x1 - hi - lo| <= 2^-16 |x1|)
                 uint32_t bh[2], bl[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    float v[2];
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int rr2 = 2 * t4 + 8 * h + e;
-                        v[e] = (g4 < B && rr2 < nrow) ? lx[(size_t)(r0 + rr2) * B + g4] : 0.f;
-                    }
-                    const __nv_bfloat162 hi = __floats2bfloat162_rn(v[0], v[1]);
-                    const float2 hf = __bfloat1622float2(hi);
-                    const __nv_bfloat162 lo = __floats2bfloat162_rn(v[0] - hf.x, v[1] - hf.y);
-                    bh[h] = *reinterpret_cast<const uint32_t *>(&hi);
-                    bl[h] = *reinterpret_cast<const uint32_t *>(&lo);
+                    const uint2 v = g4 < B ? reinterpret_cast<const uint2 *>(lx)[(size_t)((r0 >> 1) + 4 * h + t4) * B + g4]
+                                           : make_uint2(0u, 0u);
+                    bh[h] = v.x;
+                    bl[h] = v.y;
                 }
                 // A: lane -> neuron row r8 + 8 (mat / 2) (rows past nrow repeat row 0: finite, x1 = 0),
                 //    columns + 8 (mat % 2)
@@ -1173,7 +1186,9 @@ static int split_kb_maxr(const PlanData &p, int b) {  // the largest (first) tap
 }
 static size_t split_kb_fixed_smem(const PlanData &p, int b) {  // everything but the ring's stages
     const int ntiles = split_ntiles(p, b), maxr = split_kb_maxr(p, b);
-    return (size_t)(ntiles + 1 + 32) * 4 + (size_t)maxr * 8 + (size_t)maxr * b * 4 + (size_t)ntiles;
+    // x1 of the range: fp32 [maxr][b], or (MMA path) bf16x2 hi + lo per neuron pair up to a whole k-step
+    const size_t lx = split_kb_mma(p, b) ? (size_t)((maxr + 15) / 16) * 16 * b * 4 : (size_t)maxr * b * 4;
+    return (size_t)(ntiles + 1 + 32) * 4 + (size_t)maxr * 8 + lx + (size_t)ntiles;
 }
 static int split_kb_rows_per_stage(const PlanData &p, int b) {
     // (rows per stage <= 32: one bulk copy per producer lane)
