@@ -122,7 +122,7 @@ struct SplitFifoEntry {  // one active neuron waiting for its UP job
 };
 
 // KB on tensor cores (bf16, d a multiple of 1024: 4 column parts of 16-column tiles over 16 warps)
-constexpr int kSplitMmaMinB = 4;  // batches from which KA / KB use warp-level bf16 MMA (measured crossover)
+constexpr int kSplitMmaMinB = 3;  // batches from which KA / KB use warp-level bf16 MMA (measured crossover, DESIGN 5.2)
 // KA's tensor-core path in column parts (bf16, b >= kSplitMmaMinB, d a multiple of kKaPartCols): tiles of
 // 8 rows -- all 8 columns of the m16n8k16 B operand distinct rows -- and every GATE / UP job streamed as
 // d / kKaPartCols consecutive ring stages of 8 rows x kKaPartCols columns, the consumers accumulating in

@@ -13,10 +13,10 @@
 //    staged once in shared memory and TWO independent job streams per CTA (each: a producer warp, a
 //    ring, 8 consumer warps -- one producer per SM was the bottleneck). Jobs are GATE(tile of NR
 //    W_gate rows) and UP(<= NR active neurons' W_up rows, gathered across tiles from a FIFO). Every
-//    job is the same consumer work, NR x b dot products, in one of two engines: b <= 3 FHFMA.BF16
+//    job is the same consumer work, NR x b dot products, in one of two engines: b <= 2 FHFMA.BF16
 //    (fma.rn.f32.bf16 on the packed registers) + one warp reduce-scatter (NR*b - 1 shuffles);
-//    b >= 4 warp-level mma.sync m16n8k16 bf16 -> fp32 (x = A, the job's rows = B, both via ldmatrix
-//    from 16-byte-padded rows). The producer sums the group's 8 warp partials in fixed order and
+//    b >= 3 (bf16) warp-level mma.sync m16n8k16 bf16 -> fp32 (x = A, the job's rows = B; x from
+//    tensor memory where d % 1024 == 0, else ldmatrix from 16-byte-padded rows). The producer sums the group's 8 warp partials in fixed order and
 //    turns GATE results into u -> v = SiLU(u) -> keep = |v| >= t -> ballot compaction (idx / tokmask /
 //    vals / cnt, the same per-tile layout as K12, plus one mask word per tile for KB) and UP results
 //    into x1 = (x W_up[j]) * v_j (Optimization 1), written per compact position.
@@ -24,7 +24,7 @@
 //  * KB (down, static): starts from KA's per-tile mask words while KA drains; the compact active list
 //    (prefix-summed in every CTA) is cut into R equal ranges; CTA (r, q) streams the W_down rows of
 //    range r, column part q, accumulates y_r = sum_j x1_j W_down[j] in fp32 in list order (CUDA
-//    cores for b <= 3; for b >= 4 MMA with W_down^T via ldmatrix.trans and x1 as exact bf16 hi + lo),
+//    cores for b <= 2; for b >= 3 MMA with W_down^T via ldmatrix.trans and x1 as exact bf16 hi + lo),
 //    writes the partial; the last 64 CTAs to finish (no grid barrier) each sum a slice of the R partials in
 //    fixed order r = 0..R-1 into y: the deterministic two-phase split-K reduction of the north star. The
 //    tapered ranges balance the data-dependent work.
@@ -1130,7 +1130,9 @@ kb_down(const T *__restrict__ Wd, int d, int ntiles, int nr_tile, int Q, int R, 
 // ================================================================================== host side
 // KA dot-product engine: 1 = warp-level bf16 MMA (bf16 weights, b >= kSplitMmaMinB), 0 = FHFMA.BF16 / FFMA.
 // Measured (Llama2-7B): the MMA path wins from b = 4 (b = 8: KA 58 -> 38 us); at b = 2 its ldmatrix
-// traffic (x re-read per job, half the B columns duplicated) makes it slower than FHFMA.
+// traffic (x re-read per job, half the B columns duplicated) made it slower than FHFMA. With x in tensor
+// memory it wins from b = 3 (Llama2-7B 47.9 vs 52.4 us, Mistral 58.8 vs 63.6, Llama2-13B 69.6 vs 73.7;
+// b = 2 still 0.1-1.2 us slower, A/B on one box).
 // 2 = MMA in column parts (ka_colsplit: 8-row tiles, jobs of d / kKaPartCols stages)
 // 3 = MMA with x in tensor memory (d % 1024 == 0: each warp's k-steps come in whole 8-step TMEM loads)
 int split_ka_ks(const PlanData &p, int b) {

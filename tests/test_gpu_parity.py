@@ -149,9 +149,10 @@ def test_parity_full_size(model, b, k, heavy):
 
 
 # Every kernel instantiation the planner selects for the BASELINE shapes: per model,
-# b = 1 -> K12 (NR = 6 at d = 4096, NR = 4 at d = 5120); b = 2, 3 -> KA + KB on CUDA cores; b = 4..8 ->
-# KA + KB on bf16 MMA (KB MT = 4 at d = 4096, MT = 5 at d = 5120; KA in column parts with 8-row tiles at
-# d = 5120 from b = 6). The batch is a template parameter, so each (model, b) is a distinct kernel pair.
+# b = 1 -> K12 at d = 4096, KA + KB at d = 5120; b = 2 -> KA + KB on CUDA cores (6-row tiles at d = 4096);
+# b = 3..8 -> KA + KB on bf16 MMA with x in tensor memory (6-row tiles at d = 4096, 4-row at d = 5120; KB
+# MT = 4 at d = 4096, MT = 5 at d = 5120). The batch is a template parameter, so each (model, b) is a
+# distinct kernel pair.
 @pytest.mark.parametrize("model", ["mistral-7b", "llama2-7b", "llama2-13b"])
 @pytest.mark.parametrize("b", [2, 3, 4, 5, 6, 7, 8])
 def test_parity_every_planned_batch(model, b):
