@@ -239,12 +239,12 @@ cats_status_t cats_mlp_workspace_init(const cats_mlp_plan_t *plan, void *ws, siz
 
 /* y[b][d] = CATS_t gated MLP of x[b][d] over this plan's m neurons (under tensor parallelism y
  * is the rank's partial; the caller all-reduces). t >= 0; t = 0 gives dense semantics.
- * b = 1: ONE kernel launch on s (K12), a persistent dataflow kernel doing the gate GEMV, SiLU,
- * threshold, compaction, sparse up x v, down projection and the split-K reduction (TMA bulk-reduce
- * of exact fixed-point partials; the last CTA writes y).
- * b >= 2: TWO launches (KA: gate + up with compaction; KB: down projection over balanced ranges of
- * the active list + a fixed-order two-phase reduction); b >= 4 uses warp-level bf16 MMA for the
- * dot products. cats_mlp_kernels_per_call() tells which. All launches use programmatic dependent
+ * b = 1 (d <= 4096): ONE kernel launch on s (K12), a persistent dataflow kernel doing the gate GEMV,
+ * SiLU, threshold, compaction, sparse up x v, down projection and the split-K reduction (TMA
+ * bulk-reduce of exact fixed-point partials; the last CTA writes y).
+ * b >= 2, and b = 1 at d >= 5120: TWO launches (KA: gate + up with compaction; KB: down projection
+ * over balanced ranges of the active list + a fixed-order two-phase reduction); bf16 at b >= 3 uses
+ * warp-level bf16 MMA for the dot products (KA's x operand held in tensor memory where d % 1024 == 0). cats_mlp_kernels_per_call() tells which. All launches use programmatic dependent
  * launch (a successor's CTAs start streaming weights while the predecessor drains).
  * KB has no grid barrier: the last 64 of its CTAs to finish do the fixed-order reduction while the
  * others exit, so it completes whenever more than 64 of its CTAs (one per SM) can be resident at once;
