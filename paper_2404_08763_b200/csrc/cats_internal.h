@@ -122,6 +122,9 @@ struct SplitFifoEntry {  // one active neuron waiting for its UP job
 };
 
 // KB on tensor cores (bf16, d a multiple of 1024: 4 column parts of 16-column tiles over 16 warps)
+// KB's tensor-core path from b = 2 (A/B: Llama2-13B b = 2 62.1 vs 64.3 us, its TP4 shard 25.4 vs 26.6,
+// Llama2-7B 44.7 vs 44.9, Mistral 53.1 vs 53.3), KA's from b = 3 (below)
+constexpr int kSplitKbMmaMinB = 2;
 constexpr int kSplitMmaMinB = 3;  // batches from which KA / KB use warp-level bf16 MMA (measured crossover, DESIGN 5.2)
 // KA's tensor-core path in column parts (bf16, b >= kSplitMmaMinB, d a multiple of kKaPartCols): tiles of
 // 8 rows -- all 8 columns of the m16n8k16 B operand distinct rows -- and every GATE / UP job streamed as
@@ -157,7 +160,7 @@ inline int split_ntiles(const PlanData &p, int b) {
     return (p.m + split_rows_per_tile(p, b) - 1) / split_rows_per_tile(p, b);
 }
 inline bool split_kb_mma(const PlanData &p, int b) {  // instantiated for 1, 4, 5 tiles per warp
-    return b >= kSplitMmaMinB && p.esize == 2 && (p.d == 1024 || p.d == 4096 || p.d == 5120);
+    return b >= kSplitKbMmaMinB && p.esize == 2 && (p.d == 1024 || p.d == 4096 || p.d == 5120);
 }
 // scheduler words at the workspace base: [0..1] tile counter / CTA exits, [2] KB arrival tickets,
 // [3] App. D Alg. 1 append counter, [4] K12 accumulator parity, [5] tokens the last K12 call left in the

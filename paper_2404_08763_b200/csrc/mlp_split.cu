@@ -1294,7 +1294,7 @@ static cudaError_t launch_kb(const PlanData &p, const void *Wd, float *y, void *
 template <typename T, int B>
 static cudaError_t launch_kb_b(const PlanData &p, const void *Wd, float *y, void *ws, cudaStream_t s) {
     constexpr int EPT = 4;  // = split_ept()
-    if constexpr (sizeof(T) == 2 && B >= kSplitMmaMinB) {
+    if constexpr (sizeof(T) == 2 && B >= kSplitKbMmaMinB) {
         const int mt = split_kb_mt(p, B);
         if (mt == 1) return launch_kb<T, B, EPT, 1>(p, Wd, y, ws, s);
         if (mt == 4) return launch_kb<T, B, EPT, 4>(p, Wd, y, ws, s);
