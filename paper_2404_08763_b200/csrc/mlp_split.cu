@@ -24,7 +24,8 @@
 //  * KB (down, static): starts from KA's per-tile mask words while KA drains; the compact active list
 //    (prefix-summed in every CTA) is cut into R equal ranges; CTA (r, q) streams the W_down rows of
 //    range r, column part q, accumulates y_r = sum_j x1_j W_down[j] in fp32 in list order (CUDA
-//    cores for b <= 2; for b >= 3 MMA with W_down^T via ldmatrix.trans and x1 as exact bf16 hi + lo),
+//    cores at b = 1 and for fp32; bf16 from b = 2 MMA with W_down^T via ldmatrix.trans and x1 as exact
+//    bf16 hi + lo),
 //    writes the partial; the last 64 CTAs to finish (no grid barrier) each sum a slice of the R partials in
 //    fixed order r = 0..R-1 into y: the deterministic two-phase split-K reduction of the north star. The
 //    tapered ranges balance the data-dependent work.
